@@ -1,0 +1,142 @@
+/*
+ * bastion.h — C ABI of the B200-native BASTION draft→expand→verify→accept engine.
+ *
+ * Every entry point takes caller-owned DEVICE buffers (plain pointers + sizes)
+ * and an explicit CUDA stream, never allocates on the hot path, and returns an
+ * int status (0 = ok, <0 = error; text via bst_last_error()).  No torch types.
+ *
+ * Each function replaces one reference (``specplan``, Python) interface; the
+ * reference file:line is cited beside it (paths relative to
+ * /root/reference/pkg/src/specplan).  INTEGRATION.md shows the ctypes binding a
+ * maintainer adds on the reference side.
+ */
+#ifndef BASTION_H_
+#define BASTION_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* bst_stream_t; /* cudaStream_t; NULL = legacy default stream */
+
+#define BST_OK 0
+#define BST_EINVAL (-1) /* argument error   -> ValueError in the Python shim   */
+#define BST_ECUDA (-2)  /* CUDA error        -> RuntimeError                    */
+#define BST_ECAP (-3)   /* internal capacity exceeded (caller retries bigger)   */
+
+int bst_abi_version(void);
+const char* bst_last_error(void);
+
+/* ------------------------------------------------------------------------
+ * Latency curve at a fixed context c.
+ * Replaces LatencyCurve (cost_model.py:284-309): exact integer coefficients,
+ * reciprocal multiplies, variant factors slope/intercept/ratio.
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int64_t flops_lin, flops_quad;             /* cost_model.py:290-291 */
+  int64_t bytes_const, bytes_lin, bytes_quad; /* cost_model.py:292-294 */
+  double inv_peak, inv_bw;                   /* cost_model.py:295-296 */
+  double slope, intercept, ratio;            /* cost_model.py:297-303 */
+} bst_curve_t;
+
+/* Host-side evaluation of LatencyCurve.latency(s) with the device arithmetic. */
+double bst_curve_latency(const bst_curve_t* curve, int64_t s);
+
+/* ------------------------------------------------------------------------
+ * K1 — top-K candidate lattice.
+ * bst_topk_logits replaces the drafter plugin's softmax + MarginalBlock rows
+ * (lattice.py:24-55) fused with top_k_truncate (lattice.py:128-142):
+ *   m = max_v l, Z = sum_v exp64(l_v - m), prob_v = exp64(l_v - m) / Z,
+ *   keep the k best by (prob desc, token asc).
+ * logits: [gamma, row_stride] fp32 (dtype 0) or bf16 (dtype 1).
+ * probs_full (nullable): fp64 [gamma, vocab] full rows, bit-identical to the
+ * lattice probabilities (the MarginalBlock a reference plugin would return).
+ * bst_topk_probs replaces top_k_truncate on an fp64 MarginalBlock.
+ * ---------------------------------------------------------------------- */
+size_t bst_topk_workspace(int gamma, int vocab, int k);
+int bst_topk_logits(const void* logits, int dtype, int gamma, int vocab, int64_t row_stride, int k,
+                    int32_t* tok, double* prob, double* probs_full, void* ws, size_t ws_bytes,
+                    bst_stream_t stream);
+int bst_topk_probs(const double* probs, int gamma, int vocab, int k, int32_t* tok, double* prob,
+                   void* ws, size_t ws_bytes, bst_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K2 — tree expansion.
+ * policy ADAPTIVE replaces run_cycle (controller.py:56-107) incl. the
+ * LatencyCurve evaluation; FIXED replaces best_first_expand
+ * (draft_tree.py:138-155) over ExpansionFrontier/iter_best_first
+ * (draft_tree.py:69-135); BEAM replaces beam_expand (draft_tree.py:158-189),
+ * greedy chain = BEAM width 1 depth gamma (verify_sim.py:419-420).
+ * ---------------------------------------------------------------------- */
+enum { BST_POLICY_ADAPTIVE = 0, BST_POLICY_FIXED = 1, BST_POLICY_BEAM = 2 };
+enum { BST_STOP_FIRST_DECREASE = 0, BST_STOP_FRONTIER_EXHAUSTED = 1, BST_STOP_BUDGET_CAP = 2 };
+enum { BST_ALGO_AUTO = 0, BST_ALGO_SORT = 1, BST_ALGO_HEAP = 2 };
+
+typedef struct {
+  int32_t policy;   /* BST_POLICY_* */
+  int32_t n_max;    /* ControllerConfig.n_max / best_first n_max */
+  int32_t width;    /* beam width */
+  int32_t depth;    /* beam depth */
+  int32_t algo;     /* BST_ALGO_*: sort-based parallel (default) or sequential heap */
+  int32_t _pad;
+  bst_curve_t curve; /* adaptive only */
+  double fixed_cost; /* t_draft + t_aux, controller.py:73 */
+  double l_ar;       /* CycleLatencies.l_ar */
+} bst_plan_t;
+
+/* Output arrays (device), row 0 = root.  Capacity n_cap+1 rows. */
+typedef struct {
+  int32_t* parent;      /* [n_cap+1] root -1 */
+  int32_t* depth;       /* [n_cap+1] */
+  int32_t* token;       /* [n_cap+1] root -1 */
+  int32_t* rank;        /* [n_cap+1] lattice rank, root -1 */
+  double* rho;          /* [n_cap+1] path scores, root 1.0 */
+  double* trace;        /* [n_cap] S_hat per expanded node (adaptive), nullable */
+  int32_t* meta;        /* [8]: 0 n_nodes, 1 n_expanded, 2 stop, 3 algo used, 4 enumerated */
+  double* surrogate;    /* [1] */
+  uint32_t* anc_mask;   /* [(n_cap+1) * mask_words] ancestor-or-self bits, nullable */
+  int32_t mask_words;   /* u32 words per mask row (>= ceil((n_cap+1)/32)) */
+  int32_t _pad;
+  int32_t* child_start; /* [n_cap+2] children CSR offsets, nullable */
+  int32_t* child_list;  /* [n_cap] */
+} bst_tree_t;
+
+size_t bst_expand_workspace(int gamma, int k, int n_cap);
+int bst_expand(const int32_t* tok, const double* prob, int gamma, int k, const bst_plan_t* plan,
+               int n_cap, const bst_tree_t* out, void* ws, size_t ws_bytes, bst_stream_t stream);
+
+/* Dense (prefix_len + t)^2 byte mask of linearize (verify_sim.py:336-355) from
+ * the ancestor bitmask: prefix columns 1 for every row, tree block = ancestors. */
+int bst_linearize_mask(const uint32_t* anc_mask, int mask_words, int t, int prefix_len, uint8_t* mask,
+                       bst_stream_t stream);
+
+/* Ancestor-or-self bitmask of an explicit tree (parent[0] = -1, parent[i] < i),
+ * for trees built on the host (build_tree, draft_tree.py:204-236).          */
+int bst_ancestor_mask(const int32_t* parent, int t, int mask_words, uint32_t* mask, bst_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K6 — greedy acceptance walk + KV compaction.
+ * bst_accept replaces verify_tree (verify_sim.py:358-389) + commit
+ * (verify_sim.py:392-405) given the target's greedy token per tree row:
+ * out: path[max_path] node ids (root 0 first), meta[0] = accepted_len (incl.
+ * root), meta[1] = bonus token, meta[2] = number of committed tokens.
+ * committed[] receives accepted draft tokens then the bonus (commit order).
+ * ---------------------------------------------------------------------- */
+int bst_accept(const int32_t* token, const int32_t* child_start, const int32_t* child_list,
+               const int32_t* argmax, int max_path, int32_t* path, int32_t* committed, int32_t* meta,
+               bst_stream_t stream);
+
+/* Paged KV cache: layout [layer][page][2 (K,V)][n_kv][page_size][head_dim] bf16.
+ * Moves slot c+path[i] -> c+i for i < meta[0] in every layer (race-free:
+ * each CTA owns one (layer, K/V, head) slice and stages rows in smem).   */
+int bst_kv_compact(void* kv, int n_layers, int n_kv, int head_dim, int page_size, int64_t layer_stride_elems,
+                   const int32_t* page_table, const int32_t* c_dev, const int32_t* path, const int32_t* meta,
+                   int max_path, bst_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BASTION_H_ */

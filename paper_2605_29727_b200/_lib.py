@@ -1,0 +1,87 @@
+"""ctypes binding of libbastion.so (the C ABI in include/bastion.h).
+
+The library is the product path: if it is missing, or no CUDA device is
+present, every compute entry point raises — there is no CPU fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = Path(os.environ.get("BASTION_LIB", PKG / "libbastion.so"))
+
+BST_OK, BST_EINVAL, BST_ECUDA, BST_ECAP = 0, -1, -2, -3
+POLICY_ADAPTIVE, POLICY_FIXED, POLICY_BEAM = 0, 1, 2
+ALGO_AUTO, ALGO_SORT, ALGO_HEAP = 0, 1, 2
+STOP_NAMES = {0: "first-decrease", 1: "frontier-exhausted", 2: "budget-cap"}
+
+
+class Curve(C.Structure):
+    """bst_curve_t — LatencyCurve coefficients (cost_model.py:287-303)."""
+
+    _fields_ = [("flops_lin", C.c_int64), ("flops_quad", C.c_int64), ("bytes_const", C.c_int64),
+                ("bytes_lin", C.c_int64), ("bytes_quad", C.c_int64), ("inv_peak", C.c_double),
+                ("inv_bw", C.c_double), ("slope", C.c_double), ("intercept", C.c_double), ("ratio", C.c_double)]
+
+
+class Plan(C.Structure):
+    _fields_ = [("policy", C.c_int32), ("n_max", C.c_int32), ("width", C.c_int32), ("depth", C.c_int32),
+                ("algo", C.c_int32), ("_pad", C.c_int32), ("curve", Curve), ("fixed_cost", C.c_double),
+                ("l_ar", C.c_double)]
+
+
+class Tree(C.Structure):
+    _fields_ = [("parent", C.c_void_p), ("depth", C.c_void_p), ("token", C.c_void_p), ("rank", C.c_void_p),
+                ("rho", C.c_void_p), ("trace", C.c_void_p), ("meta", C.c_void_p), ("surrogate", C.c_void_p),
+                ("anc_mask", C.c_void_p), ("mask_words", C.c_int32), ("_pad", C.c_int32),
+                ("child_start", C.c_void_p), ("child_list", C.c_void_p)]
+
+
+_P, _I, _I64, _SZ, _D = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
+SIGNATURES = {
+    "bst_abi_version": (C.c_int, []),
+    "bst_last_error": (C.c_char_p, []),
+    "bst_curve_latency": (_D, [C.POINTER(Curve), _I64]),
+    "bst_topk_workspace": (_SZ, [_I, _I, _I]),
+    "bst_topk_logits": (_I, [_P, _I, _I, _I, _I64, _I, _P, _P, _P, _P, _SZ, _P]),
+    "bst_topk_probs": (_I, [_P, _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "bst_expand_workspace": (_SZ, [_I, _I, _I]),
+    "bst_expand": (_I, [_P, _P, _I, _I, C.POINTER(Plan), _I, C.POINTER(Tree), _P, _SZ, _P]),
+    "bst_linearize_mask": (_I, [_P, _I, _I, _I, _P, _P]),
+    "bst_ancestor_mask": (_I, [_P, _I, _I, _P, _P]),
+    "bst_accept": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "bst_kv_compact": (_I, [_P, _I, _I, _I, _I, _I64, _P, _P, _P, _P, _I, _P]),
+}
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Load libbastion.so once; raise loudly if it is missing."""
+    global _lib
+    if _lib is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(f"libbastion.so not built at {LIB_PATH}; run __graft_entry__.build()")
+        handle = C.CDLL(str(LIB_PATH))
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(handle, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc == BST_OK:
+        return
+    msg = (lib().bst_last_error() or b"").decode(errors="replace")
+    if rc == BST_EINVAL:
+        raise ValueError(msg)
+    raise RuntimeError(f"bastion error {rc}: {msg}")
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))

@@ -1,0 +1,70 @@
+// Shared helpers for the bastion C-ABI library (sm_100a).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "../../include/bastion.h"
+
+namespace bst {
+
+void set_error(const char* fmt, ...);
+
+#define BST_REQUIRE(cond, ...)          \
+  do {                                  \
+    if (!(cond)) {                      \
+      ::bst::set_error(__VA_ARGS__);    \
+      return BST_EINVAL;                \
+    }                                   \
+  } while (0)
+
+#define BST_CUDA(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess) {                                                           \
+      ::bst::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(e_)); \
+      return BST_ECUDA;                                                                \
+    }                                                                                  \
+  } while (0)
+
+#define BST_LAUNCH_CHECK() BST_CUDA(cudaGetLastError())
+
+inline cudaStream_t as_stream(bst_stream_t s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Positive doubles order like their bit patterns.
+__device__ __forceinline__ unsigned long long dbits(double x) {
+  return static_cast<unsigned long long>(__double_as_longlong(x));
+}
+__device__ __forceinline__ double bitsd(unsigned long long b) {
+  return __longlong_as_double(static_cast<long long>(b));
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// LatencyCurve.latency (cost_model.py:305-309) with round-to-nearest and no
+// contraction, matching Python's int->float conversion and float arithmetic.
+__host__ __device__ inline double curve_latency(const bst_curve_t& c, long long s) {
+  long long f = (c.flops_lin + c.flops_quad * s) * s;
+  long long b = c.bytes_const + (c.bytes_lin + c.bytes_quad * s) * s;
+#ifdef __CUDA_ARCH__
+  double compute = __dmul_rn(__ll2double_rn(f), c.inv_peak);
+  double memory = __dmul_rn(__ll2double_rn(b), c.inv_bw);
+  double raw = compute > memory ? compute : memory;
+  return __dmul_rn(c.ratio, __dadd_rn(__dmul_rn(c.slope, raw), c.intercept));
+#else
+  volatile double compute = (double)f * c.inv_peak;
+  volatile double memory = (double)b * c.inv_bw;
+  double raw = compute > memory ? compute : memory;
+  volatile double t = c.slope * raw;
+  volatile double u = t + c.intercept;
+  return c.ratio * u;
+#endif
+}
+
+}  // namespace bst

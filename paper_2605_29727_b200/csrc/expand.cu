@@ -1,0 +1,686 @@
+// K2 — best-first / adaptive / beam tree expansion on one CTA.
+//
+// Replaces ExpansionFrontier + iter_best_first + best_first_expand
+// (draft_tree.py:69-155), run_cycle (controller.py:56-107, incl.
+// LatencyCurve.latency cost_model.py:305-309) and beam_expand
+// (draft_tree.py:158-189).
+//
+// Best-first without a heap.  The reference pops nodes in increasing key
+// (-rho, depth, token, parent_pop_index); a node's parent and previous sibling
+// always have a strictly smaller key, so the lazy child/sibling heap pops the
+// GLOBAL key order of all positive-rho lattice nodes.  We therefore:
+//   1. estimate a threshold tau with a log-bin histogram DP over the lattice
+//      (conservative: at least min(n_max, reachable) nodes have rho >= tau);
+//   2. enumerate {rho >= tau} level by level (prefix-closed, exact fp64 rho =
+//      rho_parent * p as in draft_tree.py:102,113);
+//   3. bitonic-sort by (-rho, depth, token, enumeration index) and repair the
+//      rare exact ties of (rho, depth, token) by the parent's final position,
+//      depth by depth;
+//   4. run Algorithm 1's S_hat scan: sequential fp64 a_hat (one thread, same
+//      addition order as controller.py:85), parallel S_hat, first strict
+//      decrease via a block prefix-max.
+// If the enumeration would exceed the shared-memory capacity (pathological
+// ties / flat rows) the same kernel falls back to the reference's sequential
+// lazy heap on thread 0 — still exact, just slower.
+// Compiled with -fmad=false; every fp64 op below is also explicitly _rn.
+#include "common.cuh"
+
+namespace bst {
+
+constexpr int EX_THREADS = 1024;
+constexpr int EX_WARPS = EX_THREADS / 32;
+constexpr int EX_CAP = 8192;   // enumerated-node capacity of the sort path
+constexpr int EX_BINS = 4096;  // histogram bins of the threshold DP
+constexpr int EX_MAXG = 127;
+constexpr int EX_MAXK = 128;
+constexpr unsigned short NO_PARENT = 0xFFFF;
+
+struct HeapEntry {
+  double rho;
+  unsigned long long lo;  // depth<<44 | token<<20 | parent
+  int rank;
+  int _pad;
+};
+
+__device__ __forceinline__ bool heap_less(const HeapEntry& a, const HeapEntry& b) {
+  // smaller key pops first: rho desc, then (depth, token, parent) asc
+  return a.rho > b.rho || (a.rho == b.rho && a.lo < b.lo);
+}
+
+// ---------------------------------------------------------------- block scans
+__device__ int block_excl_scan(int v, int* sh, int* total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int t = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    sh[lane] = t;
+  }
+  __syncthreads();
+  int before = (w > 0) ? sh[w - 1] : 0;
+  *total = sh[EX_WARPS - 1];
+  __syncthreads();
+  return before + x - v;
+}
+
+// exclusive prefix-max of doubles (identity -inf)
+__device__ double block_excl_max(double v, double* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    double y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x = fmax(x, y);
+  }
+  double excl_in_warp = __shfl_up_sync(0xffffffffu, x, 1);
+  if (lane == 0) excl_in_warp = -INFINITY;
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    double t = sh[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      double y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t = fmax(t, y);
+    }
+    sh[lane] = t;
+  }
+  __syncthreads();
+  double before = (w > 0) ? sh[w - 1] : -INFINITY;
+  __syncthreads();
+  return fmax(before, excl_in_warp);
+}
+
+// ------------------------------------------------------------ shared layout
+struct ExSmem {
+  unsigned long long hi[EX_CAP];  // ~rho bits (ascending = rho desc); DP aliases here
+  unsigned long long lo[EX_CAP];  // depth<<40 | token<<16 | idx
+  unsigned short par[EX_CAP];     // enumeration index of parent (NO_PARENT for depth 1)
+  unsigned short pos[EX_CAP];     // sorted position of each enumeration index
+  unsigned char rnk[EX_CAP];
+  unsigned short runs[EX_CAP / 2];
+  int lvl_start[EX_MAXG + 2];
+  int scan[EX_WARPS];
+  double dscan[EX_WARPS];
+  int n_runs, overflow, n_enum, all_enumerated, min_stop, best_idx, max_depth;
+  double best_val;
+  double tau;
+};
+
+struct ExWs {
+  double* ahat;     // [n_cap]
+  double* shat;     // [n_cap] (used when out->trace is null)
+  int* counts;      // [n_cap + 2]
+  HeapEntry* heap;  // [2 * n_cap + 4]
+};
+
+static size_t ex_align(size_t x) { return (x + 255) & ~size_t(255); }
+
+static ExWs ex_carve(void* ws, int n_cap, size_t* total) {
+  char* p = static_cast<char*>(ws);
+  ExWs w;
+  size_t off = 0;
+  w.ahat = reinterpret_cast<double*>(p + off);
+  off += ex_align(sizeof(double) * (n_cap + 1));
+  w.shat = reinterpret_cast<double*>(p + off);
+  off += ex_align(sizeof(double) * (n_cap + 1));
+  w.counts = reinterpret_cast<int*>(p + off);
+  off += ex_align(sizeof(int) * (n_cap + 2));
+  w.heap = reinterpret_cast<HeapEntry*>(p + off);
+  off += ex_align(sizeof(HeapEntry) * (2 * (size_t)n_cap + 4));
+  *total = off;
+  return w;
+}
+
+// --------------------------------------------------- threshold estimate (DP)
+// Returns tau such that #{lattice nodes with rho >= tau} >= min(n_max, reachable),
+// or 0.0 meaning "enumerate every positive node".
+__device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, ExSmem& sm) {
+  unsigned int* hprev = reinterpret_cast<unsigned int*>(sm.hi);
+  unsigned int* hcur = hprev + EX_BINS;
+  unsigned int* tot = hcur + EX_BINS;
+  const unsigned int SAT = 1u << 30;
+  __shared__ int s_bstar;
+  int* cost = reinterpret_cast<int*>(sm.lo);  // [gamma*k] quantized -log2(p), lo is free here
+  for (int pass = 0; pass < 2; ++pass) {
+    const double S = pass == 0 ? 16.0 : 2.0;
+    // est cost = floor(-log2(p) * S) + 1 >= the true scaled cost, so a path's
+    // summed est cost never undercounts: est <= B  =>  rho > 2^(-(B+1)/S).
+    for (int e = threadIdx.x; e < gamma * k; e += EX_THREADS) {
+      double p = __ldg(prob + e);
+      double c = p > 0.0 ? floor(-log2(p) * S) + 1.0 : -1.0;
+      cost[e] = c < 0.0 ? -1 : (c < EX_BINS ? (int)c : EX_BINS);
+    }
+    for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) { hprev[b] = 0; tot[b] = 0; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int r = 0; r < k; ++r)
+        if (cost[r] >= 0 && cost[r] < EX_BINS) hprev[cost[r]] += 1;
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) tot[b] = hprev[b];
+    __syncthreads();
+    for (int d = 2; d <= gamma; ++d) {
+      const int* cr = cost + (d - 1) * k;
+      for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) {
+        unsigned long long acc = 0;
+        for (int r = 0; r < k; ++r) {
+          const int ci = cr[r];
+          if (ci < 0) break;  // sorted desc: the rest are 0 as well
+          if (ci <= b) acc += hprev[b - ci];
+        }
+        hcur[b] = acc > SAT ? SAT : (unsigned int)acc;
+      }
+      __syncthreads();
+      for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) {
+        hprev[b] = hcur[b];
+        unsigned long long t = (unsigned long long)tot[b] + hcur[b];
+        tot[b] = t > SAT ? SAT : (unsigned int)t;
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      unsigned long long cum = 0;
+      int bstar = -1;
+      for (int b = 0; b < EX_BINS; ++b) {
+        cum += tot[b];
+        if (cum >= (unsigned long long)n_max) { bstar = b; break; }
+      }
+      s_bstar = bstar;
+    }
+    __syncthreads();
+    int bstar = s_bstar;
+    __syncthreads();
+    if (bstar >= 0) return exp2(-(double)(bstar + 1) / S);
+  }
+  return 0.0;
+}
+
+// ------------------------------------------------------------- enumeration
+// Enumerate every node with rho >= tau (rho > 0).  Returns false on overflow.
+__device__ bool enumerate_nodes(const int32_t* tok, const double* prob, int gamma, int k, double tau,
+                                ExSmem& sm) {
+  if (threadIdx.x == 0) { sm.n_enum = 0; sm.overflow = 0; sm.lvl_start[1] = 0; sm.max_depth = 0; }
+  __syncthreads();
+  int prev_lo = 0, prev_hi = 0;  // enumeration range of the previous level (root for d=1)
+  for (int d = 1; d <= gamma; ++d) {
+    const double* pr = prob + (size_t)(d - 1) * k;
+    const int32_t* tr = tok + (size_t)(d - 1) * k;
+    const int n_par = d == 1 ? 1 : prev_hi - prev_lo;
+    const int per = (n_par + EX_THREADS - 1) / EX_THREADS;
+    const int p0 = threadIdx.x * per;
+    int cnt = 0;
+    for (int q = 0; q < per; ++q) {
+      int pi = p0 + q;
+      if (pi >= n_par) break;
+      double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
+      for (int r = 0; r < k; ++r) {
+        double v = __dmul_rn(prho, __ldg(pr + r));
+        if (!(v > 0.0) || v < tau) break;
+        ++cnt;
+      }
+    }
+    int total;
+    int off = block_excl_scan(cnt, sm.scan, &total);
+    const int base = sm.n_enum;
+    if (base + total > EX_CAP) {
+      if (threadIdx.x == 0) sm.overflow = 1;
+      __syncthreads();
+      return false;
+    }
+    int w = base + off;
+    for (int q = 0; q < per; ++q) {
+      int pi = p0 + q;
+      if (pi >= n_par) break;
+      double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
+      for (int r = 0; r < k; ++r) {
+        double v = __dmul_rn(prho, __ldg(pr + r));
+        if (!(v > 0.0) || v < tau) break;
+        sm.hi[w] = ~dbits(v);
+        sm.lo[w] = ((unsigned long long)d << 40) | ((unsigned long long)(unsigned)__ldg(tr + r) << 16) |
+                   (unsigned long long)w;
+        sm.par[w] = d == 1 ? NO_PARENT : (unsigned short)(prev_lo + pi);
+        sm.rnk[w] = (unsigned char)r;
+        ++w;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      sm.n_enum = base + total;
+      sm.lvl_start[d + 1] = base + total;
+      if (total > 0) sm.max_depth = d;
+    }
+    __syncthreads();
+    if (total == 0) break;
+    prev_lo = base;
+    prev_hi = base + total;
+  }
+  return true;
+}
+
+__device__ __forceinline__ bool key_gt(unsigned long long ah, unsigned long long al, unsigned long long bh,
+                                       unsigned long long bl) {
+  return ah > bh || (ah == bh && al > bl);
+}
+
+__device__ void bitonic_sort(ExSmem& sm, int n) {
+  int p2 = 1;
+  while (p2 < n) p2 <<= 1;
+  for (int i = n + threadIdx.x; i < p2; i += EX_THREADS) { sm.hi[i] = ~0ull; sm.lo[i] = ~0ull; }
+  __syncthreads();
+  for (int kk = 2; kk <= p2; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < (p2 >> 1); i += EX_THREADS) {
+        int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+        int b = a + j;
+        bool asc = (a & kk) == 0;
+        unsigned long long ah = sm.hi[a], al = sm.lo[a], bh = sm.hi[b], bl = sm.lo[b];
+        if (key_gt(ah, al, bh, bl) == asc) {
+          sm.hi[a] = bh; sm.lo[a] = bl; sm.hi[b] = ah; sm.lo[b] = al;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// Repair exact (rho, depth, token) ties by the parent's final position.
+__device__ void fix_ties(ExSmem& sm, int n) {
+  for (int i = threadIdx.x; i < n; i += EX_THREADS) sm.pos[sm.lo[i] & 0xFFFF] = (unsigned short)i;
+  if (threadIdx.x == 0) sm.n_runs = 0;
+  __syncthreads();
+  for (int i = threadIdx.x; i + 1 < n; i += EX_THREADS) {
+    bool same_next = sm.hi[i] == sm.hi[i + 1] && (sm.lo[i] >> 16) == (sm.lo[i + 1] >> 16);
+    bool same_prev = i > 0 && sm.hi[i] == sm.hi[i - 1] && (sm.lo[i] >> 16) == (sm.lo[i - 1] >> 16);
+    if (same_next && !same_prev) {
+      int slot = atomicAdd(&sm.n_runs, 1);
+      if (slot < EX_CAP / 2) sm.runs[slot] = (unsigned short)i;
+    }
+  }
+  __syncthreads();
+  const int n_runs = min(sm.n_runs, EX_CAP / 2);
+  if (n_runs == 0) return;
+  for (int d = 2; d <= sm.max_depth; ++d) {
+    for (int q = threadIdx.x; q < n_runs; q += EX_THREADS) {
+      int s = sm.runs[q];
+      if ((int)(sm.lo[s] >> 40) != d) continue;
+      unsigned long long key = sm.lo[s] >> 16;
+      int e = s + 1;
+      while (e < n && sm.hi[e] == sm.hi[s] && (sm.lo[e] >> 16) == key) ++e;
+      // insertion sort of lo[s..e) by pos[par[idx]]
+      for (int a = s + 1; a < e; ++a) {
+        unsigned long long x = sm.lo[a];
+        int kx = sm.pos[sm.par[x & 0xFFFF]];
+        int b = a - 1;
+        while (b >= s && (int)sm.pos[sm.par[sm.lo[b] & 0xFFFF]] > kx) { sm.lo[b + 1] = sm.lo[b]; --b; }
+        sm.lo[b + 1] = x;
+      }
+      for (int a = s; a < e; ++a) sm.pos[sm.lo[a] & 0xFFFF] = (unsigned short)a;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------- sequential heap fallback
+// The reference's lazy frontier verbatim (draft_tree.py:79-135), on thread 0.
+__device__ int heap_expand(const int32_t* tok, const double* prob, int gamma, int k, int limit, HeapEntry* heap,
+                           const bst_tree_t& out) {
+  int n = 0, size = 0;
+  auto push = [&](double rho, int depth, int token, int parent, int rank) {
+    HeapEntry e;
+    e.rho = rho;
+    e.lo = ((unsigned long long)depth << 44) | ((unsigned long long)(unsigned)token << 20) | (unsigned)parent;
+    e.rank = rank;
+    int i = size++;
+    while (i > 0) {
+      int p = (i - 1) >> 1;
+      if (!heap_less(e, heap[p])) break;
+      heap[i] = heap[p];
+      i = p;
+    }
+    heap[i] = e;
+  };
+  if (k > 0 && prob[0] > 0.0) push(prob[0], 1, tok[0], 0, 0);
+  while (size > 0 && n < limit) {
+    HeapEntry top = heap[0];
+    HeapEntry last = heap[--size];
+    int i = 0;
+    while (true) {
+      int c = 2 * i + 1;
+      if (c >= size) break;
+      if (c + 1 < size && heap_less(heap[c + 1], heap[c])) ++c;
+      if (!heap_less(heap[c], last)) break;
+      heap[i] = heap[c];
+      i = c;
+    }
+    if (size > 0) heap[i] = last;
+    const int depth = (int)(top.lo >> 44);
+    const int token = (int)((top.lo >> 20) & 0xFFFFFF);
+    const int parent = (int)(top.lo & 0xFFFFF);
+    const int node = ++n;
+    out.parent[node] = parent;
+    out.depth[node] = depth;
+    out.token[node] = token;
+    out.rank[node] = top.rank;
+    out.rho[node] = top.rho;
+    if (depth < gamma) {  // rank-0 child, draft_tree.py:96-104
+      double c = __dmul_rn(top.rho, prob[(size_t)depth * k]);
+      if (c > 0.0) push(c, depth + 1, tok[(size_t)depth * k], node, 0);
+    }
+    if (top.rank + 1 < k) {  // next sibling, draft_tree.py:106-115
+      double prho = parent == 0 ? 1.0 : out.rho[parent];
+      double s = __dmul_rn(prho, prob[(size_t)(depth - 1) * k + top.rank + 1]);
+      if (s > 0.0) push(s, depth, tok[(size_t)(depth - 1) * k + top.rank + 1], parent, top.rank + 1);
+    }
+  }
+  return n;
+}
+
+// -------------------------------------------------------- post-processing
+// Writes the root row, Algorithm-1 stop logic (adaptive), surrogate, meta,
+// ancestor bitmask and children CSR for the first n_nodes rows.
+__device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive, int n_max, const bst_plan_t& plan,
+                            const bst_tree_t& out, const ExWs& ws, int algo_used, int enumerated, ExSmem& sm) {
+  if (threadIdx.x == 0) {
+    out.parent[0] = -1; out.depth[0] = 0; out.token[0] = -1; out.rank[0] = -1; out.rho[0] = 1.0;
+    double a = 1.0;
+    for (int i = 0; i < n_eval; ++i) {  // controller.py:85 / draft_tree.py:153 order
+      a = __dadd_rn(a, out.rho[i + 1]);
+      ws.ahat[i] = a;
+    }
+  }
+  __syncthreads();
+  int n_nodes = n_eval, n_expanded = n_eval, stop = -1;
+  if (adaptive && n_eval > 0) {
+    double* shat = out.trace ? out.trace : ws.shat;
+    for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
+      double c_hat = __dadd_rn(plan.fixed_cost, curve_latency(plan.curve, (long long)i + 2));
+      shat[i] = __ddiv_rn(__dmul_rn(ws.ahat[i], plan.l_ar), c_hat);
+    }
+    if (threadIdx.x == 0) { sm.min_stop = 0x7fffffff; }
+    __syncthreads();
+    // contiguous segment per thread -> exclusive prefix max -> first decrease
+    const int per = (n_eval + EX_THREADS - 1) / EX_THREADS;
+    const int s0 = threadIdx.x * per;
+    double local = -INFINITY;
+    for (int i = s0; i < min(s0 + per, n_eval); ++i) local = fmax(local, shat[i]);
+    double run = block_excl_max(local, sm.dscan);
+    for (int i = s0; i < min(s0 + per, n_eval); ++i) {
+      if (shat[i] < run) { atomicMin(&sm.min_stop, i); break; }
+      run = fmax(run, shat[i]);
+    }
+    __syncthreads();
+    const int stop_i = sm.min_stop;
+    if (stop_i != 0x7fffffff) {
+      n_expanded = stop_i + 1;
+      stop = BST_STOP_FIRST_DECREASE;
+    } else {
+      n_expanded = n_eval;
+      stop = n_eval >= n_max ? BST_STOP_BUDGET_CAP : BST_STOP_FRONTIER_EXHAUSTED;
+    }
+    // best_n = first index of the maximum over the considered prefix
+    if (threadIdx.x == 0) { sm.best_val = -INFINITY; sm.best_idx = 0x7fffffff; }
+    __syncthreads();
+    double bv = -INFINITY;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < n_expanded; i += EX_THREADS)
+      if (shat[i] > bv) { bv = shat[i]; bi = i; }
+    // reduce (max value, then min index)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    __shared__ double wv[EX_WARPS];
+    __shared__ int wi[EX_WARPS];
+    if ((threadIdx.x & 31) == 0) { wv[threadIdx.x >> 5] = bv; wi[threadIdx.x >> 5] = bi; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int w = 0; w < EX_WARPS; ++w)
+        if (wv[w] > sm.best_val || (wv[w] == sm.best_val && wi[w] < sm.best_idx)) {
+          sm.best_val = wv[w];
+          sm.best_idx = wi[w];
+        }
+    }
+    __syncthreads();
+    n_nodes = sm.best_idx + 1;
+  }
+  (void)is_fixed_or_adaptive;
+  if (threadIdx.x == 0) {
+    out.meta[0] = n_nodes;
+    out.meta[1] = n_expanded;
+    out.meta[2] = stop;
+    out.meta[3] = algo_used;
+    out.meta[4] = enumerated;
+    out.surrogate[0] = n_nodes > 0 ? ws.ahat[n_nodes - 1] : 1.0;
+  }
+  // ancestor-or-self bitmask rows 0..n_nodes
+  if (out.anc_mask) {
+    const int W = out.mask_words;
+    for (int i = threadIdx.x; i <= n_nodes; i += EX_THREADS) {
+      uint32_t* row = out.anc_mask + (size_t)i * W;
+      for (int w = 0; w < W; ++w) row[w] = 0u;
+      int j = i;
+      while (j >= 0) {
+        row[j >> 5] |= 1u << (j & 31);
+        j = j == 0 ? -1 : out.parent[j];
+      }
+    }
+  }
+  // children CSR
+  if (out.child_start && out.child_list) {
+    for (int i = threadIdx.x; i <= n_nodes + 1; i += EX_THREADS) ws.counts[i] = 0;
+    __syncthreads();
+    for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) atomicAdd(&ws.counts[out.parent[i]], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int acc = 0;
+      for (int i = 0; i <= n_nodes; ++i) {
+        int c = ws.counts[i];
+        out.child_start[i] = acc;
+        ws.counts[i] = acc;
+        acc += c;
+      }
+      out.child_start[n_nodes + 1] = acc;
+    }
+    __syncthreads();
+    for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) {
+      int slot = atomicAdd(&ws.counts[out.parent[i]], 1);
+      out.child_list[slot] = i;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(EX_THREADS, 1)
+    expand_best_first_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
+                             bst_plan_t plan, int n_cap, bst_tree_t out, ExWs ws, int heap_in_smem) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
+  const bool adaptive = plan.policy == BST_POLICY_ADAPTIVE;
+  const int n_max = plan.n_max;
+  const int limit = min(n_max, n_cap);
+  int n_eval = 0;
+  int algo_used = BST_ALGO_SORT;
+  bool ok = false;
+  int enumerated = 0;
+  if (plan.algo != BST_ALGO_HEAP) {
+    double tau = estimate_tau(prob, gamma, k, limit, sm);
+    __syncthreads();
+    ok = enumerate_nodes(tok, prob, gamma, k, tau > 0.0 ? tau : 4.9406564584124654e-324, sm);
+    if (ok) {
+      const int n = sm.n_enum;
+      enumerated = n;
+      bitonic_sort(sm, n);
+      fix_ties(sm, n);
+      n_eval = min(limit, n);
+      for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
+        unsigned long long lo = sm.lo[i];
+        int idx = (int)(lo & 0xFFFF);
+        unsigned short pe = sm.par[idx];
+        out.parent[i + 1] = pe == NO_PARENT ? 0 : (int)sm.pos[pe] + 1;
+        out.depth[i + 1] = (int)(lo >> 40);
+        out.token[i + 1] = (int)((lo >> 16) & 0xFFFFFF);
+        out.rank[i + 1] = (int)sm.rnk[idx];
+        out.rho[i + 1] = bitsd(~sm.hi[i]);
+      }
+    }
+  }
+  if (!ok) {
+    algo_used = BST_ALGO_HEAP;
+    __syncthreads();
+    __shared__ int s_n;
+    if (threadIdx.x == 0) {
+      HeapEntry* heap = heap_in_smem ? reinterpret_cast<HeapEntry*>(smem_raw) : ws.heap;
+      s_n = heap_expand(tok, prob, gamma, k, limit, heap, out);
+    }
+    __syncthreads();
+    n_eval = s_n;
+  }
+  __syncthreads();
+  finish_tree(n_eval, adaptive, true, n_max, plan, out, ws, algo_used, enumerated, sm);
+}
+
+// ------------------------------------------------------------------- beam
+// beam_expand (draft_tree.py:158-189): per level, candidates (rho_parent*p,
+// token, parent id) for every survivor x every lattice entry with rho > 0,
+// sorted by (-rho, token, parent); keep `width`; ids in level order.
+__global__ void __launch_bounds__(EX_THREADS, 1)
+    expand_beam_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
+                       bst_plan_t plan, int n_cap, bst_tree_t out, ExWs ws) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
+  __shared__ int s_next_id, s_surv_lo, s_surv_hi;
+  if (threadIdx.x == 0) {
+    s_next_id = 1;
+    s_surv_lo = 0;
+    s_surv_hi = 1;  // survivors = node ids [lo, hi); root = 0
+    out.rho[0] = 1.0;
+  }
+  __syncthreads();
+  for (int level = 1; level <= plan.depth; ++level) {
+    const int lo_id = s_surv_lo, hi_id = s_surv_hi;
+    const int n_surv = hi_id - lo_id;
+    const int n_cand = n_surv * k;
+    const double* pr = prob + (size_t)(level - 1) * k;
+    const int32_t* tr = tok + (size_t)(level - 1) * k;
+    // candidate c = (survivor c / k, rank c % k); invalid -> sentinel
+    int valid_local = 0;
+    for (int c = threadIdx.x; c < n_cand; c += EX_THREADS) {
+      int sid = lo_id + c / k, r = c % k;
+      double prho = out.rho[sid];
+      double v = __dmul_rn(prho, __ldg(pr + r));
+      if (v > 0.0) {
+        sm.hi[c] = ~dbits(v);
+        sm.lo[c] = ((unsigned long long)(unsigned)__ldg(tr + r) << 40) | ((unsigned long long)sid << 8) |
+                   (unsigned long long)r;
+        ++valid_local;
+      } else {
+        sm.hi[c] = ~0ull;
+        sm.lo[c] = ~0ull;
+      }
+    }
+    int n_valid;
+    block_excl_scan(valid_local, sm.scan, &n_valid);
+    if (n_valid == 0) break;
+    bitonic_sort(sm, n_cand);
+    const int take = min(plan.width, n_valid);
+    const int base = s_next_id;
+    for (int i = threadIdx.x; i < take; i += EX_THREADS) {
+      int id = base + i;
+      if (id <= n_cap) {
+        unsigned long long lo = sm.lo[i];
+        out.parent[id] = (int)((lo >> 8) & 0xFFFFFFFF);
+        out.depth[id] = level;
+        out.token[id] = (int)(lo >> 40);
+        out.rank[id] = (int)(lo & 0xFF);
+        out.rho[id] = bitsd(~sm.hi[i]);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      s_surv_lo = base;
+      s_surv_hi = base + take;
+      s_next_id = base + take;
+    }
+    __syncthreads();
+  }
+  const int n_nodes = min(s_next_id - 1, n_cap);
+  finish_tree(n_nodes, false, false, n_nodes, plan, out, ws, BST_ALGO_SORT, n_nodes, sm);
+  if (threadIdx.x == 0) out.meta[2] = -1;
+}
+
+}  // namespace bst
+
+extern "C" size_t bst_expand_workspace(int gamma, int k, int n_cap) {
+  (void)gamma;
+  (void)k;
+  size_t need = 0;
+  bst::ex_carve(nullptr, n_cap < 1 ? 1 : n_cap, &need);
+  return need;
+}
+
+extern "C" int bst_expand(const int32_t* tok, const double* prob, int gamma, int k, const bst_plan_t* plan,
+                          int n_cap, const bst_tree_t* out, void* ws, size_t ws_bytes, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(tok && prob && plan && out, "null pointer argument");
+  BST_REQUIRE(gamma >= 1 && gamma <= EX_MAXG, "gamma must be in [1, %d], got %d", EX_MAXG, gamma);
+  BST_REQUIRE(k >= 1 && k <= EX_MAXK, "k must be in [1, %d], got %d", EX_MAXK, k);
+  BST_REQUIRE((int64_t)gamma * k <= 2 * EX_CAP, "gamma*k exceeds %d", 2 * EX_CAP);
+  BST_REQUIRE(n_cap >= 1, "n_cap must be >= 1");
+  BST_REQUIRE(out->parent && out->depth && out->token && out->rank && out->rho && out->meta && out->surrogate,
+              "tree output arrays must be non-null");
+  BST_REQUIRE(!out->anc_mask || (int64_t)out->mask_words * 32 >= (int64_t)n_cap + 1, "mask_words too small");
+  const bst_plan_t p = *plan;
+  if (p.policy == BST_POLICY_BEAM) {
+    BST_REQUIRE(p.width >= 1, "width must be >= 1, got %d", p.width);
+    BST_REQUIRE(p.depth >= 1 && p.depth <= gamma, "depth must be in [1, %d], got %d", gamma, p.depth);
+    BST_REQUIRE((int64_t)p.width * k <= EX_CAP, "beam width*k exceeds %d", EX_CAP);
+    BST_REQUIRE((int64_t)p.width * p.depth <= n_cap, "beam width*depth exceeds n_cap");
+  } else {
+    BST_REQUIRE(p.policy == BST_POLICY_ADAPTIVE || p.policy == BST_POLICY_FIXED, "unknown policy %d", p.policy);
+    BST_REQUIRE(p.n_max >= 1, "n_max must be >= 1, got %d", p.n_max);
+    BST_REQUIRE(p.n_max <= n_cap, "n_max %d exceeds n_cap %d", p.n_max, n_cap);
+    BST_REQUIRE(n_cap < (1 << 20), "n_cap must be < 2^20");
+    if (p.policy == BST_POLICY_ADAPTIVE) {
+      // exact int64 curve arithmetic up to s = n_cap + 1 (Python ints are unbounded)
+      const long double smax = (long double)n_cap + 1;
+      long double f = ((long double)p.curve.flops_lin + (long double)p.curve.flops_quad * smax) * smax;
+      long double b = (long double)p.curve.bytes_const +
+                      ((long double)p.curve.bytes_lin + (long double)p.curve.bytes_quad * smax) * smax;
+      BST_REQUIRE(f < 9.0e18L && b < 9.0e18L, "latency-curve coefficients overflow int64 at s=%d", n_cap + 1);
+    }
+  }
+  size_t need = 0;
+  ExWs w = ex_carve(ws, n_cap, &need);
+  BST_REQUIRE(ws != nullptr && ws_bytes >= need, "workspace too small: %zu < %zu", ws_bytes, need);
+  const size_t smem = sizeof(ExSmem);
+  static bool attr_done = false;
+  if (!attr_done) {
+    BST_CUDA(cudaFuncSetAttribute(expand_best_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    BST_CUDA(cudaFuncSetAttribute(expand_beam_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done = true;
+  }
+  cudaStream_t st = as_stream(stream);
+  if (p.policy == BST_POLICY_BEAM) {
+    expand_beam_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, n_cap, *out, w);
+  } else {
+    const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
+    expand_best_first_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, n_cap, *out, w, heap_in_smem);
+  }
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" double bst_curve_latency(const bst_curve_t* curve, int64_t s) { return bst::curve_latency(*curve, s); }

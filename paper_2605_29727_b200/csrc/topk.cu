@@ -1,0 +1,278 @@
+// K1 — drafter logits -> fp64 marginals -> top-K candidate lattice.
+//
+// Replaces the plugin softmax that produces MarginalBlock rows
+// (lattice.py:24-55) fused with top_k_truncate (lattice.py:128-142).
+// Ordering is (prob desc, token asc) on the FINAL fp64 probabilities, so the
+// lattice equals top_k_truncate applied to the fp64 rows this kernel also
+// emits (probs_full) — bit for bit.
+//
+// Four short launches per call, all grid-parallel over (chunk, row):
+//   A: per-chunk fp32 max                  B: per-chunk fp64 sum exp(l - m)
+//   C: probs + per-chunk top-K             D: per-row merge of chunk candidates
+// The row is split in CHUNK-element chunks so gamma=16 rows of V=151936 fill
+// ~600 CTAs (4 waves of 148 SMs) instead of 16.
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+
+namespace bst {
+
+constexpr int TK_THREADS = 256;
+constexpr int TK_PER_THREAD = 16;
+constexpr int TK_CHUNK = TK_THREADS * TK_PER_THREAD;  // 4096
+constexpr int TK_MAX_K = 256;
+
+struct TopkWs {
+  float* pmax;     // [gamma][chunks]
+  double* psum;    // [gamma][chunks]
+  double* cprob;   // [gamma][chunks][k]
+  int32_t* ctok;   // [gamma][chunks][k]
+};
+
+static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
+
+static TopkWs carve(void* ws, int gamma, int chunks, int k, size_t* total) {
+  char* p = static_cast<char*>(ws);
+  TopkWs w;
+  size_t off = 0;
+  w.pmax = reinterpret_cast<float*>(p + off);
+  off += align_up(sizeof(float) * gamma * chunks);
+  w.psum = reinterpret_cast<double*>(p + off);
+  off += align_up(sizeof(double) * gamma * chunks);
+  w.cprob = reinterpret_cast<double*>(p + off);
+  off += align_up(sizeof(double) * gamma * chunks * k);
+  w.ctok = reinterpret_cast<int32_t*>(p + off);
+  off += align_up(sizeof(int32_t) * gamma * chunks * k);
+  *total = off;
+  return w;
+}
+
+__device__ __forceinline__ float load_logit(const void* base, int dtype, int64_t idx) {
+  if (dtype == 0) return __ldg(static_cast<const float*>(base) + idx);
+  return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
+__device__ __forceinline__ bool better(double pa, int ta, double pb, int tb) {
+  return pa > pb || (pa == pb && ta < tb);
+}
+
+// --- A: chunk max ----------------------------------------------------------
+__global__ void __launch_bounds__(TK_THREADS) k1_chunk_max(const void* logits, int dtype, int vocab,
+                                                           int64_t stride, float* pmax) {
+  const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
+  const int64_t base = (int64_t)row * stride;
+  float m = -INFINITY;
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    int v = chunk * TK_CHUNK + i * TK_THREADS + threadIdx.x;
+    if (v < vocab) m = fmaxf(m, load_logit(logits, dtype, base + v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  __shared__ float red[TK_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = red[0];
+    for (int w = 1; w < TK_THREADS / 32; ++w) r = fmaxf(r, red[w]);
+    pmax[row * chunks + chunk] = r;
+  }
+}
+
+__device__ __forceinline__ float row_max(const float* pmax, int row, int chunks) {
+  // every block reduces the same small array in the same order
+  float m = -INFINITY;
+  for (int j = 0; j < chunks; ++j) m = fmaxf(m, pmax[row * chunks + j]);
+  return m;
+}
+
+// --- B: chunk sum of exp(l - m) in fp64 (fixed reduction order) ------------
+__global__ void __launch_bounds__(TK_THREADS) k1_chunk_sum(const void* logits, int dtype, int vocab,
+                                                           int64_t stride, const float* pmax,
+                                                           double* psum) {
+  const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
+  __shared__ float sm_m;
+  if (threadIdx.x == 0) sm_m = row_max(pmax, row, chunks);
+  __syncthreads();
+  const double m = (double)sm_m;
+  const int64_t base = (int64_t)row * stride;
+  double s = 0.0;
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    int v = chunk * TK_CHUNK + i * TK_THREADS + threadIdx.x;
+    if (v < vocab) s = __dadd_rn(s, exp((double)load_logit(logits, dtype, base + v) - m));
+  }
+  s = warp_sum(s);
+  __shared__ double red[TK_THREADS / 32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < TK_THREADS / 32; ++w) r = __dadd_rn(r, red[w]);
+    psum[row * chunks + chunk] = r;
+  }
+}
+
+// Block-wide argmax extraction of k winners over per-thread candidate lists.
+// cand arrays are in registers (TK_PER_THREAD per thread); taken marks used.
+__device__ void block_extract(double (&p)[TK_PER_THREAD], int (&t)[TK_PER_THREAD], int n_valid_per_thread,
+                              int k, double* out_p, int32_t* out_t) {
+  __shared__ double sp[TK_THREADS / 32];
+  __shared__ int st[TK_THREADS / 32];
+  __shared__ int sw[TK_THREADS / 32];
+  __shared__ int win_thread, win_slot;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = 0; r < k; ++r) {
+    // local best
+    double bp = -1.0;
+    int bt = 0x7fffffff, bs = -1;
+    for (int i = 0; i < n_valid_per_thread; ++i) {
+      if (t[i] >= 0 && better(p[i], t[i], bp, bt)) { bp = p[i]; bt = t[i]; bs = i; }
+    }
+    int who = threadIdx.x;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      double op = __shfl_xor_sync(0xffffffffu, bp, o);
+      int ot = __shfl_xor_sync(0xffffffffu, bt, o);
+      int ow = __shfl_xor_sync(0xffffffffu, who, o);
+      if (better(op, ot, bp, bt)) { bp = op; bt = ot; who = ow; }
+    }
+    if (lane == 0) { sp[warp] = bp; st[warp] = bt; sw[warp] = who; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double gp = sp[0];
+      int gt = st[0], gw = sw[0];
+      for (int w = 1; w < TK_THREADS / 32; ++w)
+        if (better(sp[w], st[w], gp, gt)) { gp = sp[w]; gt = st[w]; gw = sw[w]; }
+      out_p[r] = gp;
+      out_t[r] = gt;
+      win_thread = gw;
+    }
+    __syncthreads();
+    if (threadIdx.x == win_thread) {
+      // remove the winner from this thread's list
+      int wi = -1;
+      double wp = -1.0;
+      int wt = 0x7fffffff;
+      for (int i = 0; i < n_valid_per_thread; ++i)
+        if (t[i] >= 0 && better(p[i], t[i], wp, wt)) { wp = p[i]; wt = t[i]; wi = i; }
+      if (wi >= 0) t[wi] = -1;
+      (void)win_slot;
+    }
+    __syncthreads();
+  }
+}
+
+// --- C: probabilities + per-chunk top-k ------------------------------------
+__global__ void __launch_bounds__(TK_THREADS) k1_chunk_select(const void* logits, int dtype,
+                                                              const double* probs_in, int vocab,
+                                                              int64_t stride, const float* pmax,
+                                                              const double* psum, int k,
+                                                              double* probs_full, double* cprob,
+                                                              int32_t* ctok) {
+  const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
+  __shared__ double sm_z;
+  __shared__ float sm_m;
+  if (probs_in == nullptr && threadIdx.x == 0) {
+    sm_m = row_max(pmax, row, chunks);
+    double z = 0.0;
+    for (int j = 0; j < chunks; ++j) z = __dadd_rn(z, psum[row * chunks + j]);
+    sm_z = z;
+  }
+  __syncthreads();
+  double p[TK_PER_THREAD];
+  int t[TK_PER_THREAD];
+  const int64_t base = (int64_t)row * stride;
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    int v = chunk * TK_CHUNK + i * TK_THREADS + threadIdx.x;
+    if (v < vocab) {
+      double q;
+      if (probs_in != nullptr) {
+        q = probs_in[base + v];
+      } else {
+        q = __ddiv_rn(exp((double)load_logit(logits, dtype, base + v) - (double)sm_m), sm_z);
+        if (probs_full) probs_full[(int64_t)row * vocab + v] = q;
+      }
+      p[i] = q;
+      t[i] = v;
+    } else {
+      p[i] = -1.0;
+      t[i] = -1;
+    }
+  }
+  const int kk = min(k, min(TK_CHUNK, vocab - chunk * TK_CHUNK));
+  double* op = cprob + ((int64_t)row * chunks + chunk) * k;
+  int32_t* ot = ctok + ((int64_t)row * chunks + chunk) * k;
+  block_extract(p, t, TK_PER_THREAD, kk, op, ot);
+  if (threadIdx.x == 0)
+    for (int r = kk; r < k; ++r) { op[r] = -1.0; ot[r] = -1; }
+}
+
+// --- D: merge chunk candidates of one row ----------------------------------
+__global__ void __launch_bounds__(TK_THREADS) k1_merge(const double* cprob, const int32_t* ctok, int chunks,
+                                                       int k, int32_t* tok_out, double* prob_out) {
+  const int row = blockIdx.x;
+  const int n = chunks * k;
+  double p[TK_PER_THREAD];
+  int t[TK_PER_THREAD];
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    int j = i * TK_THREADS + threadIdx.x;
+    if (j < n) {
+      p[i] = cprob[(int64_t)row * n + j];
+      t[i] = ctok[(int64_t)row * n + j];
+    } else {
+      p[i] = -1.0;
+      t[i] = -1;
+    }
+  }
+  block_extract(p, t, TK_PER_THREAD, k, prob_out + (int64_t)row * k, tok_out + (int64_t)row * k);
+}
+
+static int run_topk(const void* logits, int dtype, const double* probs_in, int gamma, int vocab, int64_t stride,
+                    int k, int32_t* tok, double* prob, double* probs_full, void* ws, size_t ws_bytes,
+                    cudaStream_t st) {
+  BST_REQUIRE(gamma >= 1, "gamma must be >= 1, got %d", gamma);
+  BST_REQUIRE(vocab >= 2, "vocab_size must be >= 2, got %d", vocab);
+  BST_REQUIRE(k >= 1 && k <= vocab, "k must be in [1, %d], got %d", vocab, k);
+  BST_REQUIRE(k <= TK_MAX_K, "k=%d exceeds the kernel limit %d", k, TK_MAX_K);
+  BST_REQUIRE(stride >= vocab, "row stride %lld < vocab %d", (long long)stride, vocab);
+  const int chunks = (vocab + TK_CHUNK - 1) / TK_CHUNK;
+  BST_REQUIRE((int64_t)chunks * k <= TK_CHUNK, "vocab*k too large for one merge block");
+  size_t need = 0;
+  TopkWs w = carve(ws, gamma, chunks, k, &need);
+  BST_REQUIRE(ws != nullptr && ws_bytes >= need, "workspace too small: %zu < %zu", ws_bytes, need);
+  dim3 grid(chunks, gamma);
+  if (probs_in == nullptr) {
+    k1_chunk_max<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax);
+    k1_chunk_sum<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax, w.psum);
+  }
+  k1_chunk_select<<<grid, TK_THREADS, 0, st>>>(logits, dtype, probs_in, vocab, stride, w.pmax, w.psum, k,
+                                               probs_full, w.cprob, w.ctok);
+  k1_merge<<<gamma, TK_THREADS, 0, st>>>(w.cprob, w.ctok, chunks, k, tok, prob);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+}  // namespace bst
+
+extern "C" size_t bst_topk_workspace(int gamma, int vocab, int k) {
+  if (gamma < 1 || vocab < 1 || k < 1) return 0;
+  size_t need = 0;
+  const int chunks = (vocab + bst::TK_CHUNK - 1) / bst::TK_CHUNK;
+  bst::carve(nullptr, gamma, chunks, k, &need);
+  return need;
+}
+
+extern "C" int bst_topk_logits(const void* logits, int dtype, int gamma, int vocab, int64_t row_stride, int k,
+                               int32_t* tok, double* prob, double* probs_full, void* ws, size_t ws_bytes,
+                               bst_stream_t stream) {
+  BST_REQUIRE(dtype == 0 || dtype == 1, "dtype must be 0 (fp32) or 1 (bf16), got %d", dtype);
+  BST_REQUIRE(logits && tok && prob, "null pointer argument");
+  return bst::run_topk(logits, dtype, nullptr, gamma, vocab, row_stride, k, tok, prob, probs_full, ws, ws_bytes,
+                       bst::as_stream(stream));
+}
+
+extern "C" int bst_topk_probs(const double* probs, int gamma, int vocab, int k, int32_t* tok, double* prob,
+                              void* ws, size_t ws_bytes, bst_stream_t stream) {
+  BST_REQUIRE(probs && tok && prob, "null pointer argument");
+  return bst::run_topk(nullptr, 0, probs, gamma, vocab, vocab, k, tok, prob, nullptr, ws, ws_bytes,
+                       bst::as_stream(stream));
+}

@@ -1,0 +1,87 @@
+"""CPU-side checks of the C ABI: the library loads, exports every symbol
+include/bastion.h declares, and its host-side curve arithmetic matches the
+reference LatencyCurve bit for bit (no GPU needed)."""
+
+import re
+from pathlib import Path
+
+from codec import load, unhex
+from oracle import specplan_port as O
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def declared_symbols():
+    text = (ROOT / "include" / "bastion.h").read_text()
+    return sorted(set(re.findall(r"^\s*(?:[\w\s\*]+?)\b(bst_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2605_29727_b200 import _lib
+    lib = _lib.lib()
+    syms = declared_symbols()
+    assert len(syms) >= 12
+    for name in syms:
+        assert hasattr(lib, name), name
+        assert name in _lib.SIGNATURES, f"{name} has no ctypes signature"
+    assert lib.bst_abi_version() == 1
+
+
+def test_host_curve_matches_reference_golden():
+    from paper_2605_29727_b200 import _lib
+    g = load("cost_model")
+    for row in g["rows"]:
+        d = g["profiles"][row["profile"]]
+        dims = O.Dims(L=d["L"], h=d["h"], n_q=d["n_q"], n_kv=d["n_kv"], d=d["d"], h_ffn=d["h_ffn"], V=d["V"],
+                      bp=d["bp"], peak_flops=unhex(d["peak_flops"]), bandwidth=unhex(d["bandwidth"]))
+        cv = O.curve_for(dims, row["c"], row["variant"], unhex(row["slope"]) if row["slope"] else 1.0,
+                         unhex(row["intercept"]) if row["intercept"] else 0.0,
+                         unhex(row["ratio"]) if row["ratio"] else 1.0)
+        st = _lib.Curve(cv.flops_lin, cv.flops_quad, cv.bytes_const, cv.bytes_lin, cv.bytes_quad, cv.inv_peak,
+                        cv.inv_bw, cv.slope, cv.intercept, cv.ratio)
+        for s, want in zip(row["s"], row["curve"]):
+            assert _lib.lib().bst_curve_latency(st, s) == unhex(want)
+
+
+def test_facade_exports_reference_api():
+    import paper_2605_29727_b200 as P
+    names = ["AcceptanceRecord", "CalibrationFit", "CandidateLattice", "ControllerConfig", "ControllerDecision",
+             "CostModelParams", "CycleLatencies", "CycleRecord", "DraftTree", "EmaBias", "LatencyQuery",
+             "MarginalBlock", "Policy", "SimCache", "SimConfig", "SyntheticPairConfig", "TreeNode",
+             "VerifyLatencyEstimator", "ar_decode", "beam_expand", "best_first_expand", "build_tree", "bytes_moved",
+             "commit", "decode", "ema_update", "estimate_verify_latency", "fit_static_calibration", "flops",
+             "linearize", "marginal_gains", "realized_speedup", "roofline_latency", "run_cycle", "replay_trace",
+             "sample_continuation", "surrogate_of", "top_k_truncate", "verify_tree"]
+    for n in names:
+        assert hasattr(P, n), n
+
+
+def test_device_entry_points_fail_loudly_without_gpu():
+    import numpy as np
+    import pytest
+    import torch
+    import paper_2605_29727_b200 as P
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    block = P.MarginalBlock(gamma=1, vocab_size=3, probs=np.array([[0.5, 0.3, 0.2]]))
+    with pytest.raises(RuntimeError, match="CUDA device"):
+        P.top_k_truncate(block, 2)
+    with pytest.raises(ValueError):  # argument errors keep the reference's ValueError
+        P.top_k_truncate(block, 4)
+
+
+def test_cost_model_facade_matches_golden():
+    import paper_2605_29727_b200 as P
+    g = load("cost_model")
+    for row in g["rows"][:40]:
+        d = g["profiles"][row["profile"]]
+        p = P.CostModelParams(L=d["L"], h=d["h"], n_q=d["n_q"], n_kv=d["n_kv"], d=d["d"], h_ffn=d["h_ffn"],
+                              V=d["V"], bp=d["bp"], peak_flops=unhex(d["peak_flops"]),
+                              bandwidth=unhex(d["bandwidth"]))
+        fit = P.CalibrationFit(unhex(row["slope"]), unhex(row["intercept"]), 0.0, 0.0) if row["slope"] else None
+        bias = P.EmaBias(unhex(row["ratio"])) if row["ratio"] else None
+        est = P.VerifyLatencyEstimator(p, variant=row["variant"], fit=fit, bias=bias)
+        curve = est.curve(row["c"])
+        for s, want, want_est in zip(row["s"], row["curve"], row["estimate"]):
+            assert curve.latency(s) == unhex(want)
+            assert est.estimate(s, row["c"]) == unhex(want_est)
