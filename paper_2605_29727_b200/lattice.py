@@ -137,7 +137,7 @@ def top_k_truncate(block: MarginalBlock, k: int) -> CandidateLattice:
     if not 1 <= k <= block.vocab_size:
         raise ValueError(f"k must be in [1, {block.vocab_size}], got {k}")
     dev = require_cuda()
-    probs = torch.from_numpy(np.ascontiguousarray(block.probs)).to(dev)
+    probs = torch.from_numpy(np.array(block.probs, dtype=np.float64)).to(dev)
     tok, prob = topk_device(probs, k)
     return CandidateLattice(source=block, top_k=k, entries=_entries(tok.cpu().numpy(), prob.cpu().numpy()),
                             device=(tok, prob))
