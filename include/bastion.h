@@ -136,6 +136,31 @@ int bst_kv_compact(void* kv, int n_layers, int n_kv, int head_dim, int page_size
                    const int32_t* page_table, const int32_t* c_dev, const int32_t* path, const int32_t* meta,
                    int max_path, bst_stream_t stream);
 
+/* ------------------------------------------------------------------------
+ * K4 — bf16 weight-streaming GEMM on tcgen05, Y[m,n_out] = X[m,K] . W[n_out,K]^T.
+ * Replaces the dense matmul rows of the Appendix-D cost model
+ * (cost_model.py:118-123) — the reference has no GEMM.
+ * Output is a set of fp32 partial slots (stream-K over (tile, k-block)
+ * units); consumers reduce them in fixed order (bst_gemm_reduce / argmax or
+ * the fused epilogue kernels of the model forward).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int32_t n_out, k, m, bn;      /* bn = round_up(m, 16) token columns (<= 256) */
+  int32_t n_mt, n_kb, grid, s_max;
+  int64_t units;                /* n_mt * n_kb */
+  int32_t tmem_cols, stages;
+  int64_t partial_floats;       /* size of the partial buffer */
+} bst_gemm_sched_t;
+
+int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sched_t* out);
+int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_gemm_sched_t* sched, float* partial,
+             size_t partial_bytes, bst_stream_t stream);
+int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* y_f32, void* y_bf16, int64_t ldy,
+                    bst_stream_t stream);
+/* Per-row argmax of Y with numpy tie-break (lowest index), verify_sim.py:107-109. */
+int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* argmax,
+                    bst_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,15 @@ class Tree(C.Structure):
                 ("child_start", C.c_void_p), ("child_list", C.c_void_p)]
 
 
+class GemmSched(C.Structure):
+    """bst_gemm_sched_t — stream-K schedule of one GEMM shape."""
+
+    _fields_ = [("n_out", C.c_int32), ("k", C.c_int32), ("m", C.c_int32), ("bn", C.c_int32),
+                ("n_mt", C.c_int32), ("n_kb", C.c_int32), ("grid", C.c_int32), ("s_max", C.c_int32),
+                ("units", C.c_int64), ("tmem_cols", C.c_int32), ("stages", C.c_int32),
+                ("partial_floats", C.c_int64)]
+
+
 _P, _I, _I64, _SZ, _D = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
 SIGNATURES = {
     "bst_abi_version": (C.c_int, []),
@@ -52,6 +61,10 @@ SIGNATURES = {
     "bst_expand": (_I, [_P, _P, _I, _I, C.POINTER(Plan), _I, C.POINTER(Tree), _P, _SZ, _P]),
     "bst_linearize_mask": (_I, [_P, _I, _I, _I, _P, _P]),
     "bst_ancestor_mask": (_I, [_P, _I, _I, _P, _P]),
+    "bst_gemm_schedule": (_I, [_I, _I, _I, _I, C.POINTER(GemmSched)]),
+    "bst_gemm": (_I, [_P, _P, _I64, C.POINTER(GemmSched), _P, _SZ, _P]),
+    "bst_gemm_reduce": (_I, [_P, C.POINTER(GemmSched), _P, _P, _I64, _P]),
+    "bst_gemm_argmax": (_I, [_P, C.POINTER(GemmSched), _P, _P, _P]),
     "bst_accept": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_kv_compact": (_I, [_P, _I, _I, _I, _I, _I64, _P, _P, _P, _P, _I, _P]),
 }

@@ -1,0 +1,369 @@
+// K4 — weight-streaming bf16 GEMM on tcgen05 (TMA -> smem ring -> UMMA -> TMEM).
+//
+//   Y[m, n_out] = X[m, K] . W[n_out, K]^T        (nn.Linear, W row-major)
+//
+// Verify-time GEMMs are skinny (m = s = N+1 <= 256 tokens) and read every
+// weight byte exactly once, so the kernel is built around HBM streaming:
+// "swap AB" — the weight tile is the 128-row UMMA A operand, the token tile
+// the N operand (N = round_up(m, 16) <= 256), the accumulator is 128 lanes x N
+// fp32 columns of TMEM.  Work = (m_tile, k_block) units split evenly over one
+// persistent CTA per SM (stream-K): a CTA covers a contiguous unit range, so a
+// tile is shared by at most a few CTAs; each writes its fp32 partial to its
+// own slot and the consumer kernel (residual/norm/SwiGLU/argmax epilogue)
+// reduces the slots in fixed order — deterministic, no atomics.
+//
+// Roles per CTA (192 threads): warp 0 = TMA producer, warp 1 = TMEM owner +
+// single-thread UMMA issuer, warps 2-5 = epilogue (TMEM -> registers -> L2).
+// The TMEM accumulator is double buffered so the next segment's MMAs overlap
+// the previous segment's epilogue.
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+
+#include <mutex>
+#include <unordered_map>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "sm100.cuh"
+
+namespace bst {
+
+constexpr int G_THREADS = 192;
+constexpr int G_BM = 128;
+constexpr int G_BK = 64;
+constexpr int G_TILE_W = G_BM * G_BK * 2;  // 16 KiB
+constexpr int G_MAX_STAGES = 12;
+constexpr int G_SMEM_BUDGET = 200 * 1024;
+
+// ------------------------------------------------------------ tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static std::mutex g_mu;
+
+static int get_encoder() {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_encode) return BST_OK;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+  if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || fn == nullptr) {
+    set_error("cuTensorMapEncodeTiled unavailable: %s", cudaGetErrorString(e));
+    return BST_ECUDA;
+  }
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return BST_OK;
+}
+
+// 2-D bf16 tensor [rows, cols] (row stride in elements), box = box_rows x 64, 128B swizzle.
+int make_tmap_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t cols, uint64_t row_stride,
+                   uint32_t box_rows, uint32_t box_cols) {
+  int rc = get_encoder();
+  if (rc) return rc;
+  BST_REQUIRE(((uintptr_t)ptr & 15) == 0, "TMA base pointer must be 16-byte aligned");
+  BST_REQUIRE((row_stride * 2) % 16 == 0, "TMA row stride must be a multiple of 16 bytes");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d) rows=%llu cols=%llu box=%ux%u", (int)r,
+              (unsigned long long)rows, (unsigned long long)cols, box_rows, box_cols);
+    return BST_ECUDA;
+  }
+  return BST_OK;
+}
+
+// Tensor-map cache keyed by (ptr, rows, cols, stride, box): weights are encoded once.
+struct MapKey {
+  uintptr_t ptr;
+  uint64_t rows, cols, stride;
+  uint32_t br, bc;
+  bool operator==(const MapKey& o) const {
+    return ptr == o.ptr && rows == o.rows && cols == o.cols && stride == o.stride && br == o.br && bc == o.bc;
+  }
+};
+struct MapKeyHash {
+  size_t operator()(const MapKey& k) const {
+    return std::hash<uintptr_t>()(k.ptr) ^ (k.rows * 1315423911u) ^ (k.cols << 7) ^ (k.stride << 13) ^
+           ((uint64_t)k.br << 29) ^ ((uint64_t)k.bc << 41);
+  }
+};
+static std::unordered_map<MapKey, CUtensorMap, MapKeyHash> g_maps;
+
+int cached_tmap(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols, uint64_t stride, uint32_t br,
+                uint32_t bc) {
+  MapKey key{(uintptr_t)ptr, rows, cols, stride, br, bc};
+  {
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto it = g_maps.find(key);
+    if (it != g_maps.end()) {
+      *out = it->second;
+      return BST_OK;
+    }
+  }
+  int rc = make_tmap_bf16(out, ptr, rows, cols, stride, br, bc);
+  if (rc) return rc;
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_maps.size() > 4096) g_maps.clear();
+  g_maps[key] = *out;
+  return BST_OK;
+}
+
+// ------------------------------------------------------------------ kernel
+struct Seg {
+  int tile, kb_lo, kb_hi, slot;
+};
+
+__device__ __forceinline__ bool next_seg(const bst_gemm_sched_t& s, int64_t& u, int64_t u1, Seg& seg) {
+  if (u >= u1) return false;
+  seg.tile = (int)(u / s.n_kb);
+  seg.kb_lo = (int)(u % s.n_kb);
+  { const int64_t lim = (int64_t)seg.kb_lo + (u1 - u); seg.kb_hi = (int)(lim < s.n_kb ? lim : s.n_kb); }
+  seg.slot = (int)blockIdx.x - sched_first_cta(s, seg.tile);
+  u += seg.kb_hi - seg.kb_lo;
+  return true;
+}
+
+__global__ void __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                     bst_gemm_sched_t s, float* __restrict__ partial, int stages) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[G_MAX_STAGES], empty[G_MAX_STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
+  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
+  const int bn = s.bn;
+  const uint32_t x_bytes = (uint32_t)bn * G_BK * 2;
+  const uint32_t stage_bytes = G_TILE_W + x_bytes;
+  const uint32_t tcols = s.tmem_cols;
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tmW);
+    sm100::prefetch_tmap(&tmX);
+    for (int i = 0; i < stages; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&tfull[i], 1); sm100::mbar_init(&tempty[i], 4); }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_base_sh, tcols);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  const int64_t u0 = (int64_t)blockIdx.x * s.units / s.grid;
+  const int64_t u1 = (int64_t)(blockIdx.x + 1) * s.units / s.grid;
+
+  if (warp == 0) {
+    // ---------------- TMA producer
+    if (lane == 0) {
+      const uint64_t pol_w = sm100::policy_evict_first();
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t u = u0;
+      Seg seg;
+      while (next_seg(s, u, u1, seg)) {
+        for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
+          sm100::mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sw = smem + stage * stage_bytes;
+          sm100::mbar_expect_tx(&full[stage], stage_bytes);
+          sm100::tma_load_2d_hint(sw, &tmW, &full[stage], kb * G_BK, seg.tile * G_BM, pol_w);
+          sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- UMMA issuer
+    const uint32_t idesc = sm100::idesc_bf16(G_BM, bn);
+    int stage = 0;
+    uint32_t phase = 0;
+    int64_t u = u0;
+    Seg seg;
+    int j = 0;
+    while (next_seg(s, u, u1, seg)) {
+      const int acc = j & 1;
+      sm100::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      sm100::tc_fence_after();
+      const uint32_t d = tmem + acc * bn;
+      for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
+        sm100::mbar_wait(&full[stage], phase);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t a_addr = base + stage * stage_bytes;
+          const uint64_t adesc = sm100::desc_k_sw128(a_addr);
+          const uint64_t bdesc = sm100::desc_k_sw128(a_addr + G_TILE_W);
+#pragma unroll
+          for (int k = 0; k < G_BK / 16; ++k)  // +32 B per K=16 step inside the 128B swizzle atom
+            sm100::umma_f16(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+          sm100::umma_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == stages) { stage = 0; phase ^= 1; }
+      }
+      if (sm100::elect_one()) sm100::umma_commit(&tfull[acc]);
+      __syncwarp();
+      ++j;
+    }
+  } else {
+    // ---------------- epilogue: TMEM -> fp32 partial slot
+    const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const int row = quad * 32 + lane;
+    int64_t u = u0;
+    Seg seg;
+    int j = 0;
+    while (next_seg(s, u, u1, seg)) {
+      const int acc = j & 1;
+      sm100::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      sm100::tc_fence_after();
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * bn;
+      float* dst = partial + ((int64_t)(seg.tile * s.s_max + seg.slot) * bn) * G_BM + row;
+      for (int c0 = 0; c0 < bn; c0 += 16) {
+        float v[16];
+        sm100::tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < s.m) dst[(int64_t)(c0 + i) * G_BM] = v[i];
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      ++j;
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, tcols);
+  }
+}
+
+// ------------------------------------------------------ reduction kernels
+__global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* y_f32,
+                                   __nv_bfloat16* y_bf16, int64_t ldy) {
+  const int t = blockIdx.y;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < s.n_out; n += gridDim.x * blockDim.x) {
+    float v = gemm_load(partial, s, t, n);
+    if (y_f32) y_f32[(int64_t)t * ldy + n] = v;
+    if (y_bf16) y_bf16[(int64_t)t * ldy + n] = __float2bfloat16(v);
+  }
+}
+
+// Per-token argmax over the full output width, lowest index on ties (np.argmax).
+__global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_sched_t s,
+                                   unsigned long long* best) {
+  const int t = blockIdx.y;
+  unsigned long long key = 0;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < s.n_out; n += gridDim.x * blockDim.x) {
+    float v = gemm_load(partial, s, t, n);
+    unsigned int b = __float_as_uint(v);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)n);
+    key = k > key ? k : key;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+    key = ok > key ? ok : key;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(best + t, key);
+}
+
+__global__ void argmax_finalize_kernel(const unsigned long long* best, int m, int32_t* out) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(best[t] & 0xFFFFFFFFull));
+}
+
+}  // namespace bst
+
+// ---------------------------------------------------------------- C ABI
+extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sched_t* out) {
+  using namespace bst;
+  BST_REQUIRE(out, "null schedule");
+  BST_REQUIRE(n_out >= 1 && k >= 1, "bad GEMM shape n_out=%d k=%d", n_out, k);
+  BST_REQUIRE(m >= 1 && m <= 256, "m must be in [1, 256] (got %d); chunk larger batches", m);
+  BST_REQUIRE(k % 8 == 0, "K must be a multiple of 8 (16-byte TMA rows), got %d", k);
+  bst_gemm_sched_t s{};
+  s.n_out = n_out;
+  s.k = k;
+  s.m = m;
+  s.bn = ((m + 15) / 16) * 16;
+  s.n_mt = (n_out + G_BM - 1) / G_BM;
+  s.n_kb = (k + G_BK - 1) / G_BK;
+  s.units = (int64_t)s.n_mt * s.n_kb;
+  if (grid <= 0) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    grid = sms;
+  }
+  s.grid = (int)(s.units < grid ? s.units : grid);
+  int smax = 1;
+  for (int t = 0; t < s.n_mt; ++t) {
+    int c = sched_last_cta(s, t) - sched_first_cta(s, t) + 1;
+    smax = c > smax ? c : smax;
+  }
+  s.s_max = smax;
+  int tc = 32;
+  while (tc < 2 * s.bn) tc <<= 1;
+  s.tmem_cols = tc;
+  const int stage_bytes = G_TILE_W + s.bn * G_BK * 2;
+  int stages = (G_SMEM_BUDGET - 1024) / stage_bytes;
+  s.stages = stages > G_MAX_STAGES ? G_MAX_STAGES : stages;
+  s.partial_floats = (int64_t)s.n_mt * s.s_max * s.bn * G_BM;
+  *out = s;
+  return BST_OK;
+}
+
+extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_gemm_sched_t* sched, float* partial,
+                        size_t partial_bytes, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(w && x && sched && partial, "null pointer argument");
+  const bst_gemm_sched_t s = *sched;
+  BST_REQUIRE(partial_bytes >= (size_t)s.partial_floats * sizeof(float), "partial buffer too small");
+  BST_REQUIRE(ld_x >= s.k, "ld_x < K");
+  CUtensorMap tw, tx;
+  int rc = cached_tmap(&tw, w, (uint64_t)s.n_out, (uint64_t)s.k, (uint64_t)s.k, G_BM, G_BK);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tx, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)s.bn, G_BK);
+  if (rc) return rc;
+  const int smem = s.stages * (G_TILE_W + s.bn * G_BK * 2) + 1024;
+  static int configured = 0;
+  if (smem > configured) {
+    BST_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured = smem;
+  }
+  gemm_bf16_kernel<<<s.grid, G_THREADS, smem, as_stream(stream)>>>(tw, tx, s, partial, s.stages);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* y_f32, void* y_bf16,
+                               int64_t ldy, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(partial && sched && (y_f32 || y_bf16), "null pointer argument");
+  const bst_gemm_sched_t s = *sched;
+  dim3 grid((s.n_out + 255) / 256 < 64 ? (s.n_out + 255) / 256 : 64, s.m);
+  gemm_reduce_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, s, y_f32,
+                                                          static_cast<__nv_bfloat16*>(y_bf16), ldy);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64,
+                               int32_t* argmax, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(partial && sched && scratch_u64 && argmax, "null pointer argument");
+  const bst_gemm_sched_t s = *sched;
+  cudaStream_t st = as_stream(stream);
+  BST_CUDA(cudaMemsetAsync(scratch_u64, 0, sizeof(unsigned long long) * s.m, st));
+  dim3 grid(64, s.m);
+  gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64));
+  argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
+                                                            argmax);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
