@@ -85,6 +85,13 @@ typedef struct {
   bst_curve_t curve; /* adaptive only */
   double fixed_cost; /* t_draft + t_aux, controller.py:73 */
   double l_ar;       /* CycleLatencies.l_ar */
+  /* Optional device-resident decode state: when `state` is non-null the
+   * context is c = state[c_idx] and the curve coefficients are
+   * base + d_* * c (exact integers, LatencyCurve at context c).            */
+  const int32_t* state;
+  int32_t c_idx;
+  int32_t _pad2;
+  int64_t d_flops_lin, d_bytes_const, d_bytes_lin;
 } bst_plan_t;
 
 /* Output arrays (device), row 0 = root.  Capacity n_cap+1 rows. */
@@ -125,6 +132,12 @@ int bst_ancestor_mask(const int32_t* parent, int t, int mask_words, uint32_t* ma
  * root), meta[1] = bonus token, meta[2] = number of committed tokens.
  * committed[] receives accepted draft tokens then the bonus (commit order).
  * ---------------------------------------------------------------------- */
+/* Device plan variant: identical to bst_expand but the plan lives in device
+ * memory (so a captured CUDA graph can be re-planned by a host->device copy). */
+int bst_expand_dev(const int32_t* tok, const double* prob, int gamma, int k, const bst_plan_t* plan_dev,
+                   int policy, int n_max, int n_cap, const bst_tree_t* out, void* ws, size_t ws_bytes,
+                   bst_stream_t stream);
+
 int bst_accept(const int32_t* token, const int32_t* child_start, const int32_t* child_list,
                const int32_t* argmax, int max_path, int32_t* path, int32_t* committed, int32_t* meta,
                bst_stream_t stream);
@@ -160,6 +173,58 @@ int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* 
 /* Per-row argmax of Y with numpy tie-break (lowest index), verify_sim.py:107-109. */
 int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* argmax,
                     bst_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * K3 — tree-masked attention over the paged KV cache
+ * (mask semantics of linearize, verify_sim.py:336-355; cost PAPER.md:1056-1062).
+ * mode 0 TREE (prefix + ancestor bitmask), 1 CAUSAL (chunked prefill),
+ * 2 FULL (drafter block).  c = state[c_idx] when state is non-null.
+ * ---------------------------------------------------------------------- */
+int bst_attention(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                  int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
+                  int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
+                  const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes, bst_stream_t stream);
+size_t bst_attention_workspace(int n_q, int s, int n_splits);
+
+/* ------------------------------------------------------------------------
+ * K5 — fused elementwise epilogues of the target/drafter forward.
+ * ---------------------------------------------------------------------- */
+int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* emb, int h, const void* w, float eps, float* resid,
+                      void* x, int64_t ldx, bst_stream_t stream);
+int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t* sched, float* resid, int rows, int h,
+                         const void* w, float eps, void* x, int64_t ldx, void* feat, int64_t ldf, bst_stream_t stream);
+/* pos/slot are relative to c = state[c_idx]; slot == INT32_MIN skips the KV write,
+ * qrow < 0 skips the q write. */
+int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv, const void* q_norm,
+                 const void* k_norm, float eps, const float* inv_freq /* [64] */, const int32_t* pos,
+                 const int32_t* slot,
+                 const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv, int64_t layer_off_elems,
+                 const int32_t* page_table, int page_size, const int32_t* state, int state_c_idx, bst_stream_t stream);
+int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act, int64_t lda,
+               bst_stream_t stream);
+int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx, const int32_t* count, int max_rows, int cols,
+                    void* dst, int64_t ldd, bst_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Decode-state plumbing of the on-device loop (no host round trip):
+ * state[0]=c (cached tokens = root slot), [1]=n_new (pending drafter
+ * context rows), [2]=bonus (pending root token), [3]=committed count.
+ * ---------------------------------------------------------------------- */
+enum { BST_ST_C = 0, BST_ST_NNEW = 1, BST_ST_BONUS = 2, BST_ST_COMMITTED = 3, BST_ST_CYCLE = 4 };
+/* verify rows from the tree: token (root = bonus), pos = depth, slot = row;
+ * rows beyond n_nodes are padding (token 0, pos 0, slot = row). */
+int bst_verify_rows(const int32_t* state, const int32_t* tree_token, const int32_t* tree_depth, const int32_t* meta,
+                    int rows, int32_t* tokens, int32_t* pos, int32_t* slot, bst_stream_t stream);
+/* drafter rows: block rows 0..gamma (bonus, mask x gamma) at pos/slot 0..gamma;
+ * ctx rows i < n_new at pos/slot i - n_new, the rest skipped. */
+int bst_drafter_rows(const int32_t* state, int gamma, int mask_token, int ctx_rows, int32_t* tokens, int32_t* pos,
+                     int32_t* slot, int32_t* qrow, bst_stream_t stream);
+/* after bst_accept: append committed tokens to out_tokens, c += len,
+ * n_new = len, bonus = meta[1]; log this cycle (tree meta, len, c, bonus,
+ * surrogate) at log[state[BST_ST_CYCLE]] (8 int32 + 1 f64 per cycle). */
+int bst_commit_state(int32_t* state, const int32_t* accept_meta, const int32_t* committed, int max_path,
+                     int32_t* out_tokens, int out_cap, const int32_t* tree_meta, const double* surrogate,
+                     int32_t* log_i32, double* log_f64, int log_cap, bst_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -30,7 +30,8 @@ class Curve(C.Structure):
 class Plan(C.Structure):
     _fields_ = [("policy", C.c_int32), ("n_max", C.c_int32), ("width", C.c_int32), ("depth", C.c_int32),
                 ("algo", C.c_int32), ("_pad", C.c_int32), ("curve", Curve), ("fixed_cost", C.c_double),
-                ("l_ar", C.c_double)]
+                ("l_ar", C.c_double), ("state", C.c_void_p), ("c_idx", C.c_int32), ("_pad2", C.c_int32),
+                ("d_flops_lin", C.c_int64), ("d_bytes_const", C.c_int64), ("d_bytes_lin", C.c_int64)]
 
 
 class Tree(C.Structure):
@@ -65,6 +66,19 @@ SIGNATURES = {
     "bst_gemm": (_I, [_P, _P, _I64, C.POINTER(GemmSched), _P, _SZ, _P]),
     "bst_gemm_reduce": (_I, [_P, C.POINTER(GemmSched), _P, _P, _I64, _P]),
     "bst_gemm_argmax": (_I, [_P, C.POINTER(GemmSched), _P, _P, _P]),
+    "bst_expand_dev": (_I, [_P, _P, _I, _I, _P, _I, _I, _I, C.POINTER(Tree), _P, _SZ, _P]),
+    "bst_attention": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I,
+                           _P, _SZ, _P]),
+    "bst_attention_workspace": (_SZ, [_I, _I, _I]),
+    "bst_embed_rmsnorm": (_I, [_P, _I, _P, _I, _P, C.c_float, _P, _P, _I64, _P]),
+    "bst_residual_rmsnorm": (_I, [_P, _P, _P, _I, _I, _P, C.c_float, _P, _I64, _P, _I64, _P]),
+    "bst_qkv_rope": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64, _P, _I64,
+                          _P, _I, _P, _I, _P]),
+    "bst_swiglu": (_I, [_P, C.POINTER(GemmSched), _I, _I, _P, _I64, _P]),
+    "bst_gather_rows": (_I, [_P, _I64, _P, _P, _I, _I, _P, _I64, _P]),
+    "bst_verify_rows": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
+    "bst_drafter_rows": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "bst_commit_state": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _I, _P]),
     "bst_accept": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_kv_compact": (_I, [_P, _I, _I, _I, _I, _I64, _P, _P, _P, _P, _I, _P]),
 }

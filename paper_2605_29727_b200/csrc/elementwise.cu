@@ -1,0 +1,319 @@
+// K5 — fused elementwise epilogues of the Qwen3-style forward (omitted from
+// the reference cost model: PAPER.md:1002-1003).  Every kernel
+// reads the GEMM's fp32 stream-K partial slots directly (gemm_load), so the
+// GEMM output never round-trips through a separate reduction pass.
+//
+//   embed_rmsnorm     tokens -> residual (fp32) and RMSNorm(x)*w (bf16)
+//   qkv_rope          q/k RMSNorm per head + RoPE (theta) at positions pos[],
+//                     q -> bf16, k/v -> paged KV cache slot slot[] (append)
+//   residual_rmsnorm  residual += Y; x = RMSNorm(residual)*w; optional bf16
+//                     copy of the residual (target features for the drafter)
+//   swiglu            act = silu(gate) * up  (gate/up = one fused GEMM)
+//   gather_rows       rows[path[i]] -> dst[i]  (accepted-path hidden features)
+#include <climits>
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "gemm.cuh"
+
+namespace bst {
+
+constexpr int E_THREADS = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* sh) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (threadIdx.x < 32) {
+    t = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    t = warp_sum(t);
+    if (threadIdx.x == 0) sh[0] = t;
+  }
+  __syncthreads();
+  t = sh[0];
+  __syncthreads();
+  return t;
+}
+
+// ----------------------------------------------------------------- embed
+__global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ emb, int h,
+                                     const __nv_bfloat16* __restrict__ w, float eps, float* __restrict__ resid,
+                                     __nv_bfloat16* __restrict__ x, int64_t ldx) {
+  __shared__ float sh[32];
+  const int t = blockIdx.x;
+  const int64_t tok = tokens[t];
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    float v = __bfloat162float(emb[tok * h + i]);
+    resid[(int64_t)t * h + i] = v;
+    ss += v * v;
+  }
+  const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
+  for (int i = threadIdx.x; i < h; i += blockDim.x)
+    x[(int64_t)t * ldx + i] = __float2bfloat16(resid[(int64_t)t * h + i] * inv * __bfloat162float(w[i]));
+}
+
+// ------------------------------------------------------- residual + norm
+// y == nullptr: only normalise.  resid == nullptr: normalise Y itself.
+__global__ void residual_rmsnorm_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* resid, int h,
+                                        const __nv_bfloat16* __restrict__ w, float eps, __nv_bfloat16* x, int64_t ldx,
+                                        __nv_bfloat16* feat, int64_t ldf, int rows) {
+  __shared__ float sh[32];
+  __shared__ float vals[8192];
+  const int t = blockIdx.x;
+  if (t >= rows) return;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < h; i += blockDim.x) {
+    float v = resid ? resid[(int64_t)t * h + i] : 0.f;
+    if (partial) v += gemm_load(partial, s, t, i);
+    if (resid) resid[(int64_t)t * h + i] = v;
+    if (feat) feat[(int64_t)t * ldf + i] = __float2bfloat16(v);
+    vals[i] = v;
+    ss += v * v;
+  }
+  const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
+  if (x)
+    for (int i = threadIdx.x; i < h; i += blockDim.x)
+      x[(int64_t)t * ldx + i] = __float2bfloat16(vals[i] * inv * __bfloat162float(w[i]));
+}
+
+// ------------------------------------------------------------- q/k/v + rope
+// One CTA per token row; one warp per head (d = 128, 4 values per lane).
+__global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int n_q, int n_kv,
+                                const __nv_bfloat16* __restrict__ qn, const __nv_bfloat16* __restrict__ kn, float eps,
+                                const float* __restrict__ inv_freq, const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
+                                const int32_t* __restrict__ qrow, __nv_bfloat16* q_out, int64_t q_tok_stride,
+                                __nv_bfloat16* kv, int64_t layer_off, const int32_t* __restrict__ page_table,
+                                int page_size, const int32_t* __restrict__ state, int state_c_idx) {
+  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nw = blockDim.x >> 5;
+  const int c0 = state ? state[state_c_idx] : 0;
+  const int p = pos[t] + c0;
+  const int sl = slot[t] == INT_MIN ? -1 : slot[t] + c0;
+  const int qr = qrow ? qrow[t] : t;
+  // rotary angles for this lane's 4 dims (i in [0,64) pairs with i+64)
+  float cs[4], sn[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int i = (lane * 4 + e) & 63;
+    const float ang = (float)p * inv_freq[i];
+    sincosf(ang, &sn[e], &cs[e]);
+  }
+  for (int hd = warp; hd < n_q + 2 * n_kv; hd += nw) {
+    const bool is_q = hd < n_q, is_k = !is_q && hd < n_q + n_kv;
+    if (is_q && qr < 0) continue;
+    if (!is_q && sl < 0) continue;
+    const int col0 = hd * 128 + lane * 4;
+    float v[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) v[e] = gemm_load(partial, s, t, col0 + e);
+    if (is_q || is_k) {
+      const __nv_bfloat16* nw_ = is_q ? qn : kn;
+      float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
+      ss = warp_sum(ss);
+      const float inv = rsqrtf(ss / 128.f + eps);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = v[e] * inv * __bfloat162float(nw_[lane * 4 + e]);
+      // rotate_half: lanes 0-15 hold dims 0-63, lanes 16-31 hold 64-127
+      float o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float partner = __shfl_xor_sync(0xffffffffu, v[e], 16);
+        o[e] = lane < 16 ? v[e] * cs[e] - partner * sn[e] : v[e] * cs[e] + partner * sn[e];
+      }
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v[e] = o[e];
+    }
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
+    if (is_q) {
+      __nv_bfloat16* dst = q_out + (int64_t)qr * q_tok_stride + hd * 128 + lane * 4;
+      *reinterpret_cast<__nv_bfloat162*>(dst) = lo;
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2) = hi;
+    } else {
+      const int head = is_k ? hd - n_q : hd - n_q - n_kv;
+      const int which = is_k ? 0 : 1;
+      const int64_t page = page_table[sl / page_size];
+      const int64_t off = ((page * 2 + which) * n_kv + head) * page_size + (sl % page_size);
+      __nv_bfloat16* dst = kv + layer_off + off * 128 + lane * 4;
+      *reinterpret_cast<__nv_bfloat162*>(dst) = lo;
+      *reinterpret_cast<__nv_bfloat162*>(dst + 2) = hi;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- swiglu
+__global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int ffn, __nv_bfloat16* act,
+                              int64_t lda) {
+  const int t = blockIdx.y;
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ffn; j += gridDim.x * blockDim.x) {
+    const float gt = gemm_load(partial, s, t, j);
+    const float up = gemm_load(partial, s, t, ffn + j);
+    const float si = gt / (1.f + __expf(-gt));
+    act[(int64_t)t * lda + j] = __float2bfloat16(si * up);
+  }
+}
+
+// ------------------------------------------------------------ gather rows
+__global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx,
+                                   const int32_t* __restrict__ count, int max_rows, int cols,
+                                   __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+  const int r = blockIdx.x;
+  const int n = count ? *count : max_rows;
+  const int4* sp = reinterpret_cast<const int4*>(src + (int64_t)(r < n ? idx[r] : 0) * lds);
+  int4* dp = reinterpret_cast<int4*>(dst + (int64_t)r * ldd);
+  for (int i = threadIdx.x; i < cols / 8; i += blockDim.x) dp[i] = r < n ? sp[i] : make_int4(0, 0, 0, 0);
+}
+
+}  // namespace bst
+
+// ------------------------------------------------------------------ C ABI
+using namespace bst;
+
+extern "C" int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* emb, int h, const void* w, float eps,
+                                 float* resid, void* x, int64_t ldx, bst_stream_t stream) {
+  BST_REQUIRE(tokens && emb && w && resid && x, "null pointer argument");
+  embed_rmsnorm_kernel<<<rows, E_THREADS, 0, as_stream(stream)>>>(
+      tokens, static_cast<const __nv_bfloat16*>(emb), h, static_cast<const __nv_bfloat16*>(w), eps, resid,
+      static_cast<__nv_bfloat16*>(x), ldx);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t* sched, float* resid, int rows, int h,
+                                    const void* w, float eps, void* x, int64_t ldx, void* feat, int64_t ldf,
+                                    bst_stream_t stream) {
+  BST_REQUIRE(h <= 8192, "hidden size > 8192 unsupported");
+  BST_REQUIRE(!partial || sched, "partial without schedule");
+  bst_gemm_sched_t s{};
+  if (sched) s = *sched;
+  residual_rmsnorm_kernel<<<rows, E_THREADS, 0, as_stream(stream)>>>(
+      partial, s, resid, h, static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
+      static_cast<__nv_bfloat16*>(feat), ldf, rows);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
+                            const void* q_norm, const void* k_norm, float eps, const float* inv_freq, const int32_t* pos,
+                            const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv,
+                            int64_t layer_off_elems, const int32_t* page_table, int page_size, const int32_t* state,
+                            int state_c_idx, bst_stream_t stream) {
+  BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
+              "null pointer argument");
+  BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
+  qkv_rope_kernel<<<rows, 512, 0, as_stream(stream)>>>(
+      partial, *sched, n_q, n_kv, static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm),
+      eps, inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride, static_cast<__nv_bfloat16*>(kv),
+      layer_off_elems, page_table, page_size, state, state_c_idx);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act,
+                          int64_t lda, bst_stream_t stream) {
+  BST_REQUIRE(partial && sched && act, "null pointer argument");
+  BST_REQUIRE(sched->n_out == 2 * ffn, "gate/up width mismatch");
+  dim3 grid((ffn + 255) / 256 < 48 ? (ffn + 255) / 256 : 48, rows);
+  swiglu_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, *sched, ffn, static_cast<__nv_bfloat16*>(act), lda);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx, const int32_t* count, int max_rows,
+                               int cols, void* dst, int64_t ldd, bst_stream_t stream) {
+  BST_REQUIRE(src && idx && dst, "null pointer argument");
+  BST_REQUIRE(cols % 8 == 0 && lds % 8 == 0 && ldd % 8 == 0, "rows must be 16-byte multiples");
+  gather_rows_kernel<<<max_rows, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(src), lds, idx, count,
+                                                              max_rows, cols, static_cast<__nv_bfloat16*>(dst), ldd);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+// ------------------------------------------------------ decode-state plumbing
+namespace bst {
+__global__ void verify_rows_kernel(const int32_t* state, const int32_t* tree_token, const int32_t* tree_depth,
+                                   const int32_t* meta, int rows, int32_t* tokens, int32_t* pos, int32_t* slot) {
+  const int n = meta[0];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
+    const bool real = i <= n;
+    tokens[i] = i == 0 ? state[BST_ST_BONUS] : (real ? tree_token[i] : 0);
+    pos[i] = real ? tree_depth[i] : 0;
+    slot[i] = i;
+  }
+}
+__global__ void drafter_rows_kernel(const int32_t* state, int gamma, int mask_token, int ctx_rows, int32_t* tokens,
+                                    int32_t* pos, int32_t* slot, int32_t* qrow) {
+  const int n_new = state[BST_ST_NNEW];
+  const int i = threadIdx.x;
+  if (i <= gamma) {
+    tokens[i] = i == 0 ? state[BST_ST_BONUS] : mask_token;
+    pos[i] = i;
+    slot[i] = i;
+    qrow[i] = i;
+  } else if (i < gamma + 1 + ctx_rows) {
+    const int j = i - gamma - 1;
+    tokens[i] = 0;
+    pos[i] = j - n_new;
+    slot[i] = j < n_new ? j - n_new : INT_MIN;
+    qrow[i] = -1;
+  }
+}
+__global__ void commit_state_kernel(int32_t* state, const int32_t* meta, const int32_t* committed, int max_path,
+                                    int32_t* out_tokens, int out_cap, const int32_t* tree_meta,
+                                    const double* surrogate, int32_t* log_i32, double* log_f64, int log_cap) {
+  const int len = meta[0];
+  const int base = state[BST_ST_COMMITTED];
+  for (int i = threadIdx.x; i < len && i < max_path; i += blockDim.x)
+    if (base + i < out_cap) out_tokens[base + i] = committed[i];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const int cyc = state[BST_ST_CYCLE];
+    if (log_i32 && cyc < log_cap) {
+      log_i32[cyc * 8 + 0] = tree_meta ? tree_meta[0] : -1;  // tree size N
+      log_i32[cyc * 8 + 1] = tree_meta ? tree_meta[1] : -1;  // nodes expanded
+      log_i32[cyc * 8 + 2] = tree_meta ? tree_meta[2] : -1;  // stop reason
+      log_i32[cyc * 8 + 3] = len;                            // accepted_len (incl. bonus)
+      log_i32[cyc * 8 + 4] = state[BST_ST_C];                // context c of this cycle
+      log_i32[cyc * 8 + 5] = meta[1];                        // bonus
+      if (log_f64) log_f64[cyc] = surrogate ? surrogate[0] : 0.0;
+    }
+    state[BST_ST_C] += len;
+    state[BST_ST_NNEW] = len;
+    state[BST_ST_BONUS] = meta[1];
+    state[BST_ST_COMMITTED] = base + len;
+    state[BST_ST_CYCLE] = cyc + 1;
+  }
+}
+}  // namespace bst
+
+extern "C" int bst_verify_rows(const int32_t* state, const int32_t* tree_token, const int32_t* tree_depth,
+                               const int32_t* meta, int rows, int32_t* tokens, int32_t* pos, int32_t* slot,
+                               bst_stream_t stream) {
+  BST_REQUIRE(state && tree_token && tree_depth && meta && tokens && pos && slot, "null pointer argument");
+  verify_rows_kernel<<<(rows + 255) / 256, 256, 0, as_stream(stream)>>>(state, tree_token, tree_depth, meta, rows,
+                                                                        tokens, pos, slot);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_drafter_rows(const int32_t* state, int gamma, int mask_token, int ctx_rows, int32_t* tokens,
+                                int32_t* pos, int32_t* slot, int32_t* qrow, bst_stream_t stream) {
+  BST_REQUIRE(state && tokens && pos && slot && qrow, "null pointer argument");
+  BST_REQUIRE(gamma + 1 + ctx_rows <= 1024, "too many drafter rows");
+  drafter_rows_kernel<<<1, 1024, 0, as_stream(stream)>>>(state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_commit_state(int32_t* state, const int32_t* accept_meta, const int32_t* committed, int max_path,
+                                int32_t* out_tokens, int out_cap, const int32_t* tree_meta, const double* surrogate,
+                                int32_t* log_i32, double* log_f64, int log_cap, bst_stream_t stream) {
+  BST_REQUIRE(state && accept_meta && committed && out_tokens, "null pointer argument");
+  commit_state_kernel<<<1, 128, 0, as_stream(stream)>>>(state, accept_meta, committed, max_path, out_tokens, out_cap,
+                                                        tree_meta, surrogate, log_i32, log_f64, log_cap);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}

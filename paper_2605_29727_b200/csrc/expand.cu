@@ -503,11 +503,32 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
   }
 }
 
+// Effective plan: optionally loaded from device memory and specialised to the
+// device-resident context c (LatencyCurve at c: cost_model.py:290-294 are
+// affine in c with exact integer slopes).
+__device__ __forceinline__ bst_plan_t resolve_plan(bst_plan_t plan, const bst_plan_t* plan_dev) {
+  if (plan_dev) {
+    const int32_t policy = plan.policy, n_max = plan.n_max;
+    plan = *plan_dev;
+    plan.policy = policy;
+    plan.n_max = n_max;
+  }
+  if (plan.state) {
+    const long long c = plan.state[plan.c_idx];
+    plan.curve.flops_lin += plan.d_flops_lin * c;
+    plan.curve.bytes_const += plan.d_bytes_const * c;
+    plan.curve.bytes_lin += plan.d_bytes_lin * c;
+  }
+  return plan;
+}
+
 __global__ void __launch_bounds__(EX_THREADS, 1)
     expand_best_first_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
-                             bst_plan_t plan, int n_cap, bst_tree_t out, ExWs ws, int heap_in_smem) {
+                             bst_plan_t plan_in, const bst_plan_t* plan_dev, int n_cap, bst_tree_t out, ExWs ws,
+                             int heap_in_smem) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
+  const bst_plan_t plan = resolve_plan(plan_in, plan_dev);
   const bool adaptive = plan.policy == BST_POLICY_ADAPTIVE;
   const int n_max = plan.n_max;
   const int limit = min(n_max, n_cap);
@@ -677,10 +698,38 @@ extern "C" int bst_expand(const int32_t* tok, const double* prob, int gamma, int
     expand_beam_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, n_cap, *out, w);
   } else {
     const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
-    expand_best_first_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, n_cap, *out, w, heap_in_smem);
+    expand_best_first_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, nullptr, n_cap, *out, w,
+                                                          heap_in_smem);
   }
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
 
 extern "C" double bst_curve_latency(const bst_curve_t* curve, int64_t s) { return bst::curve_latency(*curve, s); }
+
+extern "C" int bst_expand_dev(const int32_t* tok, const double* prob, int gamma, int k, const bst_plan_t* plan_dev,
+                              int policy, int n_max, int n_cap, const bst_tree_t* out, void* ws, size_t ws_bytes,
+                              bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(tok && prob && plan_dev && out, "null pointer argument");
+  BST_REQUIRE(policy == BST_POLICY_ADAPTIVE || policy == BST_POLICY_FIXED, "device plans support adaptive/fixed");
+  BST_REQUIRE(gamma >= 1 && gamma <= EX_MAXG && k >= 1 && k <= EX_MAXK, "bad lattice shape");
+  BST_REQUIRE(n_max >= 1 && n_max <= n_cap && n_cap < (1 << 20), "bad n_max/n_cap");
+  size_t need = 0;
+  ExWs w = ex_carve(ws, n_cap, &need);
+  BST_REQUIRE(ws != nullptr && ws_bytes >= need, "workspace too small: %zu < %zu", ws_bytes, need);
+  const size_t smem = sizeof(ExSmem);
+  static bool attr_done = false;
+  if (!attr_done) {
+    BST_CUDA(cudaFuncSetAttribute(expand_best_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done = true;
+  }
+  bst_plan_t p{};
+  p.policy = policy;
+  p.n_max = n_max;
+  const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
+  expand_best_first_kernel<<<1, EX_THREADS, smem, as_stream(stream)>>>(tok, prob, gamma, k, p, plan_dev, n_cap, *out,
+                                                                        w, heap_in_smem);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}

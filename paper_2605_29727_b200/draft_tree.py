@@ -181,3 +181,15 @@ def build_tree(lattice: CandidateLattice, paths: Sequence[Sequence[int]]) -> Dra
         seen[path] = node
     return DraftTree(nodes=tuple(nodes), lattice=lattice, surrogate=math.fsum(n.path_score for n in nodes),
                      method="manual")
+
+
+def expand_device_plan(tok: torch.Tensor, prob: torch.Tensor, plan_dev: torch.Tensor, policy: int, n_max: int,
+                       out: DeviceTree) -> DeviceTree:
+    """K2 with the plan read from device memory (re-plannable inside a captured graph)."""
+    gamma, k = tok.shape
+    need = _lib.lib().bst_expand_workspace(gamma, k, out.n_cap)
+    ws = workspace("expand", need)
+    st = out.struct()
+    _lib.call("bst_expand_dev", tok.data_ptr(), prob.data_ptr(), gamma, k, plan_dev.data_ptr(), policy, n_max,
+              out.n_cap, st, ws.data_ptr(), ws.numel(), stream_ptr())
+    return out

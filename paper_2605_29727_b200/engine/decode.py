@@ -1,0 +1,400 @@
+"""B200Engine — the on-device draft -> expand -> verify -> accept loop.
+
+One decode cycle (the reference's ``decode_full`` body, verify_sim.py:437-460):
+
+  [graph D]  drafter forward (K3/K4/K5) -> K1 top-K lattice -> K2 expand
+             (adaptive Algorithm 1 with the latency curve at the device-side
+             context c, or fixed-N best-first)
+  [host]     read the tree size N* (the only host sync of the cycle)
+  [graph V_b] verify rows -> target forward on s = N*+1 rows padded to the
+             bucket b (K4/K5/K3 with the ancestor bitmask) -> LM-head argmax
+             -> K6 accept walk -> KV compaction -> drafter feature gather ->
+             state update (c += accepted_len, pending bonus) + per-cycle log
+
+Both graphs read every per-cycle scalar from the device ``state`` vector, so
+they are captured once (V per 16-row bucket) and replayed.  CUDA events
+around the two graphs give T_draft/T_verify; the verify time feeds the
+estimator's online EMA (``VerifyLatencyEstimator.observe``, K7).
+
+The engine also implements the reference plugin protocol
+(``drafter_marginals`` / ``next_token`` / ``tree_argmax``) and the decode fast
+path (``engine_decode``) the façade's ``decode`` dispatches to.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .. import _lib, ops
+from ..controller import STOP_BUDGET_CAP
+from ..cost_model import CycleLatencies, VerifyLatencyEstimator
+from ..draft_tree import DeviceTree, expand_device_plan
+from ..lattice import MarginalBlock, topk_logits_into
+from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
+from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
+from .weights import DrafterWeights, TargetWeights
+
+ST_C, ST_NNEW, ST_BONUS, ST_COMMITTED, ST_CYCLE = 0, 1, 2, 3, 4
+MAX_ROWS = 256
+BUCKET = 16
+
+
+@dataclass
+class CycleStats:
+    tree_size: int
+    n_expanded: int
+    stop: int
+    accepted_len: int
+    context: int
+    bonus: int
+    surrogate: float
+    t_draft: float
+    t_verify: float
+
+
+class B200Engine:
+    """Qwen3-shape target + DFlash-style drafter, random-init bf16, one request per engine."""
+
+    def __init__(self, cfg: ModelConfig = QWEN3_8B, dcfg: DrafterConfig | None = None, max_ctx: int = 4096,
+                 seed: int = 0, n_cap: int = MAX_ROWS - 1, top_k: int = 8, device=None, max_cycles: int = 4096):
+        if not torch.cuda.is_available():
+            raise RuntimeError("B200Engine needs a CUDA device; there is no CPU fallback")
+        self.dev = torch.device(device or "cuda")
+        torch.cuda.set_device(self.dev)
+        self.cfg = cfg
+        dcfg = dcfg or DrafterConfig()
+        feat = dcfg.feat_layers or default_feat_layers(cfg.L)
+        self.dcfg = DrafterConfig(layers=dcfg.layers, gamma=dcfg.gamma, feat_layers=feat, mask_token=dcfg.mask_token,
+                                  logit_scale=dcfg.logit_scale)
+        self.gamma, self.top_k = self.dcfg.gamma, top_k
+        self.n_cap = min(n_cap, MAX_ROWS - 1)
+        self.max_ctx = max_ctx
+        slots = max_ctx + MAX_ROWS + PAGE
+        self.tw = TargetWeights.random(cfg, seed, self.dev)
+        self.dw = DrafterWeights.random(cfg, self.dcfg, len(feat), seed, self.dev)
+        self.target = TargetModel(cfg, self.tw, slots, MAX_ROWS, feat, self.dev)
+        self.drafter = DrafterModel(cfg, self.dcfg, self.dw, self.tw, slots, len(feat), self.dev)
+        i32 = dict(dtype=torch.int32, device=self.dev)
+        self.state = torch.zeros(8, **i32)
+        self.out_tokens = torch.zeros(max_ctx + MAX_ROWS, **i32)
+        self.lat_tok = torch.zeros(self.gamma, top_k, **i32)
+        self.lat_prob = torch.zeros(self.gamma, top_k, dtype=torch.float64, device=self.dev)
+        self.probs_full = None  # fp64 [gamma, V] when export is on
+        self.tree = DeviceTree(self.n_cap, self.dev)
+        self.path = torch.zeros(self.gamma + 1, **i32)
+        self.committed = torch.zeros(self.gamma + 1, **i32)
+        self.acc_meta = torch.zeros(4, **i32)
+        self.log_i32 = torch.zeros(max_cycles * 8, **i32)
+        self.log_f64 = torch.zeros(max_cycles, dtype=torch.float64, device=self.dev)
+        self.plan_dev = torch.zeros(C.sizeof(_lib.Plan), dtype=torch.uint8, device=self.dev)
+        self.plan_host = torch.zeros(C.sizeof(_lib.Plan), dtype=torch.uint8).pin_memory()
+        self.meta_host = torch.zeros(16, dtype=torch.int32).pin_memory()
+        self.stream = torch.cuda.Stream(self.dev)
+        self.graph_d = None
+        self.graphs_v: dict[int, torch.cuda.CUDAGraph] = {}
+        self.graph_ar = None
+        self.policy = (_lib.POLICY_FIXED, 64)
+        self.prompt_len = 0
+        self.use_graphs = True
+        self.export = False  # debug: keep fp64 drafter rows + verify argmax per cycle (parity tests)
+        self.exported: list[dict] = []
+        self.draft_override = None
+        torch.cuda.synchronize()
+
+    # ------------------------------------------------------------------ setup
+    def reset(self, prompt) -> None:
+        """Prefill prompt[:-1] (causal, chunks of 256) and make prompt[-1] the pending root."""
+        prompt = [int(t) for t in prompt]
+        if not prompt:
+            raise ValueError("prompt must contain at least one token")
+        P = len(prompt)
+        if P + MAX_ROWS > self.max_ctx + MAX_ROWS:
+            raise ValueError("prompt longer than max_ctx")
+        self.prompt_len = P
+        with torch.cuda.stream(self.stream):
+            t, d = self.target, self.drafter
+            for start in range(0, P - 1, MAX_ROWS):
+                n = min(MAX_ROWS, P - 1 - start)
+                self.state.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+                t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
+                ar = torch.arange(n, dtype=torch.int32, device=self.dev)
+                t.pos[:n].copy_(ar)
+                t.slot[:n].copy_(ar)
+                t.forward(n, self.state, MODE_CAUSAL, keys_after_c=n, head=None, c_host=start)
+                d.feat_in[:n].copy_(t.feat[:n])
+                d.pos[:n].copy_(ar)
+                d.slot[:n].copy_(ar)
+                d.prefill_ctx(n, self.state)
+            self.state.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+        self.stream.synchronize()
+        self.exported = []
+
+    def set_policy(self, kind: str, n: int = 0, estimator: VerifyLatencyEstimator | None = None,
+                   latencies: CycleLatencies | None = None, n_max: int | None = None) -> None:
+        """Adaptive (Algorithm 1 on the device) or fixed-N best-first."""
+        cfg = self.cfg
+        if kind == "fixed":
+            if not 1 <= n <= self.n_cap:
+                raise ValueError(f"fixed budget must be in [1, {self.n_cap}]")
+            self.policy = (_lib.POLICY_FIXED, n)
+            plan = _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n)
+        elif kind == "adaptive":
+            if estimator is None or latencies is None:
+                raise ValueError("adaptive policy needs an estimator and cycle latencies")
+            n_max = min(n_max or self.n_cap, self.n_cap)
+            curve = estimator.curve(0).device_struct()
+            p = estimator.params
+            plan = _lib.Plan(policy=_lib.POLICY_ADAPTIVE, n_max=n_max, curve=curve,
+                             fixed_cost=latencies.t_draft + latencies.t_aux, l_ar=latencies.l_ar,
+                             state=self.state.data_ptr(), c_idx=ST_C, d_flops_lin=4 * p.L * p.h_q,
+                             d_bytes_const=p.bp * p.L * 2 * p.h_kv, d_bytes_lin=p.bp * p.L * 2 * p.n_q)
+            self.policy = (_lib.POLICY_ADAPTIVE, n_max)
+        else:
+            raise ValueError(f"unsupported engine policy {kind!r} (beam/greedy run through the façade)")
+        raw = bytes(plan)
+        self.plan_host.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
+        with torch.cuda.stream(self.stream):
+            self.plan_dev.copy_(self.plan_host, non_blocking=True)
+        self.graph_d = None  # policy/n_max are launch parameters of K2
+
+    # --------------------------------------------------------------- phases
+    def _draft_body(self) -> None:
+        if self.draft_override is not None:  # test hook: externally supplied drafter logits [gamma, V]
+            logits = self.draft_override(self)
+        else:
+            logits = self.drafter.forward(self.state)
+        topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
+        expand_device_plan(self.lat_tok, self.lat_prob, self.plan_dev, self.policy[0], self.policy[1], self.tree)
+
+    def _verify_body(self, rows: int) -> None:
+        t, d, tr = self.target, self.drafter, self.tree
+        ops.verify_rows(self.state, tr.token, tr.depth, tr.meta, rows, t.tokens, t.pos, t.slot)
+        t.forward(rows, self.state, MODE_TREE, keys_after_c=rows, anc=tr.anc_mask, mask_words=tr.mask_words,
+                  head="argmax")
+        from ..verify_sim import accept_device
+        accept_device(tr.token, tr.child_start, tr.child_list, t.argmax, self.gamma + 1, self.path, self.committed,
+                      self.acc_meta)
+        kv = t.kv
+        ops.kv_compact(kv.buf, self.cfg.L, self.cfg.n_kv, PAGE, kv.layer_stride, kv.page_table, self.state, self.path,
+                       self.acc_meta, self.gamma + 1)
+        ops.gather_rows(t.feat, self.path, self.acc_meta, d.CR, d.feat_in)
+        ops.commit_state(self.state, self.acc_meta, self.committed, self.gamma + 1, self.out_tokens, tr.meta,
+                         tr.surrogate, self.log_i32, self.log_f64)
+
+    def _bucket(self, n_nodes: int) -> int:
+        return min(MAX_ROWS, ((n_nodes + 1 + BUCKET - 1) // BUCKET) * BUCKET)
+
+    def _capture(self, fn) -> torch.cuda.CUDAGraph:
+        # warm-up run outside the graph (kernel attributes, tensor maps, workspaces), then capture
+        saved = self.state.clone()
+        with torch.cuda.stream(self.stream):
+            fn()
+        self.stream.synchronize()
+        self.state.copy_(saved)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream):
+            fn()
+        self.stream.synchronize()
+        self.state.copy_(saved)
+        torch.cuda.synchronize()
+        return g
+
+    def _run_draft(self) -> None:
+        if not self.use_graphs or self.export or self.draft_override is not None:
+            with torch.cuda.stream(self.stream):
+                self._draft_body()
+            return
+        if self.graph_d is None:
+            self.graph_d = self._capture(self._draft_body)
+        with torch.cuda.stream(self.stream):
+            self.graph_d.replay()
+
+    def _run_verify(self, rows: int) -> None:
+        if not self.use_graphs or self.export:
+            with torch.cuda.stream(self.stream):
+                self._verify_body(rows)
+            return
+        g = self.graphs_v.get(rows)
+        if g is None:
+            g = self.graphs_v[rows] = self._capture(lambda: self._verify_body(rows))
+        with torch.cuda.stream(self.stream):
+            g.replay()
+
+    # --------------------------------------------------------------- decode
+    def draft(self, events=None) -> tuple[int, int]:
+        """Phase 1 (graph D) + the cycle's single host sync.
+
+        Returns (tree size N*, tokens committed before this cycle)."""
+        st = self.stream
+        if events:
+            events[0].record(st)
+        if self.export:
+            self.probs_full = torch.empty(self.gamma, self.cfg.V, dtype=torch.float64, device=self.dev)
+        self._run_draft()
+        if events:
+            events[1].record(st)
+        with torch.cuda.stream(st):
+            self.meta_host[:8].copy_(self.tree.meta, non_blocking=True)
+            self.meta_host[8:].copy_(self.state, non_blocking=True)
+        st.synchronize()
+        return int(self.meta_host[0]), int(self.meta_host[8 + ST_COMMITTED])
+
+    def verify(self, n_nodes: int, events=None) -> None:
+        """Phase 2 (graph V_bucket): verify, accept, compact, commit — asynchronous."""
+        if self.export:
+            self._export_pre(n_nodes)
+        self._run_verify(self._bucket(n_nodes))
+        if events:
+            events[2].record(self.stream)
+        if self.export:
+            self._export_post(n_nodes)
+
+    def cycle(self, events=None) -> int:
+        """One draft->expand->verify->accept cycle; returns the tree size N*."""
+        n_nodes, _ = self.draft(events)
+        self.verify(n_nodes, events)
+        return n_nodes
+
+    def _export_pre(self, n: int) -> None:
+        tr = self.tree
+        self.exported.append(dict(
+            probs=self.probs_full.cpu().numpy(), tok=self.lat_tok.cpu().numpy(), prob=self.lat_prob.cpu().numpy(),
+            parent=tr.parent[: n + 1].cpu().numpy(), depth=tr.depth[: n + 1].cpu().numpy(),
+            token=tr.token[: n + 1].cpu().numpy(), rho=tr.rho[: n + 1].cpu().numpy(),
+            meta=tr.meta.cpu().numpy(), trace=tr.trace[: int(tr.meta[1].item())].cpu().numpy(),
+            surrogate=float(tr.surrogate.item()), c=int(self.state[ST_C].item())))
+
+    def _export_post(self, n: int) -> None:
+        self.stream.synchronize()
+        e = self.exported[-1]
+        e["argmax"] = self.target.argmax[: n + 1].cpu().numpy()
+        e["path"] = self.path[: int(self.acc_meta[0].item())].cpu().numpy()
+        e["bonus"] = int(self.acc_meta[1].item())
+
+    def run(self, max_new_tokens: int, timing: bool = True) -> tuple[list[CycleStats], list[int]]:
+        """Decode until >= max_new_tokens tokens are committed (the reference loop condition)."""
+        stats_t: list = []
+        while True:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timing else None
+            n_nodes, committed = self.draft(ev)  # committed count is read at the cycle's one sync
+            if committed >= max_new_tokens:
+                break  # the speculative draft of a cycle that will not run is discarded
+            self.verify(n_nodes, ev)
+            stats_t.append(ev)
+        self.stream.synchronize()
+        return self.read_log(stats_t), self.tokens()
+
+    def read_log(self, events=None) -> list[CycleStats]:
+        self.stream.synchronize()
+        ncyc = int(self.state[ST_CYCLE].item())
+        li = self.log_i32[: ncyc * 8].view(ncyc, 8).cpu().numpy()
+        lf = self.log_f64[:ncyc].cpu().numpy()
+        out = []
+        for i in range(ncyc):
+            td = tv = float("nan")
+            if events and i < len(events) and events[i]:
+                e = events[i]
+                td = e[0].elapsed_time(e[1]) * 1e-3
+                tv = e[1].elapsed_time(e[2]) * 1e-3
+            out.append(CycleStats(int(li[i, 0]), int(li[i, 1]), int(li[i, 2]), int(li[i, 3]), int(li[i, 4]),
+                                  int(li[i, 5]), float(lf[i]), td, tv))
+        return out
+
+    def tokens(self) -> list[int]:
+        n = int(self.state[ST_COMMITTED].item())
+        return self.out_tokens[:n].cpu().tolist()
+
+    # ------------------------------------------------------- AR reference
+    def ar_step_body(self) -> None:
+        """One autoregressive target step on the pending root (s = 1)."""
+        t = self.target
+        t.tokens[:1].copy_(self.state[ST_BONUS:ST_BONUS + 1])
+        t.pos[:1].zero_()
+        t.slot[:1].zero_()
+        t.forward(1, self.state, MODE_CAUSAL, keys_after_c=1, head="argmax")
+        # commit: c += 1, root <- argmax
+        self.state[ST_C:ST_C + 1].add_(1)
+        self.state[ST_BONUS:ST_BONUS + 1].copy_(t.argmax[:1])
+
+    def ar_decode(self, n_tokens: int) -> list[int]:
+        out = []
+        with torch.cuda.stream(self.stream):
+            for _ in range(n_tokens):
+                self.ar_step_body()
+                out.append(self.target.argmax[:1].clone())
+        self.stream.synchronize()
+        return [int(x.item()) for x in out]
+
+    def measure_ar_step(self, iters: int = 10) -> float:
+        """CUDA-event latency of one AR target step (the l_ar of Algorithm 1)."""
+        saved = self.state.clone()
+        if self.graph_ar is None:
+            self.graph_ar = self._capture(self.ar_step_body)
+        ts = []
+        for _ in range(iters + 3):
+            self.state.copy_(saved)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(self.stream)
+            with torch.cuda.stream(self.stream):
+                self.graph_ar.replay()
+            b.record(self.stream)
+            b.synchronize()
+            ts.append(a.elapsed_time(b) * 1e-3)
+        self.state.copy_(saved)
+        torch.cuda.synchronize()
+        return float(np.median(ts[3:]))
+
+    # --------------------------------------------------- plugin protocol
+    def engine_decode(self, sim_cfg, policy, estimator: VerifyLatencyEstimator):
+        """Fast path of the façade's ``decode`` (verify_sim.py:464): the loop runs on the device.
+
+        The context of every cycle is the engine's KV length c (= prompt_len - 1 +
+        committed), the reference's ``context_len + len(prefix)`` under the
+        alignment contract (SURVEY §8a′); the SimConfig's latencies drive Algorithm 1.
+        """
+        from ..verify_sim import CycleRecord
+        lat = sim_cfg.controller.latencies
+        if policy.kind == "adaptive":
+            self.set_policy("adaptive", estimator=estimator, latencies=lat, n_max=sim_cfg.controller.n_max)
+        elif policy.kind == "fixed":
+            self.set_policy("fixed", n=policy.n)
+        else:
+            raise ValueError("engine fast path supports adaptive and fixed-N policies")
+        if sim_cfg.top_k != self.top_k:
+            raise ValueError(f"engine was built with top_k={self.top_k}")
+        stats, toks = self.run(sim_cfg.run_length)
+        records = []
+        for st in stats:
+            if not np.isnan(st.t_verify):
+                estimator.observe(st.tree_size + 1, st.context, st.t_verify)
+            t_verify = estimator.estimate_for_budget(st.tree_size, st.context)
+            cyc = lat.t_draft + t_verify + lat.t_aux
+            records.append(CycleRecord(tree_size=st.tree_size, accepted_len=st.accepted_len, surrogate=st.surrogate,
+                                       t_draft=lat.t_draft, t_verify=t_verify, t_aux=lat.t_aux, l_ar=lat.l_ar,
+                                       cycle_speedup=st.accepted_len * lat.l_ar / cyc))
+        return records, tuple(toks)
+
+    def drafter_marginals(self, prefix) -> MarginalBlock:
+        """fp64 drafter rows for the engine's current state (prefix must be its committed stream)."""
+        self._check_prefix(prefix)
+        self.probs_full = torch.empty(self.gamma, self.cfg.V, dtype=torch.float64, device=self.dev)
+        with torch.cuda.stream(self.stream):
+            logits = self.drafter.forward(self.state)
+            topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
+        self.stream.synchronize()
+        return MarginalBlock(gamma=self.gamma, vocab_size=self.cfg.V, probs=self.probs_full.cpu().numpy())
+
+    def _check_prefix(self, prefix) -> None:
+        if tuple(prefix) != tuple(self.tokens()):
+            raise ValueError("engine plugin: prefix does not match the engine's committed stream")
+
+    def __repr__(self) -> str:  # pragma: no cover
+        return f"B200Engine({self.cfg.name}, gamma={self.gamma}, top_k={self.top_k}, n_cap={self.n_cap})"
+
+
+def default_stop_name(stop: int) -> str:
+    return _lib.STOP_NAMES.get(stop, STOP_BUDGET_CAP)

@@ -1,0 +1,202 @@
+"""Target verify forward and DFlash-style drafter forward over the C-ABI kernels.
+
+Every launch goes to the current torch stream and reads its per-cycle scalars
+(context length c, pending drafter rows, bonus token) from the device-resident
+decode ``state`` — so both forwards can be captured once in a CUDA graph and
+replayed every cycle without a host round trip.
+
+Per target layer (s rows):
+  qkv  = K4(x)                     -> K5 qkv_rope: q/k norm, RoPE(c+depth), KV append at c+row
+  attn = K3(q, paged KV, ancestor bitmask)
+  o    = K4(attn)                  -> K5 residual += o; x = RMSNorm
+  gu   = K4(x)                     -> K5 SwiGLU
+  dn   = K4(act)                   -> K5 residual += dn; x = RMSNorm(next); tap features
+LM head: K4 -> per-row argmax (numpy tie-break) or fp32 logits.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from .. import ops
+from .config import DrafterConfig, ModelConfig
+from .weights import DrafterWeights, TargetWeights, rope_inv_freq
+
+PAGE = 64
+MODE_TREE, MODE_CAUSAL, MODE_FULL = 0, 1, 2
+SKIP_SLOT = -(2**31)
+
+
+class PagedKV:
+    """[layer][page][K|V][n_kv][64][128] bf16, zero-initialised (masked slots stay finite)."""
+
+    def __init__(self, n_layers: int, n_kv: int, max_slots: int, dev) -> None:
+        self.n_layers, self.n_kv = n_layers, n_kv
+        self.n_pages = (max_slots + PAGE - 1) // PAGE
+        self.layer_stride = self.n_pages * 2 * n_kv * PAGE * 128
+        self.buf = torch.zeros(n_layers * self.layer_stride, dtype=torch.bfloat16, device=dev)
+        self.page_table = torch.arange(self.n_pages, dtype=torch.int32, device=dev)
+
+    @property
+    def max_slots(self) -> int:
+        return self.n_pages * PAGE
+
+
+def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
+    g = cfg.n_q // cfg.n_kv
+    best = 0
+    for s in range(1, max_rows + 1):
+        rb = math.ceil(g * s / 128)
+        splits = max(1, 148 // (cfg.n_kv * rb))
+        splits = min(splits, pages)
+        pps = math.ceil(pages / splits)
+        splits = math.ceil(pages / pps)
+        if splits > 1:
+            best = max(best, splits * s * cfg.n_q * 130)
+    return max(best, 1)
+
+
+def _max_partial(shapes, max_rows: int) -> int:
+    return max(ops.gemm_schedule(n, k, max_rows).partial_floats for n, k in shapes)
+
+
+class TargetModel:
+    def __init__(self, cfg: ModelConfig, w: TargetWeights, max_slots: int, max_rows: int, feat_layers, dev) -> None:
+        self.cfg, self.w, self.dev, self.max_rows = cfg, w, dev, max_rows
+        self.kv = PagedKV(cfg.L, cfg.n_kv, max_slots, dev)
+        self.inv_freq = rope_inv_freq(cfg, dev)
+        self.feat_layers = tuple(feat_layers)
+        R, h = max_rows, cfg.h
+        f32, bf = dict(dtype=torch.float32, device=dev), dict(dtype=torch.bfloat16, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.resid = torch.empty(R, h, **f32)
+        self.x = torch.empty(R, h, **bf)
+        self.q = torch.empty(R, cfg.h_q, **bf)
+        self.attn = torch.empty(R, cfg.h_q, **bf)
+        self.act = torch.empty(R, cfg.h_ffn, **bf)
+        self.feat = torch.empty(R, max(1, len(self.feat_layers)) * h, **bf)
+        self.tokens = torch.zeros(R, **i32)
+        self.pos = torch.zeros(R, **i32)
+        self.slot = torch.zeros(R, **i32)
+        self.argmax = torch.zeros(R, **i32)
+        self.amx_scratch = torch.zeros(R, dtype=torch.int64, device=dev)
+        shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h)]
+        self.partial = torch.empty(_max_partial(shapes, R), **f32)
+        self.attn_ws = torch.empty(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
+        self.logits = None
+
+    def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
+                head: str | None = "argmax", c_host: int = 0) -> None:
+        """Run `rows` query rows (tokens/pos/slot buffers already filled, relative to c = state[0])."""
+        cfg, w, kv = self.cfg, self.w, self.kv
+        n, eps = rows, cfg.eps
+        x, resid = self.x[:n], self.resid[:n]
+        ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
+        for li, lw in enumerate(w.layers):
+            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
+            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
+                         None, self.q, kv.buf, li * kv.layer_stride, kv.page_table, PAGE, state)
+            ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, kv.page_table, cfg.n_q,
+                          cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
+                          self.attn_ws)
+            p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
+            ops.residual_rmsnorm(p, resid, n, cfg.h, lw.post_norm, eps, x=x)
+            p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
+            ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
+            p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
+            nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
+            feat = None
+            if li in self.feat_layers:
+                j = self.feat_layers.index(li)
+                feat = self.feat[:n, j * cfg.h:(j + 1) * cfg.h]
+            ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
+        if head == "argmax":
+            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
+            ops.gemm_argmax(p, out=self.argmax[:n], scratch=self.amx_scratch)
+        elif head == "logits":
+            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
+            self.logits = ops.gemm_reduce(p)
+
+
+class DrafterModel:
+    """Block drafter: gamma+1 query rows ([bonus] + gamma masks) + gamma+1 context rows."""
+
+    def __init__(self, cfg: ModelConfig, dcfg: DrafterConfig, w: DrafterWeights, target: TargetWeights,
+                 max_slots: int, n_feat: int, dev, prefill_rows: int = 256) -> None:
+        self.cfg, self.dcfg, self.w, self.tw, self.dev = cfg, dcfg, w, target, dev
+        self.kv = PagedKV(dcfg.layers, cfg.n_kv, max_slots, dev)
+        self.inv_freq = rope_inv_freq(cfg, dev)
+        self.B = dcfg.gamma + 1
+        self.CR = dcfg.gamma + 1
+        self.mask_token = dcfg.mask_token if dcfg.mask_token >= 0 else cfg.V - 1
+        R = max(self.B + self.CR, prefill_rows)
+        h = cfg.h
+        f32, bf = dict(dtype=torch.float32, device=dev), dict(dtype=torch.bfloat16, device=dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.resid = torch.empty(self.B, h, **f32)
+        self.X = torch.zeros(R, h, **bf)
+        self.q = torch.empty(self.B, cfg.h_q, **bf)
+        self.attn = torch.empty(self.B, cfg.h_q, **bf)
+        self.act = torch.empty(self.B, cfg.h_ffn, **bf)
+        self.feat_in = torch.zeros(max(self.CR, prefill_rows), n_feat * h, **bf)
+        self.tokens = torch.zeros(R, **i32)
+        self.pos = torch.zeros(R, **i32)
+        self.slot = torch.zeros(R, **i32)
+        self.qrow = torch.zeros(R, **i32)
+        shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h), (h, n_feat * h)]
+        self.partial = torch.empty(_max_partial(shapes, R), **f32)
+        self.attn_ws = torch.empty(_attn_ws_floats(cfg, self.B, self.kv.n_pages), **f32)
+        self.logits = torch.empty(dcfg.gamma, cfg.V, **f32)
+
+    def _ctx_rows(self, n: int, x_ctx: torch.Tensor, state: torch.Tensor) -> None:
+        """fc + hidden_norm of n feature rows -> x_ctx (context inputs of every drafter layer)."""
+        cfg = self.cfg
+        p = ops.gemm_partial(self.feat_in[:n], self.w.fc, out=self.partial)
+        ops.residual_rmsnorm(p, None, n, cfg.h, self.w.hidden_norm, cfg.eps, x=x_ctx)
+
+    def prefill_ctx(self, n: int, state: torch.Tensor) -> None:
+        """Write context K/V for n prompt rows (features in feat_in[:n], pos/slot = 0..n-1 relative to c)."""
+        cfg = self.cfg
+        x = self.X[:n]
+        self._ctx_rows(n, x, state)
+        self.qrow[:n].fill_(-1)
+        for li, lw in enumerate(self.w.layers):
+            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
+            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, cfg.eps, self.inv_freq, self.pos,
+                         self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, self.kv.page_table,
+                         PAGE, state)
+
+    def forward(self, state: torch.Tensor) -> torch.Tensor:
+        """Draft one block: returns logits [gamma, V] fp32 for future positions c+1..c+gamma."""
+        cfg, w, B, CR = self.cfg, self.w, self.B, self.CR
+        eps, M = cfg.eps, B + CR
+        ops.drafter_rows(state, self.dcfg.gamma, self.mask_token, CR, self.tokens, self.pos, self.slot, self.qrow)
+        self._ctx_rows(CR, self.X[B:M], state)
+        xb, resid = self.X[:B], self.resid
+        ops.embed_rmsnorm(self.tokens, B, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
+        for li, lw in enumerate(w.layers):
+            p = ops.gemm_partial(self.X[:M], lw.qkv, out=self.partial)
+            ops.qkv_rope(p, M, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
+                         self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, self.kv.page_table, PAGE, state)
+            ops.attention(self.q, self.attn, self.kv.buf, self.dcfg.layers, self.kv.n_pages, li, self.kv.page_table,
+                          cfg.n_q, cfg.n_kv, B, 0, B, self.kv.max_slots, state, MODE_FULL, None, 0, self.attn_ws)
+            p = ops.gemm_partial(self.attn, lw.o, out=self.partial)
+            ops.residual_rmsnorm(p, resid, B, cfg.h, lw.post_norm, eps, x=xb)
+            p = ops.gemm_partial(xb, lw.gate_up, out=self.partial)
+            ops.swiglu(p, B, cfg.h_ffn, self.act)
+            p = ops.gemm_partial(self.act, lw.down, out=self.partial)
+            nxt = w.layers[li + 1].in_norm if li + 1 < len(w.layers) else w.final_norm
+            ops.residual_rmsnorm(p, resid, B, cfg.h, nxt, eps, x=xb)
+        p = ops.gemm_partial(self.X[1:B], self.tw.lm_head, out=self.partial)
+        _reduce_into(p, self.logits)
+        return self.logits
+
+
+def _reduce_into(p: ops.PartialOut, y: torch.Tensor) -> None:
+    import ctypes as C
+
+    from .. import _lib
+    from ..device import stream_ptr
+    _lib.call("bst_gemm_reduce", p.buf.data_ptr(), C.byref(p.sched), y.data_ptr(), None, y.stride(0), stream_ptr())

@@ -197,3 +197,14 @@ def block_from_rows(rows: Sequence[Sequence[float]]) -> MarginalBlock:
     if probs.ndim != 2:
         raise ValueError("rows must be a 2-D table")
     return MarginalBlock(gamma=probs.shape[0], vocab_size=probs.shape[1], probs=probs)
+
+
+def topk_logits_into(logits: torch.Tensor, k: int, tok: torch.Tensor, prob: torch.Tensor,
+                     full: torch.Tensor | None = None) -> None:
+    """K1 into caller-owned buffers (graph-capturable; workspace must already be sized)."""
+    gamma, vocab = logits.shape
+    dtype = {torch.float32: 0, torch.bfloat16: 1}[logits.dtype]
+    need = _lib.lib().bst_topk_workspace(gamma, vocab, k)
+    ws = workspace("topk", need)
+    _lib.call("bst_topk_logits", logits.data_ptr(), dtype, gamma, vocab, logits.stride(0), k, tok.data_ptr(),
+              prob.data_ptr(), None if full is None else full.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())

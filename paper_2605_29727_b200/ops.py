@@ -63,3 +63,68 @@ def gemm_argmax(p: PartialOut, out: torch.Tensor | None = None, scratch: torch.T
     scratch = scratch if scratch is not None else torch.empty(s.m, dtype=torch.int64, device=p.buf.device)
     _lib.call("bst_gemm_argmax", p.buf.data_ptr(), C.byref(s), scratch.data_ptr(), out.data_ptr(), stream_ptr())
     return out
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def attention(q, out, kv, n_layers, n_pages, layer, page_table, n_q, n_kv, s, c, keys_after_c, max_keys, state,
+              mode, anc=None, mask_words=0, ws=None, n_splits=0):
+    """K3 launch; q/out [s][n_q*128] bf16 (token stride = row stride)."""
+    _lib.call("bst_attention", q.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0), kv.data_ptr(), n_layers,
+              n_pages, layer, page_table.data_ptr(), n_q, n_kv, s, c, keys_after_c, max_keys, _p(state), 0, mode,
+              _p(anc), mask_words, n_splits, _p(ws), 0 if ws is None else ws.numel() * 4, stream_ptr())
+
+
+def embed_rmsnorm(tokens, rows, emb, w, eps, resid, x):
+    _lib.call("bst_embed_rmsnorm", tokens.data_ptr(), rows, emb.data_ptr(), emb.shape[1], w.data_ptr(),
+              C.c_float(eps), resid.data_ptr(), x.data_ptr(), x.stride(0), stream_ptr())
+
+
+def residual_rmsnorm(p: PartialOut | None, resid, rows, h, w, eps, x=None, feat=None):
+    sched = C.byref(p.sched) if p is not None else None
+    _lib.call("bst_residual_rmsnorm", None if p is None else p.buf.data_ptr(), sched, _p(resid), rows, h,
+              w.data_ptr(), C.c_float(eps), _p(x), 0 if x is None else x.stride(0), _p(feat),
+              0 if feat is None else feat.stride(0), stream_ptr())
+
+
+def qkv_rope(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv, layer_off,
+             page_table, page_size, state):
+    _lib.call("bst_qkv_rope", p.buf.data_ptr(), C.byref(p.sched), rows, n_q, n_kv, q_norm.data_ptr(),
+              k_norm.data_ptr(), C.c_float(eps), inv_freq.data_ptr(), pos.data_ptr(), slot.data_ptr(), _p(qrow),
+              q_out.data_ptr(), q_out.stride(0), kv.data_ptr(), layer_off, page_table.data_ptr(), page_size,
+              _p(state), 0, stream_ptr())
+
+
+def swiglu(p: PartialOut, rows, ffn, act):
+    _lib.call("bst_swiglu", p.buf.data_ptr(), C.byref(p.sched), rows, ffn, act.data_ptr(), act.stride(0),
+              stream_ptr())
+
+
+def gather_rows(src, idx, count, max_rows, dst):
+    _lib.call("bst_gather_rows", src.data_ptr(), src.stride(0), idx.data_ptr(), _p(count), max_rows, src.shape[1],
+              dst.data_ptr(), dst.stride(0), stream_ptr())
+
+
+def kv_compact(kv, n_layers, n_kv, page_size, layer_stride, page_table, state, path, meta, max_path):
+    _lib.call("bst_kv_compact", kv.data_ptr(), n_layers, n_kv, 128, page_size, layer_stride, page_table.data_ptr(),
+              state.data_ptr(), path.data_ptr(), meta.data_ptr(), max_path, stream_ptr())
+
+
+def verify_rows(state, tree_token, tree_depth, meta, rows, tokens, pos, slot):
+    _lib.call("bst_verify_rows", state.data_ptr(), tree_token.data_ptr(), tree_depth.data_ptr(), meta.data_ptr(),
+              rows, tokens.data_ptr(), pos.data_ptr(), slot.data_ptr(), stream_ptr())
+
+
+def drafter_rows(state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow):
+    _lib.call("bst_drafter_rows", state.data_ptr(), gamma, mask_token, ctx_rows, tokens.data_ptr(), pos.data_ptr(),
+              slot.data_ptr(), qrow.data_ptr(), stream_ptr())
+
+
+def commit_state(state, accept_meta, committed, max_path, out_tokens, tree_meta=None, surrogate=None, log_i32=None,
+                 log_f64=None):
+    cap = 0 if log_i32 is None else log_i32.numel() // 8
+    _lib.call("bst_commit_state", state.data_ptr(), accept_meta.data_ptr(), committed.data_ptr(), max_path,
+              out_tokens.data_ptr(), out_tokens.numel(), _p(tree_meta), _p(surrogate), _p(log_i32), _p(log_f64), cap,
+              stream_ptr())

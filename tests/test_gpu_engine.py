@@ -1,0 +1,179 @@
+"""End-to-end engine tests on the tiny config (C1): GPU forward vs the torch
+oracle, planning bit-parity given the GPU-exported logits, and KV compaction
+correctness through greedy-output preservation."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import specplan_port as O
+
+pytestmark = pytest.mark.gpu
+
+GAMMA = 8
+
+
+@pytest.fixture(scope="module")
+def eng():
+    from paper_2605_29727_b200.engine.config import TINY, DrafterConfig
+    from paper_2605_29727_b200.engine.decode import B200Engine
+    return B200Engine(TINY, DrafterConfig(layers=2, gamma=GAMMA, logit_scale=4.0), max_ctx=640, seed=0, n_cap=64)
+
+
+@pytest.fixture(scope="module")
+def ref(eng):
+    from oracle.model_ref import RefModel
+    return RefModel(eng.cfg, eng.tw, eng.dw, eng.target.feat_layers, eng.target.inv_freq)
+
+
+def _prompt(n, V, seed=0):
+    return np.random.default_rng(seed).integers(0, V - 1, n).tolist()
+
+
+def test_forward_matches_oracle(eng, ref):
+    from oracle.model_ref import causal_mask, verify_mask
+    prompt = _prompt(300, eng.cfg.V)  # > 256: exercises chunked prefill
+    eng.reset(prompt)
+    eng.export = True
+    eng.set_policy("fixed", n=40)
+    eng.cycle()
+    eng.export = False
+    ex = eng.exported[-1]
+    c = len(prompt) - 1
+    logits_p, feat = ref.target(prompt[:-1], list(range(c)), causal_mask(c))
+    # drafter block vs oracle (probabilities, fp64 rows exported by K1)
+    dl = ref.drafter(feat, c, prompt[-1], GAMMA, eng.cfg.V - 1).double()
+    p_ref = torch.softmax(dl, -1).numpy()
+    assert np.abs(ex["probs"] - p_ref).max() < 2e-2
+    # verify logits/argmax vs oracle on the same tree
+    parent, depth, token = ex["parent"], ex["depth"], ex["token"]
+    anc = torch.from_numpy(O.ancestor_bits(parent))
+    toks = prompt[:-1] + [prompt[-1]] + token[1:].tolist()
+    pos = list(range(c)) + [c + int(d) for d in depth]
+    lv, _ = ref.target(toks, pos, verify_mask(c, anc))
+    lv = lv[c:]
+    top2 = lv.topk(2, dim=-1).values
+    clear = (top2[:, 0] - top2[:, 1]) > 1e-2
+    am_ref = lv.argmax(-1).numpy()
+    assert clear.float().mean() > 0.8
+    assert (ex["argmax"][clear.numpy()] == am_ref[clear.numpy()]).all()
+
+
+def _replay_check(eng, exported, tokens, policy, dims=None, t_draft=0.0, t_aux=0.0, l_ar=1.0, n_max=64):
+    """Run the ORACLE decode loop on the GPU-exported fp64 rows + verify argmax: must be bit-identical."""
+    P = eng.prompt_len
+    by_prefix = {}
+    committed = []
+    for e in exported:
+        by_prefix[tuple(committed)] = e
+        committed = committed + [int(e["token"][i]) for i in e["path"][1:]] + [e["bonus"]]
+
+    def drafter(prefix):
+        return by_prefix[tuple(prefix)]["probs"]
+
+    def target(seq, T):
+        for k in range(len(seq), -1, -1):  # find the cycle whose prefix this seq extends
+            e = by_prefix.get(tuple(seq[:k]))
+            if e is None:
+                continue
+            walk = seq[k:]
+            node = 0
+            kids = {}
+            for i in range(1, len(e["parent"])):
+                kids.setdefault(int(e["parent"][i]), {})[int(e["token"][i])] = i
+            for t in walk:
+                node = kids[node][t]
+            return int(e["argmax"][node])
+        raise KeyError(seq)
+
+    run_len = len(tokens)
+    records, toks = O.decode_loop(drafter, target, run_len, eng.top_k, policy, n_max, dims, P - 1, t_draft, t_aux,
+                                  l_ar)
+    assert list(toks) == list(tokens)
+    for rec, e in zip(records, exported):
+        assert rec["tree_size"] == int(e["meta"][0])
+        assert rec["surrogate"] == e["surrogate"]
+    return records
+
+
+def test_planning_bit_parity_fixed(eng):
+    eng.reset(_prompt(50, eng.cfg.V, seed=1))
+    eng.export = True
+    eng.set_policy("fixed", n=24)
+    _, toks = eng.run(30)
+    eng.export = False
+    dims = O.Dims(L=2, h=256, n_q=4, n_kv=2, d=128, h_ffn=512, V=1024, bp=2, peak_flops=1e15, bandwidth=1e12)
+    _replay_check(eng, eng.exported, toks, ("fixed", 24, 0, 0), dims)
+
+
+def test_planning_bit_parity_adaptive(eng):
+    from paper_2605_29727_b200 import CostModelParams, CycleLatencies, VerifyLatencyEstimator
+    from paper_2605_29727_b200.engine.config import QWEN3_8B
+    params = QWEN3_8B.cost_params(1649.1e12, 6457.7e9)  # plan with the 8B roofline on the tiny engine
+    est = VerifyLatencyEstimator(params, variant="static")
+    l_ar = est.estimate(1, 1000)
+    lat = CycleLatencies(t_draft=3e-4, t_aux=2e-5, l_ar=l_ar)
+    eng.reset(_prompt(60, eng.cfg.V, seed=2))
+    eng.export = True
+    eng.set_policy("adaptive", estimator=est, latencies=lat, n_max=64)
+    _, toks = eng.run(30)
+    eng.export = False
+    dims = O.Dims(**{k: getattr(params, k) for k in ("L", "h", "n_q", "n_kv", "d", "h_ffn", "V", "bp")},
+                  peak_flops=params.peak_flops, bandwidth=params.bandwidth)
+    recs = _replay_check(eng, eng.exported, toks, ("adaptive", 0, 0, 0), dims, 3e-4, 2e-5, l_ar, 64)
+    assert all(r["tree_size"] >= 1 for r in recs)
+    for e in eng.exported:  # the device S_hat trace equals the oracle's
+        c = e["c"]
+        want = O.controller(e["tok"], e["prob"], 64, O.curve_for(dims, c), 3e-4, 2e-5, l_ar)
+        assert np.array(want.trace).tobytes() == e["trace"].tobytes()
+        assert want.budget == int(e["meta"][0])
+
+
+def _decoy_drafter(ar, gamma, V, seed):
+    """Test drafter: the target's greedy token competes with decoys so the accepted path is non-contiguous."""
+    rng = np.random.default_rng(seed)
+
+    def fn(e):
+        k = int(e.state[3].item())  # committed so far
+        lg = torch.zeros(gamma, V, device="cuda")
+        for j in range(gamma):
+            if k + j < len(ar):
+                lg[j, ar[k + j]] = 5.0
+            dec = rng.choice(V, 3, replace=False)
+            lg[j, torch.from_numpy(dec).cuda()] = torch.tensor([5.3, 4.9, 4.7], device="cuda")
+        return lg
+    return fn
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_kv_compaction_preserves_greedy_output(eng, graphs):
+    """Greedy output preservation: tree decode with acceptance == target AR decode."""
+    prompt = _prompt(70, eng.cfg.V, seed=3)
+    eng.reset(prompt)
+    ar = eng.ar_decode(80)
+    eng.reset(prompt)
+    eng.set_policy("fixed", n=48)
+    eng.draft_override = _decoy_drafter(ar, GAMMA, eng.cfg.V, 0)
+    eng.use_graphs = graphs
+    try:
+        stats, toks = eng.run(60)
+    finally:
+        eng.draft_override = None
+        eng.use_graphs = True
+    assert toks[:60] == ar[:60]
+    accepted = [s.accepted_len for s in stats]
+    assert max(accepted) > 3 and np.mean(accepted) > 2.0  # compaction really ran
+    # non-contiguous paths happened (moves, not just identity)
+    assert len(stats) < 40
+
+
+def test_graph_and_eager_cycles_agree(eng):
+    prompt = _prompt(40, eng.cfg.V, seed=4)
+    eng.set_policy("fixed", n=32)
+    out = []
+    for graphs in (False, True):
+        eng.use_graphs = graphs
+        eng.reset(prompt)
+        out.append(eng.run(20)[1])
+    eng.use_graphs = True
+    assert out[0] == out[1]
