@@ -63,7 +63,10 @@ class B200Engine:
                  seed: int = 0, n_cap: int = MAX_ROWS - 1, top_k: int = 8, device=None, max_cycles: int = 4096):
         if not torch.cuda.is_available():
             raise RuntimeError("B200Engine needs a CUDA device; there is no CPU fallback")
-        self.dev = torch.device(device or "cuda")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
         torch.cuda.set_device(self.dev)
         self.cfg = cfg
         dcfg = dcfg or DrafterConfig()

@@ -137,10 +137,10 @@ def _decoy_drafter(ar, gamma, V, seed):
         k = int(e.state[3].item())  # committed so far
         lg = torch.zeros(gamma, V, device="cuda")
         for j in range(gamma):
+            dec = int(rng.integers(0, V))
+            lg[j, dec] = 10.3  # a decoy ranked above the target's token
             if k + j < len(ar):
-                lg[j, ar[k + j]] = 5.0
-            dec = rng.choice(V, 3, replace=False)
-            lg[j, torch.from_numpy(dec).cuda()] = torch.tensor([5.3, 4.9, 4.7], device="cuda")
+                lg[j, ar[k + j]] = 10.0
         return lg
     return fn
 
