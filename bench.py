@@ -1,0 +1,367 @@
+"""Benchmark: BASTION tree-speculative decode on B200 (BASELINE.json config 2).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+
+A "step" is one decode cycle of the hot path: drafter forward -> K1 top-K
+lattice -> K2 adaptive best-first expansion (Algorithm 1) -> tree-masked
+target verify -> K6 greedy accept + KV compaction.  Workload (config 2):
+Qwen3-8B-shape target + DFlash-style 5-layer drafter, random-init bf16,
+batch 1, 2048-token synthetic prompt, gamma 16, K 8, adaptive budget.
+N > 1 (torchrun): one independent request per rank, no collective on the data
+path (weak scaling); time = max over ranks of the device-timed region.
+
+Prints ONE JSON line (rank 0).  `--impl reference` times the reference's
+planning path (the CPU oracle port of specplan) on the host cores instead.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "decode tokens/s + tree-verify µs/step (Qwen3-8B shape, greedy); mean accept len"
+WORKLOAD = ("config2: Qwen3-8B-shape target + DFlash-style 5-layer block drafter, random-init bf16, batch 1 "
+            "per GPU, 2048-token context, gamma 16, top-K 8, adaptive budget (Algorithm 1, N_max 255)")
+
+
+def load_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"], "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback"}
+
+
+# --------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc = index, None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        self.out = ""
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for line in (self.out or "").splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        loaded = [x for x in sm if x > 0.5 * mx] or sm
+        return {"sm_mhz": statistics.median(loaded), "sm_max_mhz": mx, "reasons": sorted(reasons)}
+
+
+# ------------------------------------------------------------- CPU baseline
+def cpu_reference_cycles(n_cycles: int, seed: int = 0, context: int = 2048, vocab: int = 151936, gamma: int = 16,
+                         top_k: int = 8) -> dict:
+    """The reference planning path on this host (oracle port of specplan): per cycle
+    fp64 softmax + MarginalBlock validation + top_k_truncate + run_cycle (adaptive,
+    Qwen3-8B roofline at c) + linearize (c + t)^2 mask + verify_tree walk + commit."""
+    import numpy as np
+
+    from oracle import specplan_port as O
+    rng = np.random.default_rng(seed)
+    peaks = load_peaks()
+    dims = O.Dims(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=vocab, bp=2,
+                  peak_flops=peaks["bf16_tflops"] * 1e12, bandwidth=peaks["hbm_gbs"] * 1e9)
+    committed = 0
+    times = []
+    for i in range(n_cycles):
+        lg = (rng.standard_normal((gamma, vocab), dtype=np.float32) * 6.0)
+        lg = (lg.view(np.uint32) & 0xFFFF0000).view(np.float32)  # bf16-valued logits
+        c = context + committed
+        t0 = time.perf_counter()
+        probs = O.softmax_rows_f64(lg)
+        if np.any(probs < 0) or np.any(probs > 1) or np.any(np.abs(probs.sum(1) - 1) > 1e-9):  # lattice.py:47-53
+            raise ValueError("invalid block")
+        tok, prob = O.topk_rows(probs, top_k)
+        l_ar = O.roofline(dims, 1, c)
+        dec = O.controller(tok, prob, 255, O.curve_for(dims, c), 5e-4, 0.0, l_ar)
+        mask = O.linear_mask(dec.tree.parent, c)
+        am = rng.integers(0, vocab, dec.tree.size + 1)  # random-init target: the tree is rejected at the root
+        path, bonus = O.accept_from_argmax(dec.tree.parent, dec.tree.token, am)
+        toks = O.committed_tokens(path, dec.tree.token, bonus)
+        times.append(time.perf_counter() - t0)
+        committed += len(toks)
+        del mask
+    total = sum(times)
+    return {"tokens": committed, "seconds": total, "cycles": n_cycles, "median_cycle_s": statistics.median(times)}
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    warm = cpu_reference_cycles(args.warmup, seed=1)
+    del warm
+    r = cpu_reference_cycles(args.steps, seed=0)
+    value = r["tokens"] / r["seconds"]
+    sample = (f"{args.steps} cycles of the reference planning path on config-2 shapes (gamma 16 x V 151936 bf16 "
+              f"drafter logits, c=2048, adaptive N_max 255): fp64 softmax+validation, top_k_truncate, run_cycle, "
+              f"linearize, verify_tree, commit; model forward not included (the reference has none)")
+    print(json.dumps({
+        "metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOAD},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# -------------------------------------------------------------------- ours
+def run_ours(args) -> None:
+    import numpy as np
+    import torch
+
+    import paper_2605_29727_b200 as P
+    from paper_2605_29727_b200 import _lib, ops
+    from paper_2605_29727_b200.device import graph_kernel_nodes
+    from paper_2605_29727_b200.engine.config import MODELS, DrafterConfig
+    from paper_2605_29727_b200.engine.decode import ST_COMMITTED, B200Engine
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = load_peaks()
+    cfg = MODELS[args.model]
+    steps_total = args.warmup + args.steps + args.e2e_cycles + 64
+    eng = B200Engine(cfg, DrafterConfig(layers=5, gamma=16, logit_scale=args.logit_scale),
+                     max_ctx=args.context + 17 * steps_total + 256, seed=rank, n_cap=255, top_k=8)
+    prompt = np.random.default_rng(1000 + rank).integers(0, cfg.V - 1, args.context + 1).tolist()
+    eng.reset(prompt)
+    params = cfg.cost_params(peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9)
+
+    # ---- K7: measure l_ar / t_draft, static calibration of the verify roofline
+    l_ar = eng.measure_ar_step()
+    calib = []
+    for n in (15, 47, 95, 159, 255):
+        eng.reset(prompt)
+        eng.set_policy("fixed", n=n)
+        obs = []
+        for _ in range(4):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            nn, _ = eng.draft(ev)
+            eng.verify(nn, ev)
+            ev[2].synchronize()
+            obs.append((nn + 1, ev[0].elapsed_time(ev[1]) * 1e-3, ev[1].elapsed_time(ev[2]) * 1e-3))
+        s, td, tv = obs[-1][0], statistics.median(o[1] for o in obs[1:]), statistics.median(o[2] for o in obs[1:])
+        calib.append((s, td, tv))
+    t_draft = statistics.median(x[1] for x in calib)
+    pairs = [(P.roofline_latency(params, P.LatencyQuery(s=s, c=args.context)), tv) for s, _, tv in calib]
+    fit = P.fit_static_calibration(pairs)
+    est = P.VerifyLatencyEstimator(params, variant="static", fit=fit)
+    lat = P.CycleLatencies(t_draft=t_draft, t_aux=0.0, l_ar=l_ar)
+
+    # ---- device-timed decode (inputs resident, graphs)
+    eng.reset(prompt)
+    if args.policy == "adaptive":
+        eng.set_policy("adaptive", estimator=est, latencies=lat, n_max=255)
+    else:
+        eng.set_policy("fixed", n=int(args.policy.split("-")[1]))
+    for _ in range(args.warmup):
+        eng.cycle()
+    eng.stream.synchronize()
+    c0 = int(eng.state[ST_COMMITTED].item())
+    cyc0 = int(eng.state[4].item())
+    _lib.launch_count = 0
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    per = []
+    buckets = []
+    with ClockSampler(local) as clk:
+        start.record(eng.stream)
+        for _ in range(args.steps):
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            n = eng.cycle(ev)
+            per.append(ev)
+            buckets.append(eng._bucket(n))
+        end.record(eng.stream)
+        end.synchronize()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    elapsed = start.elapsed_time(end) * 1e-3
+    tokens = int(eng.state[ST_COMMITTED].item()) - c0
+    stats = eng.read_log()[cyc0:cyc0 + args.steps]
+    t_ver = [e[1].elapsed_time(e[2]) * 1e-3 for e in per]  # seconds
+    t_dr = [e[0].elapsed_time(e[1]) * 1e-3 for e in per]
+    if dist:
+        t = torch.tensor([elapsed, float(tokens)], device="cuda", dtype=torch.float64)
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = t.clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        elapsed, tokens_all = float(mx[0]), float(sm[1])
+    else:
+        tokens_all = float(tokens)
+    value = tokens_all / elapsed
+    # exact kernel count: nodes of the graphs replayed in the timed region
+    kd = graph_kernel_nodes(eng.graph_d)
+    kv = {b: graph_kernel_nodes(g) for b, g in eng.graphs_v.items()}
+    gpu_launches = sum(kd + kv[b] for b in buckets)
+
+    # ---- e2e: the public API (façade decode -> engine fast path, EMA estimator re-planned every cycle)
+    eng.reset(prompt)
+    est_ema = P.VerifyLatencyEstimator(params, variant="ema_calib", fit=fit, bias=P.EmaBias())
+    sim = P.SimConfig(controller=P.ControllerConfig(n_max=255, latencies=lat, variant="ema_calib",
+                                                    context_len=args.context), run_length=args.e2e_cycles,
+                      top_k=8)
+    torch.cuda.synchronize()
+    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e_start.record(eng.stream)
+    t0 = time.perf_counter()
+    records, toks_e2e = P.decode_full(eng, sim, P.Policy.adaptive(), est_ema)
+    e_end.record(eng.stream)
+    e_end.synchronize()
+    e2e_time = max(e_start.elapsed_time(e_end) * 1e-3, time.perf_counter() - t0)
+    e2e_tokens = sum(r.accepted_len for r in records)
+    e2e_val = e2e_tokens / e2e_time
+    if dist:
+        t = torch.tensor([e2e_time, float(e2e_tokens)], device="cuda", dtype=torch.float64)
+        mx, sm = t.clone(), t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        e2e_val = float(sm[1]) / float(mx[0])
+    aal_e2e = e2e_tokens / max(1, len(records))
+
+    # ---- roofline of the dominant kernel (K4 GEMM) at the timed region's median verify size
+    s_med = int(statistics.median(buckets))
+    t = eng.target
+    x = t.x[:s_med]
+    shapes = []
+    for lw in eng.tw.layers:
+        shapes += [lw.qkv, lw.o, lw.gate_up, lw.down]
+    shapes.append(eng.tw.lm_head)
+    evs = []
+    with torch.cuda.stream(eng.stream):
+        for w in shapes + shapes:  # second pass timed
+            k = w.shape[1]
+            xin = {cfg.h: t.x, cfg.h_q: t.attn, cfg.h_ffn: t.act}[k][:s_med]
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(eng.stream)
+            ops.gemm_partial(xin, w, out=t.partial)
+            b.record(eng.stream)
+            evs.append((a, b, w.numel() * 2 + s_med * k * 2))
+    eng.stream.synchronize()
+    evs = evs[len(shapes):]
+    g_time = sum(a.elapsed_time(b) for a, b, _ in evs) * 1e-3
+    g_bytes = sum(n for _, _, n in evs)
+    achieved = g_bytes / g_time / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "gemm_dram_bytes.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+
+    # ---- CPU baseline (rank 0, N=1 only): bounded sample of the reference planning path
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        r = cpu_reference_cycles(args.cpu_cycles)
+        cpu = {"value": r["tokens"] / r["seconds"], "unit": "tokens/s", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_cycles} cycles of the specplan planning path (oracle port) at config-2 shapes; "
+                         f"fp64 softmax/validation, top_k_truncate, run_cycle, linearize, verify_tree, commit; "
+                         f"no model forward (the reference has none); median {r['median_cycle_s'] * 1e3:.0f} ms/cycle"}
+
+    if rank != 0:
+        return
+    n_exp = [s.tree_size for s in stats]
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init bf16 weights, uniform random prompt tokens)",
+        "config": {"workload": WORKLOAD, "context": args.context, "policy": args.policy, "gamma": 16, "top_k": 8,
+                   "drafter_logit_scale": args.logit_scale,
+                   "l2": "inputs larger than L2: 16.4 GB of target weights + 1.9 GB drafter streamed per step"},
+        "tree_verify_us_per_step": 1e6 * statistics.mean(t_ver), "draft_us_per_step": 1e3 * statistics.mean(t_dr),
+        "mean_accept_len": statistics.mean(s.accepted_len for s in stats),
+        "mean_tree_size": statistics.mean(n_exp), "verify_rows_bucket_median": s_med,
+        "l_ar_us": l_ar * 1e6, "ar_tokens_per_s_equiv": 1.0 / l_ar,
+        "calibration": {"slope": fit.slope, "intercept": fit.intercept, "rmse_before": fit.rmse_before,
+                        "rmse_after": fit.rmse_after, "points": [[s, tv] for s, _, tv in calib]},
+        "roofline": {"bound": "hbm", "kernel": "gemm_bf16_kernel (K4, tcgen05 weight streaming)",
+                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+                     "traffic": traffic, "peak_src": peaks["src"],
+                     "algorithmic_bytes": "bf16 weights + X rows per launch, 36x(qkv,o,gate_up,down)+lm_head "
+                                          f"at m={s_med}", "avg_launch_us": 1e6 * g_time / len(evs)},
+        "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": 200,
+                "d2h_bytes_per_step": 64 + 40 + int(4 * aal_e2e), "api": "paper_2605_29727_b200.decode_full(engine, "
+                "SimConfig, Policy.adaptive(), VerifyLatencyEstimator(ema_calib))", "cycles": len(records)},
+        "gpu_launches": gpu_launches,
+        "clocks": clk.summary(),
+    }
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--model", default="qwen3-8b")
+    ap.add_argument("--context", type=int, default=2048)
+    ap.add_argument("--policy", default="adaptive")
+    ap.add_argument("--logit-scale", type=float, default=6.0)
+    ap.add_argument("--e2e-cycles", type=int, default=30)
+    ap.add_argument("--cpu-cycles", type=int, default=30)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -98,6 +98,7 @@ class B200Engine:
         self.meta_host = torch.zeros(16, dtype=torch.int32).pin_memory()
         self.stream = torch.cuda.Stream(self.dev)
         self.graph_d = None
+        self.graphs_d: dict[tuple, torch.cuda.CUDAGraph] = {}
         self.graphs_v: dict[int, torch.cuda.CUDAGraph] = {}
         self.graph_ar = None
         self.policy = (_lib.POLICY_FIXED, 64)
@@ -162,7 +163,11 @@ class B200Engine:
         self.plan_host.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8))
         with torch.cuda.stream(self.stream):
             self.plan_dev.copy_(self.plan_host, non_blocking=True)
-        self.graph_d = None  # policy/n_max are launch parameters of K2
+        self.graph_d = self.graphs_d.get(self.policy)  # policy/n_max are launch parameters of K2
+
+    def refresh_plan(self, estimator: VerifyLatencyEstimator, latencies: CycleLatencies) -> None:
+        """Re-upload the adaptive plan (e.g. after an EMA update) — one small H2D copy, no recapture."""
+        self.set_policy("adaptive", estimator=estimator, latencies=latencies, n_max=self.policy[1])
 
     # --------------------------------------------------------------- phases
     def _draft_body(self) -> None:
@@ -212,7 +217,7 @@ class B200Engine:
                 self._draft_body()
             return
         if self.graph_d is None:
-            self.graph_d = self._capture(self._draft_body)
+            self.graph_d = self.graphs_d[self.policy] = self._capture(self._draft_body)
         with torch.cuda.stream(self.stream):
             self.graph_d.replay()
 
@@ -357,11 +362,14 @@ class B200Engine:
 
         The context of every cycle is the engine's KV length c (= prompt_len - 1 +
         committed), the reference's ``context_len + len(prefix)`` under the
-        alignment contract (SURVEY §8a′); the SimConfig's latencies drive Algorithm 1.
+        alignment contract (SURVEY §8a′); the SimConfig's latencies drive
+        Algorithm 1.  Every measured verify time is fed to ``estimator.observe``
+        (K7, §5.2); EMA variants re-plan the next cycle from the updated bias.
         """
         from ..verify_sim import CycleRecord
         lat = sim_cfg.controller.latencies
-        if policy.kind == "adaptive":
+        adaptive = policy.kind == "adaptive"
+        if adaptive:
             self.set_policy("adaptive", estimator=estimator, latencies=lat, n_max=sim_cfg.controller.n_max)
         elif policy.kind == "fixed":
             self.set_policy("fixed", n=policy.n)
@@ -369,17 +377,35 @@ class B200Engine:
             raise ValueError("engine fast path supports adaptive and fixed-N policies")
         if sim_cfg.top_k != self.top_k:
             raise ValueError(f"engine was built with top_k={self.top_k}")
-        stats, toks = self.run(sim_cfg.run_length)
+        ema = estimator.variant in ("ema", "ema_calib")
+        events: list = []
+        pending = None  # (index, s, events) of the previous cycle, observed at this cycle's sync
+        cyc0 = int(self.state[ST_CYCLE].item())
+        while True:
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+            n_nodes, committed = self.draft(ev)
+            if pending is not None:
+                s, c, pev = pending
+                estimator.observe(s, c, pev[1].elapsed_time(pev[2]) * 1e-3)
+                if ema and adaptive:
+                    self.refresh_plan(estimator, lat)
+            if committed >= sim_cfg.run_length:
+                break
+            c = int(self.meta_host[8 + ST_C])
+            self.verify(n_nodes, ev)
+            events.append(ev)
+            pending = (n_nodes + 1, c, ev)
+        if pending is not None and ema:
+            self.stream.synchronize()
+        stats = self.read_log(events=[None] * cyc0 + events)[cyc0:]
         records = []
         for st in stats:
-            if not np.isnan(st.t_verify):
-                estimator.observe(st.tree_size + 1, st.context, st.t_verify)
             t_verify = estimator.estimate_for_budget(st.tree_size, st.context)
             cyc = lat.t_draft + t_verify + lat.t_aux
             records.append(CycleRecord(tree_size=st.tree_size, accepted_len=st.accepted_len, surrogate=st.surrogate,
                                        t_draft=lat.t_draft, t_verify=t_verify, t_aux=lat.t_aux, l_ar=lat.l_ar,
                                        cycle_speedup=st.accepted_len * lat.l_ar / cyc))
-        return records, tuple(toks)
+        return records, tuple(self.tokens())
 
     def drafter_marginals(self, prefix) -> MarginalBlock:
         """fp64 drafter rows for the engine's current state (prefix must be its committed stream)."""
