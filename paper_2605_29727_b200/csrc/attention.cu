@@ -103,6 +103,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
 
+  sm100::grid_dep_launch();
   const int head = blockIdx.x;  // kv head
   const int split = blockIdx.y;
   if (a.state) a.c = a.state[a.c_idx];
@@ -304,6 +305,7 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 
 // merge flash-decoding splits: one warp per (token, q-head) row
 __global__ void attn_combine_kernel(AttnArgs a) {
+  sm100::grid_dep_launch();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int rows = a.s * a.n_q;
@@ -348,8 +350,12 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   const int pages = (max_keys + A_PAGE - 1) / A_PAGE;
   BST_REQUIRE(pages <= n_pages_total, "context exceeds the page table");
   if (n_splits <= 0) {
+    // enough CTAs to cover the SMs at long context, but >= 8 pages per split so
+    // short contexts do not pay a split/combine for two-tile CTAs
     int want = 148 / (n_kv * row_blocks);
-    n_splits = want < 1 ? 1 : want;
+    int by_work = pages / 8;
+    n_splits = want < by_work ? want : by_work;
+    if (n_splits < 1) n_splits = 1;
   }
   if (n_splits > pages) n_splits = pages;
   const int pps = (pages + n_splits - 1) / n_splits;

@@ -15,6 +15,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "sm100.cuh"
 
 namespace bst {
 
@@ -41,6 +42,7 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ emb, int h,
                                      const __nv_bfloat16* __restrict__ w, float eps, float* __restrict__ resid,
                                      __nv_bfloat16* __restrict__ x, int64_t ldx) {
+  sm100::grid_dep_launch();
   __shared__ float sh[32];
   const int t = blockIdx.x;
   const int64_t tok = tokens[t];
@@ -56,27 +58,45 @@ __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const _
 }
 
 // ------------------------------------------------------- residual + norm
-// y == nullptr: only normalise.  resid == nullptr: normalise Y itself.
-__global__ void residual_rmsnorm_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* resid, int h,
-                                        const __nv_bfloat16* __restrict__ w, float eps, __nv_bfloat16* x, int64_t ldx,
-                                        __nv_bfloat16* feat, int64_t ldf, int rows) {
+// One CTA (1024 threads) per row; each thread owns groups of 4 columns.
+// partial == nullptr: only normalise.  resid == nullptr: normalise Y itself.
+constexpr int R_THREADS = 1024;
+__global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
+    const float* __restrict__ partial, bst_gemm_sched_t s, float* resid, int h, const __nv_bfloat16* __restrict__ w,
+    float eps, __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf, int rows) {
+  sm100::grid_dep_launch();
   __shared__ float sh[32];
-  __shared__ float vals[8192];
+  __shared__ float4 vals[2048];
   const int t = blockIdx.x;
   if (t >= rows) return;
+  const int ng = h >> 2;
   float ss = 0.f;
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    float v = resid ? resid[(int64_t)t * h + i] : 0.f;
-    if (partial) v += gemm_load(partial, s, t, i);
-    if (resid) resid[(int64_t)t * h + i] = v;
-    if (feat) feat[(int64_t)t * ldf + i] = __float2bfloat16(v);
-    vals[i] = v;
-    ss += v * v;
+  for (int g = threadIdx.x; g < ng; g += R_THREADS) {
+    float4 v = resid ? reinterpret_cast<const float4*>(resid + (int64_t)t * h)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
+    if (partial) {
+      const float4 y = gemm_load4(partial, s, t, g * 4);
+      v.x += y.x; v.y += y.y; v.z += y.z; v.w += y.w;
+    }
+    if (resid) reinterpret_cast<float4*>(resid + (int64_t)t * h)[g] = v;
+    if (feat) {
+      __nv_bfloat162* f = reinterpret_cast<__nv_bfloat162*>(feat + (int64_t)t * ldf + g * 4);
+      f[0] = __floats2bfloat162_rn(v.x, v.y);
+      f[1] = __floats2bfloat162_rn(v.z, v.w);
+    }
+    vals[g] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
   }
   const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
-  if (x)
-    for (int i = threadIdx.x; i < h; i += blockDim.x)
-      x[(int64_t)t * ldx + i] = __float2bfloat16(vals[i] * inv * __bfloat162float(w[i]));
+  if (x) {
+    for (int g = threadIdx.x; g < ng; g += R_THREADS) {
+      const float4 v = vals[g];
+      const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w + g * 4);
+      const float2 w01 = __bfloat1622float2(wp[0]), w23 = __bfloat1622float2(wp[1]);
+      __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(x + (int64_t)t * ldx + g * 4);
+      xp[0] = __floats2bfloat162_rn(v.x * inv * w01.x, v.y * inv * w01.y);
+      xp[1] = __floats2bfloat162_rn(v.z * inv * w23.x, v.w * inv * w23.y);
+    }
+  }
 }
 
 // ------------------------------------------------------------- q/k/v + rope
@@ -87,6 +107,7 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
                                 const int32_t* __restrict__ qrow, __nv_bfloat16* q_out, int64_t q_tok_stride,
                                 __nv_bfloat16* kv, int64_t layer_off, const int32_t* __restrict__ page_table,
                                 int page_size, const int32_t* __restrict__ state, int state_c_idx) {
+  sm100::grid_dep_launch();
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -107,9 +128,8 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
     if (is_q && qr < 0) continue;
     if (!is_q && sl < 0) continue;
     const int col0 = hd * 128 + lane * 4;
-    float v[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = gemm_load(partial, s, t, col0 + e);
+    const float4 y4 = gemm_load4(partial, s, t, col0);
+    float v[4] = {y4.x, y4.y, y4.z, y4.w};
     if (is_q || is_k) {
       const __nv_bfloat16* nw_ = is_q ? qn : kn;
       float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
@@ -148,11 +168,14 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
 __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int ffn, __nv_bfloat16* act,
                               int64_t lda) {
   const int t = blockIdx.y;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ffn; j += gridDim.x * blockDim.x) {
-    const float gt = gemm_load(partial, s, t, j);
-    const float up = gemm_load(partial, s, t, ffn + j);
-    const float si = gt / (1.f + __expf(-gt));
-    act[(int64_t)t * lda + j] = __float2bfloat16(si * up);
+  sm100::grid_dep_launch();
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (ffn >> 2); g += gridDim.x * blockDim.x) {
+    const float4 gt = gemm_load4(partial, s, t, g * 4);
+    const float4 up = gemm_load4(partial, s, t, ffn + g * 4);
+    auto si = [](float z) { return z / (1.f + __expf(-z)); };
+    __nv_bfloat162* ap = reinterpret_cast<__nv_bfloat162*>(act + (int64_t)t * lda + g * 4);
+    ap[0] = __floats2bfloat162_rn(si(gt.x) * up.x, si(gt.y) * up.y);
+    ap[1] = __floats2bfloat162_rn(si(gt.z) * up.z, si(gt.w) * up.w);
   }
 }
 
@@ -185,11 +208,11 @@ extern "C" int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* em
 extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t* sched, float* resid, int rows, int h,
                                     const void* w, float eps, void* x, int64_t ldx, void* feat, int64_t ldf,
                                     bst_stream_t stream) {
-  BST_REQUIRE(h <= 8192, "hidden size > 8192 unsupported");
+  BST_REQUIRE(h <= 8192 && h % 4 == 0, "hidden size must be a multiple of 4 and <= 8192");
   BST_REQUIRE(!partial || sched, "partial without schedule");
   bst_gemm_sched_t s{};
   if (sched) s = *sched;
-  residual_rmsnorm_kernel<<<rows, E_THREADS, 0, as_stream(stream)>>>(
+  residual_rmsnorm_kernel<<<rows, R_THREADS, 0, as_stream(stream)>>>(
       partial, s, resid, h, static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
       static_cast<__nv_bfloat16*>(feat), ldf, rows);
   BST_LAUNCH_CHECK();
@@ -215,8 +238,8 @@ extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched,
 extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act,
                           int64_t lda, bst_stream_t stream) {
   BST_REQUIRE(partial && sched && act, "null pointer argument");
-  BST_REQUIRE(sched->n_out == 2 * ffn, "gate/up width mismatch");
-  dim3 grid((ffn + 255) / 256 < 48 ? (ffn + 255) / 256 : 48, rows);
+  BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
+  dim3 grid((ffn / 4 + 255) / 256, rows);
   swiglu_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, *sched, ffn, static_cast<__nv_bfloat16*>(act), lda);
   BST_LAUNCH_CHECK();
   return BST_OK;

@@ -33,7 +33,7 @@ constexpr int G_BM = 128;
 constexpr int G_BK = 64;
 constexpr int G_TILE_W = G_BM * G_BK * 2;  // 16 KiB
 constexpr int G_MAX_STAGES = 12;
-constexpr int G_SMEM_BUDGET = 200 * 1024;
+constexpr int G_SMEM_BUDGET = 160 * 1024;  // leaves room for a co-resident epilogue CTA (PDL overlap)
 
 // ------------------------------------------------------------ tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -159,19 +159,44 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 
   if (warp == 0) {
     // ---------------- TMA producer
+    // PDL: the weight tiles of the first `stages` k-blocks do not depend on the
+    // previous kernel, so they are issued before griddepcontrol.wait; the X
+    // (activation) tiles are issued only after the dependency resolves.
     if (lane == 0) {
       const uint64_t pol_w = sm100::policy_evict_first();
       int stage = 0;
       uint32_t phase = 0;
       int64_t u = u0;
       Seg seg;
+      int issued = 0;
+      // pass 1: prologue weights
+      {
+        int64_t uu = u0;
+        Seg sg;
+        int st = 0;
+        while (st < stages && next_seg(s, uu, u1, sg)) {
+          for (int kb = sg.kb_lo; kb < sg.kb_hi && st < stages; ++kb, ++st) {
+            uint8_t* sw = smem + st * stage_bytes;
+            sm100::mbar_add_tx(&full[st], G_TILE_W);
+            sm100::tma_load_2d_hint(sw, &tmW, &full[st], kb * G_BK, sg.tile * G_BM, pol_w);
+          }
+        }
+        issued = st;
+      }
+      sm100::grid_dep_wait();
+      int idx = 0;
       while (next_seg(s, u, u1, seg)) {
-        for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
-          sm100::mbar_wait(&empty[stage], phase ^ 1);
+        for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb, ++idx) {
           uint8_t* sw = smem + stage * stage_bytes;
-          sm100::mbar_expect_tx(&full[stage], stage_bytes);
-          sm100::tma_load_2d_hint(sw, &tmW, &full[stage], kb * G_BK, seg.tile * G_BM, pol_w);
-          sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
+          if (idx < issued) {  // weights already in flight: add the X tile and arrive
+            sm100::mbar_expect_tx(&full[stage], x_bytes);
+            sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
+          } else {
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            sm100::mbar_expect_tx(&full[stage], stage_bytes);
+            sm100::tma_load_2d_hint(sw, &tmW, &full[stage], kb * G_BK, seg.tile * G_BM, pol_w);
+            sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
+          }
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -245,10 +270,22 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 __global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* y_f32,
                                    __nv_bfloat16* y_bf16, int64_t ldy) {
   const int t = blockIdx.y;
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < s.n_out; n += gridDim.x * blockDim.x) {
-    float v = gemm_load(partial, s, t, n);
-    if (y_f32) y_f32[(int64_t)t * ldy + n] = v;
-    if (y_bf16) y_bf16[(int64_t)t * ldy + n] = __float2bfloat16(v);
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g * 4 < s.n_out; g += gridDim.x * blockDim.x) {
+    const int n0 = g * 4;
+    if (n0 + 4 <= s.n_out) {
+      const float4 v = gemm_load4(partial, s, t, n0);
+      const float vv[4] = {v.x, v.y, v.z, v.w};
+      for (int e = 0; e < 4; ++e) {
+        if (y_f32) y_f32[(int64_t)t * ldy + n0 + e] = vv[e];
+        if (y_bf16) y_bf16[(int64_t)t * ldy + n0 + e] = __float2bfloat16(vv[e]);
+      }
+    } else {
+      for (int n = n0; n < s.n_out; ++n) {
+        const float v = gemm_load(partial, s, t, n);
+        if (y_f32) y_f32[(int64_t)t * ldy + n] = v;
+        if (y_bf16) y_bf16[(int64_t)t * ldy + n] = __float2bfloat16(v);
+      }
+    }
   }
 }
 
@@ -257,12 +294,23 @@ __global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_s
                                    unsigned long long* best) {
   const int t = blockIdx.y;
   unsigned long long key = 0;
-  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < s.n_out; n += gridDim.x * blockDim.x) {
-    float v = gemm_load(partial, s, t, n);
+  auto consider = [&](float v, int n) {
     unsigned int b = __float_as_uint(v);
     b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-    unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)n);
+    const unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)n);
     key = k > key ? k : key;
+  };
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g * 4 < s.n_out; g += gridDim.x * blockDim.x) {
+    const int n0 = g * 4;
+    if (n0 + 4 <= s.n_out) {
+      const float4 v = gemm_load4(partial, s, t, n0);
+      consider(v.x, n0);
+      consider(v.y, n0 + 1);
+      consider(v.z, n0 + 2);
+      consider(v.w, n0 + 3);
+    } else {
+      for (int n = n0; n < s.n_out; ++n) consider(gemm_load(partial, s, t, n), n);
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -336,8 +384,17 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
     BST_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = smem;
   }
-  gemm_bf16_kernel<<<s.grid, G_THREADS, smem, as_stream(stream)>>>(tw, tx, s, partial, s.stages);
-  BST_LAUNCH_CHECK();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(s.grid);
+  cfg.blockDim = dim3(G_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = as_stream(stream);
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  BST_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel, tw, tx, s, partial, (int)s.stages));
   return BST_OK;
 }
 
@@ -346,7 +403,7 @@ extern "C" int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sch
   using namespace bst;
   BST_REQUIRE(partial && sched && (y_f32 || y_bf16), "null pointer argument");
   const bst_gemm_sched_t s = *sched;
-  dim3 grid((s.n_out + 255) / 256 < 64 ? (s.n_out + 255) / 256 : 64, s.m);
+  dim3 grid((s.n_out / 4 + 255) / 256 < 148 ? (s.n_out / 4 + 255) / 256 + 1 : 148, s.m);
   gemm_reduce_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, s, y_f32,
                                                           static_cast<__nv_bfloat16*>(y_bf16), ldy);
   BST_LAUNCH_CHECK();
@@ -360,7 +417,7 @@ extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sch
   const bst_gemm_sched_t s = *sched;
   cudaStream_t st = as_stream(stream);
   BST_CUDA(cudaMemsetAsync(scratch_u64, 0, sizeof(unsigned long long) * s.m, st));
-  dim3 grid(64, s.m);
+  dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
   gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64));
   argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
                                                             argmax);

@@ -17,6 +17,36 @@ __host__ __device__ __forceinline__ int sched_last_cta(const bst_gemm_sched_t& s
   return (int)(c < 0 ? 0 : (c >= s.grid ? s.grid - 1 : c));
 }
 
+// 32-bit fast path of the slot lookup (units * grid < 2^32 for every verify shape).
+__device__ __forceinline__ int tile_nslot(const bst_gemm_sched_t& s, int tile) {
+  const uint32_t U = (uint32_t)s.units, G = (uint32_t)s.grid, kb = (uint32_t)s.n_kb;
+  const uint32_t first = ((uint32_t)tile * kb + 1) * G;
+  const uint32_t last = ((uint32_t)(tile + 1) * kb) * G;
+  int f = (int)((first + U - 1) / U) - 1, l = (int)((last + U - 1) / U) - 1;
+  f = f < 0 ? 0 : (f >= (int)G ? (int)G - 1 : f);
+  l = l < 0 ? 0 : (l >= (int)G ? (int)G - 1 : l);
+  return l - f + 1;
+}
+
+// Four consecutive outputs Y[t, n0..n0+3] (n0 % 4 == 0, same 128-wide tile): one
+// slot lookup, float4 loads, slots summed lowest k range first.
+__device__ __forceinline__ float4 gemm_load4(const float* __restrict__ partial, const bst_gemm_sched_t& s, int t,
+                                             int n0) {
+  const int tile = n0 >> 7;
+  const int nslot = tile_nslot(s, tile);
+  const float4* p = reinterpret_cast<const float4*>(partial + ((int64_t)tile * s.s_max * s.bn + t) * 128 + (n0 & 127));
+  const int64_t stride = (int64_t)s.bn * 32;  // in float4
+  float4 acc = __ldg(p);
+  for (int k = 1; k < nslot; ++k) {
+    const float4 v = __ldg(p + k * stride);
+    acc.x += v.x;
+    acc.y += v.y;
+    acc.z += v.z;
+    acc.w += v.w;
+  }
+  return acc;
+}
+
 // Y[t, n] = sum of the tile's partial slots, lowest k range first (deterministic).
 __device__ __forceinline__ float gemm_load(const float* __restrict__ partial, const bst_gemm_sched_t& s, int t,
                                            int n) {

@@ -32,6 +32,7 @@ import torch
 from .. import _lib, ops
 from ..controller import STOP_BUDGET_CAP
 from ..cost_model import CycleLatencies, VerifyLatencyEstimator
+from ..device import graph_kernel_nodes
 from ..draft_tree import DeviceTree, expand_device_plan
 from ..lattice import MarginalBlock, topk_logits_into
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
@@ -107,6 +108,7 @@ class B200Engine:
         self.export = False  # debug: keep fp64 drafter rows + verify argmax per cycle (parity tests)
         self.exported: list[dict] = []
         self.draft_override = None
+        self.graph_kernels: dict[int, int] = {}
         torch.cuda.synchronize()
 
     # ------------------------------------------------------------------ setup
@@ -203,9 +205,11 @@ class B200Engine:
             fn()
         self.stream.synchronize()
         self.state.copy_(saved)
-        g = torch.cuda.CUDAGraph()
+        g = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g, stream=self.stream):
             fn()
+        self.graph_kernels[id(g)] = graph_kernel_nodes(g)  # exact launches per replay
+        g.instantiate()
         self.stream.synchronize()
         self.state.copy_(saved)
         torch.cuda.synchronize()
