@@ -303,26 +303,47 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   }
 }
 
-// merge flash-decoding splits: one warp per (token, q-head) row
+// merge flash-decoding splits: one warp per (token, q-head) row, single pass
+// with online rescaling, 4 splits in flight per iteration
 __global__ void attn_combine_kernel(AttnArgs a) {
   sm100::grid_dep_launch();
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int rows = a.s * a.n_q;
   if (row >= rows) return;
-  float M = -INFINITY;
-  for (int sp = 0; sp < a.n_splits; ++sp) M = fmaxf(M, a.ws_ml[((int64_t)sp * rows + row) * 2]);
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, L = 0.f;
-  for (int sp = 0; sp < a.n_splits; ++sp) {
-    const float m = a.ws_ml[((int64_t)sp * rows + row) * 2];
-    const float l = a.ws_ml[((int64_t)sp * rows + row) * 2 + 1];
-    const float w = (m == -INFINITY) ? 0.f : exp2f(m - M);
-    L += w * l;
-    const float4 v = *reinterpret_cast<const float4*>(a.ws_o + ((int64_t)sp * rows + row) * A_D + lane * 4);
-    acc[0] += w * v.x;
-    acc[1] += w * v.y;
-    acc[2] += w * v.z;
-    acc[3] += w * v.w;
+  float M = -INFINITY, L = 0.f;
+  float acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int sp0 = 0; sp0 < a.n_splits; sp0 += 4) {
+    float m[4], l[4];
+    float4 v[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int sp = sp0 + j;
+      if (sp < a.n_splits) {
+        const int64_t r = (int64_t)sp * rows + row;
+        m[j] = a.ws_ml[r * 2];
+        l[j] = a.ws_ml[r * 2 + 1];
+        v[j] = *reinterpret_cast<const float4*>(a.ws_o + r * A_D + lane * 4);
+      } else {
+        m[j] = -INFINITY;
+        l[j] = 0.f;
+        v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    float Mn = M;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Mn = fmaxf(Mn, m[j]);
+    if (Mn == -INFINITY) continue;
+    const float sc = (M == -INFINITY) ? 0.f : exp2f(M - Mn);
+    L *= sc;
+    acc[0] *= sc; acc[1] *= sc; acc[2] *= sc; acc[3] *= sc;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float w = (m[j] == -INFINITY) ? 0.f : exp2f(m[j] - Mn);
+      L += w * l[j];
+      acc[0] += w * v[j].x; acc[1] += w * v[j].y; acc[2] += w * v[j].z; acc[3] += w * v[j].w;
+    }
+    M = Mn;
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   const int tok = row / a.n_q, qh = row % a.n_q;
@@ -350,12 +371,10 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   const int pages = (max_keys + A_PAGE - 1) / A_PAGE;
   BST_REQUIRE(pages <= n_pages_total, "context exceeds the page table");
   if (n_splits <= 0) {
-    // enough CTAs to cover the SMs at long context, but >= 8 pages per split so
-    // short contexts do not pay a split/combine for two-tile CTAs
+    // one wave of CTAs: per-tile work (GQA group x tokens rows against 64 keys)
+    // dominates a CTA's fixed cost, so spread the pages over every SM
     int want = 148 / (n_kv * row_blocks);
-    int by_work = pages / 8;
-    n_splits = want < by_work ? want : by_work;
-    if (n_splits < 1) n_splits = 1;
+    n_splits = want < 1 ? 1 : want;
   }
   if (n_splits > pages) n_splits = pages;
   const int pps = (pages + n_splits - 1) / n_splits;
