@@ -173,6 +173,17 @@ def run_ours(args) -> None:
     eng.reset(prompt)
     params = cfg.cost_params(peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9)
 
+    if args.profile:  # short run for ncu launch lists: fixed budget, graphs, no calibration/e2e/cpu legs
+        eng.set_policy("fixed", n=31)
+        for _ in range(args.warmup):
+            eng.cycle()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        for _ in range(args.steps):
+            eng.cycle()
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        return
     # ---- K7: measure l_ar / t_draft, static calibration of the verify roofline
     l_ar = eng.measure_ar_step()
     calib = []
@@ -366,6 +377,7 @@ def main() -> None:
     ap.add_argument("--e2e-cycles", type=int, default=30)
     ap.add_argument("--cpu-cycles", type=int, default=30)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--profile", action="store_true", help="only the cycle loop (for ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
