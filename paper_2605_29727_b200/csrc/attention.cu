@@ -15,6 +15,7 @@
 // on mma.sync bf16 (the bytes/flop ratio at s <= 64 is HBM bound); softmax is
 // the online exp2 form in fp32.  Splits are merged by attn_combine_kernel.
 #include <cuda_bf16.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -86,6 +87,46 @@ __device__ __forceinline__ uint32_t tile_addr(uint32_t tile, int row, int q) {
   return tile + half * (A_PAGE * 128) + row * 128 + ((cq ^ (row & 7)) << 4);
 }
 
+// 64-bit visibility of keys slot0..slot0+63 for query row `tok`:
+// prefix (< c) always, tree/causal part per mode, nothing at or beyond n_keys.
+__device__ __forceinline__ uint64_t bits_from(int lo, int hi) {  // bits [lo, hi] (clamped to 0..63)
+  lo = lo < 0 ? 0 : lo;
+  hi = hi > 63 ? 63 : hi;
+  if (hi < lo) return 0ull;
+  const uint64_t upto = hi == 63 ? ~0ull : ((1ull << (hi + 1)) - 1);
+  return upto & ~((1ull << lo) - 1);
+}
+__device__ __forceinline__ uint64_t mask_get64(const uint32_t* m, int words, int start) {
+  const int w = start >> 5, sh = start & 31;
+  const uint64_t w0 = w < words ? m[w] : 0u, w1 = w + 1 < words ? m[w + 1] : 0u, w2 = w + 2 < words ? m[w + 2] : 0u;
+  const uint64_t lo = w0 | (w1 << 32);
+  return sh ? (lo >> sh) | (w2 << (64 - sh)) : lo;
+}
+__device__ __forceinline__ uint64_t row_vis64(int mode, int c, int n_keys, int tok, int slot0, const uint32_t* mrow,
+                                              int words) {
+  const uint64_t lim = bits_from(0, n_keys - slot0 - 1);
+  if (mode == 2) return lim;
+  const int np = c - slot0;  // prefix keys in this tile
+  const uint64_t pre = bits_from(0, np - 1);
+  if (np >= 64) return pre & lim;
+  const int j0 = slot0 - c;  // tree index of key 0 (< 0: the tile starts in the prefix)
+  uint64_t tail;
+  if (mode == 1) {
+    tail = bits_from(-j0, tok - j0);
+  } else if (j0 >= 0) {
+    tail = mask_get64(mrow, words, j0);
+  } else {
+    tail = mask_get64(mrow, words, 0) << (-j0);
+  }
+  return (pre | tail) & lim;
+}
+
+__device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ex2(-inf) = +0
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ bool visible(const AttnArgs& a, int tok, int slot, const uint32_t* mrow) {
   if (slot >= a.n_keys) return false;
   if (a.mode == 2) return true;
@@ -106,11 +147,11 @@ __global__ void __launch_bounds__(A_THREADS, 1)
   sm100::grid_dep_launch();
   const int head = blockIdx.x;  // kv head
   const int split = blockIdx.y;
-  if (a.state) a.c = a.state[a.c_idx];
-  a.n_keys = a.c + a.keys_after_c;
+  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
+  const int n_keys = c_ctx + a.keys_after_c;
   const int R = a.group * a.s;  // query rows of this kv head: r = t * group + g
   const int page0 = split * a.pages_per_split;
-  const int n_pages_keys = (a.n_keys + A_PAGE - 1) / A_PAGE;
+  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
   const int page1 = min(page0 + a.pages_per_split, n_pages_keys);
   const int n_tiles = max(page1 - page0, 0);
 
@@ -196,14 +237,15 @@ __global__ void __launch_bounds__(A_THREADS, 1)
       }
       // mask + online softmax (rows g and g+8 of this warp's block)
       float mx[2] = {-INFINITY, -INFINITY};
+      const uint64_t vis0 = rv[0] ? row_vis64(a.mode, c_ctx, n_keys, tok[0], slot0, mrow[0], a.mask_words) : 0ull;
+      const uint64_t vis1 = rv[1] ? row_vis64(a.mode, c_ctx, n_keys, tok[1], slot0, mrow[1], a.mask_words) : 0ull;
 #pragma unroll
       for (int n = 0; n < 8; ++n) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int h = e >> 1;
-          const int slot = slot0 + n * 8 + 2 * cq + (e & 1);
-          float v = sacc[n][e] * a.scale_log2;
-          if (!rv[h] || !visible(a, tok[h], slot, mrow[h])) v = -INFINITY;
+          const int k = n * 8 + 2 * cq + (e & 1);
+          const float v = (((h ? vis1 : vis0) >> k) & 1ull) ? sacc[n][e] * a.scale_log2 : -INFINITY;
           sacc[n][e] = v;
           mx[h] = fmaxf(mx[h], v);
         }
@@ -300,6 +342,289 @@ __global__ void __launch_bounds__(A_THREADS, 1)
         a.ws_ml[row * 2 + 1] = l_run[h];
       }
     }
+  }
+}
+
+
+// ===========================================================================
+// tcgen05 variant (default): S = Q K^T and O += P V on the 5th-gen tensor cores.
+// One CTA = one KV head x one KV split x up to 128 query rows (UMMA M = 128).
+// warp 0: TMA producer (K/V pages, 4-stage ring); warp 1: TMEM owner + single
+// issuing thread; warps 2-5: one thread per query row — Q staging, tcgen05.ld of
+// S, mask + online softmax (lazy O rescale when the row max grows by > 2^8),
+// P -> smem (K-major, 128B swizzle), epilogue.  TMEM: S double buffer (2 x 64
+// columns) + O (128 columns).  V is consumed as an MN-major UMMA operand.
+// ===========================================================================
+__device__ long long* g_attn_trace = nullptr;  // debug: [32 tiles][8] globaltimer stamps of CTA (0,0,0)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TRACE(i, k)                                                                                   \
+  do {                                                                                                \
+    if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 32)            \
+      g_attn_trace[(i) * 8 + (k)] = gtimer();                                                         \
+  } while (0)
+
+constexpr int T_THREADS = 192;
+constexpr int T_STAGES = 4;
+constexpr int T_Q_BYTES = 128 * A_D * 2;   // 32 KiB: two [128 rows][64] SW128 halves
+constexpr int T_P_BYTES = 128 * A_PAGE * 2; // 16 KiB: [128 rows][64 keys]
+constexpr float T_RESCALE = 8.f;            // log2 units
+
+__global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done, q_ready;
+  __shared__ uint32_t tmem_sh;
+  sm100::grid_dep_launch();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
+  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
+  const uint32_t sQ = base, sP = base + T_Q_BYTES, sKV = sP + T_P_BYTES;
+  uint8_t* gQ = smem;
+  uint8_t* gP = smem + T_Q_BYTES;
+  uint8_t* gKV = gP + T_P_BYTES;
+
+  const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
+  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
+  const int n_keys = c_ctx + a.keys_after_c;
+  const int R = a.group * a.s;
+  const int page0 = split * a.pages_per_split;
+  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
+  const int n_tiles = max(min(page0 + a.pages_per_split, n_pages_keys) - page0, 0);
+
+  if (threadIdx.x == 0) {
+    sm100::prefetch_tmap(&tmKV);
+    for (int i = 0; i < T_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&s_free[i], 4); }
+    sm100::mbar_init(&p_full, 4);
+    sm100::mbar_init(&o_done, 1);
+    sm100::mbar_init(&q_ready, 4);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 256);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // PDL: pages entirely below c hold committed K/V the previous kernel does not
+      // touch; the page holding slot c onwards is written by qkv_rope right before us.
+      const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
+      bool waited = false;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % T_STAGES;
+        if (i >= T_STAGES) sm100::mbar_wait(&empty[st], ((i / T_STAGES) & 1) ^ 1);
+        if (!waited && (i >= safe_tiles || i >= T_STAGES)) {
+          sm100::grid_dep_wait();
+          waited = true;
+        }
+        const int phys = a.page_table[page0 + i];
+        const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
+        const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
+        uint8_t* dst = gKV + st * A_STAGE_BYTES;
+        sm100::mbar_expect_tx(&full[st], A_STAGE_BYTES);
+        sm100::tma_load_2d(dst, &tmKV, &full[st], 0, (int)rowK);
+        sm100::tma_load_2d(dst + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowK);
+        sm100::tma_load_2d(dst + A_TILE_BYTES, &tmKV, &full[st], 0, (int)rowV);
+        sm100::tma_load_2d(dst + A_TILE_BYTES + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowV);
+        TRACE(i, 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = sm100::idesc_bf16(128, A_PAGE);
+    const uint32_t idO = sm100::idesc_bf16_bmn(128, A_D);
+    sm100::mbar_wait(&q_ready, 0);
+    for (int i = 0; i <= n_tiles; ++i) {
+      if (i < n_tiles) {
+        const int st = i % T_STAGES, b = i & 1;
+        sm100::mbar_wait(&full[st], (i / T_STAGES) & 1);
+        if (lane == 0) TRACE(i, 1);
+        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t kb = sKV + st * A_STAGE_BYTES;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint64_t ad = sm100::desc_k_sw128(sQ + (j >> 2) * (128 * 128) + (j & 3) * 32);
+            const uint64_t bd = sm100::desc_k_sw128(kb + (j >> 2) * (A_PAGE * 128) + (j & 3) * 32);
+            sm100::umma_f16(tmem + b * A_PAGE, ad, bd, idS, j > 0 ? 1u : 0u);
+          }
+          sm100::umma_commit(&s_full[b]);
+        }
+        __syncwarp();
+      }
+      if (i >= 1) {
+        const int j = i - 1, stj = j % T_STAGES;
+        sm100::mbar_wait(&p_full, j & 1);
+        if (lane == 0) TRACE(j, 2);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t vb = sKV + stj * A_STAGE_BYTES + A_TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sm100::desc_k_sw128(sP + kk * 32);
+            const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
+            sm100::umma_f16(tmem + 128, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          sm100::umma_commit(&o_done);
+          sm100::umma_commit(&empty[stj]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- one thread per query row
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int rg = rb * 128 + row;
+    const bool valid = rg < R;
+    const int rr = valid ? rg : 0;
+    const int tok = rr / a.group;
+    const int qh = head * a.group + rr % a.group;
+    const uint32_t* mrow = a.mode == 0 ? a.anc + (int64_t)tok * a.mask_words : nullptr;
+    const int mode = a.mode, mwords = a.mask_words;
+    const float scale = a.scale_log2;
+    sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
+    {  // stage Q row (256 B) into the swizzled K-major tile
+      const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) {
+        const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(gQ + (q >> 3) * (128 * 128) + row * 128 + (((q & 7) ^ (row & 7)) << 4)) = v;
+      }
+    }
+    sm100::fence_async_shared();
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&q_ready);
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int b = i & 1;
+      sm100::mbar_wait(&s_full[b], (i >> 1) & 1);
+      if (threadIdx.x == 64) TRACE(i, 3);
+      sm100::tc_fence_after();
+      float sv[64];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float t16[16];
+        sm100::tmem_ld16(lane_base + b * A_PAGE + 16 * k, t16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sv[16 * k + e] = t16[e];
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&s_free[b]);
+      if (threadIdx.x == 64) TRACE(i, 7);
+      const int slot0 = (page0 + i) * A_PAGE;
+      const uint64_t vis = valid ? row_vis64(mode, c_ctx, n_keys, tok, slot0, mrow, mwords) : 0ull;
+      float mx8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+      if (__all_sync(0xffffffffu, vis == ~0ull)) {  // prefix tile: no masking
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          sv[k] *= scale;
+          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const float v = ((vis >> k) & 1ull) ? sv[k] * scale : -INFINITY;
+          sv[k] = v;
+          mx8[k & 7] = fmaxf(mx8[k & 7], v);
+        }
+      }
+      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = fmaxf(m_run, mt);
+      const bool rescale = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + T_RESCALE);
+      const float m_ref = rescale ? m_new : m_run;
+      const float alpha = (rescale && m_run != -INFINITY) ? ex2(m_run - m_ref) : (rescale ? 0.f : 1.f);
+      const float msub = m_ref == -INFINITY ? 0.f : m_ref;  // all-masked row: ex2(-inf) = 0
+      float rs8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) rs8[k] = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        const float p0 = ex2(sv[k] - msub);
+        const float p1 = ex2(sv[k + 1] - msub);
+        rs8[(k >> 1) & 7] += p0 + p1;
+        pk[k >> 1] = pack_bf16(p0, p1);
+      }
+      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      if (threadIdx.x == 64) TRACE(i, 4);
+      if (i >= 1) sm100::mbar_wait(&o_done, (i - 1) & 1);  // PV(i-1) done: O stable, P free
+      if (threadIdx.x == 64) TRACE(i, 5);
+      sm100::tc_fence_after();
+      // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it
+      if (__any_sync(0xffffffffu, rescale && i >= 1)) {
+        const float f = (rescale && i >= 1) ? alpha : 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < 8; ++cc) {
+          float ov[16];
+          sm100::tmem_ld16(lane_base + 128 + 16 * cc, ov);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ov[e] *= f;
+          sm100::tmem_st16(lane_base + 128 + 16 * cc, ov);
+        }
+        sm100::tmem_st_wait();
+      }
+      l_run = rescale ? l_run * alpha + rs : l_run + rs;
+      m_run = m_ref;
+#pragma unroll
+      for (int cq = 0; cq < 8; ++cq)
+        *reinterpret_cast<uint4*>(gP + row * 128 + ((cq ^ (row & 7)) << 4)) =
+            make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
+      sm100::fence_async_shared();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&p_full);
+      if (threadIdx.x == 64) TRACE(i, 6);
+    }
+    // ---------------- epilogue
+    float o[128];
+    if (n_tiles > 0) {
+      sm100::mbar_wait(&o_done, (n_tiles - 1) & 1);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < 8; ++cc) {
+        float t16[16];
+        sm100::tmem_ld16(lane_base + 128 + 16 * cc, t16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[16 * cc + e] = t16[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 128; ++e) o[e] = 0.f;
+    }
+    if (valid) {
+      if (a.n_splits == 1) {
+        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+        uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D);
+#pragma unroll
+        for (int q = 0; q < 16; ++q)
+          op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                             pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+      } else {
+        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D);
+#pragma unroll
+        for (int q = 0; q < 32; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        a.ws_ml[r * 2 + 0] = m_run;
+        a.ws_ml[r * 2 + 1] = l_run;
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 256);
   }
 }
 
@@ -413,14 +738,35 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)A_D);
   a.ws_o = ws;
   a.ws_ml = ws ? ws + (size_t)n_splits * s * n_q * A_D : nullptr;
-  const int smem = A_STAGES * A_STAGE_BYTES + 1024;
+  cudaStream_t st = as_stream(stream);
+  static int variant = -1;
+  if (variant < 0) {
+    const char* e = getenv("BST_ATTN");
+    variant = (e && e[0] == 'm') ? 1 : 0;  // BST_ATTN=mma selects the mma.sync kernel (A/B comparisons)
+  }
   static bool attr = false;
+  const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
+  const int smem_tc = T_Q_BYTES + T_P_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
   if (!attr) {
-    BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mma));
+    BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     attr = true;
   }
-  cudaStream_t st = as_stream(stream);
-  attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem, st>>>(tm, a);
+  if (variant == 1)
+    attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
+  else {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_kv, n_splits, row_blocks);
+    cfg.blockDim = dim3(T_THREADS);
+    cfg.dynamicSmemBytes = smem_tc;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, a));
+  }
   if (n_splits > 1) {
     const int rows_total = s * n_q;
     attn_combine_kernel<<<(rows_total + 7) / 8, 256, 0, st>>>(a);
@@ -431,4 +777,9 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
 
 extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {
   return (size_t)(n_splits < 1 ? 1 : n_splits) * s * n_q * (128 + 2) * sizeof(float);
+}
+
+extern "C" int bst_debug_attn_trace(void* buf) {
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_attn_trace, &buf, sizeof(void*)));
+  return BST_OK;
 }
