@@ -240,15 +240,8 @@ def run_ours(args) -> None:
     stats = eng.read_log()[cyc0:cyc0 + args.steps]
     t_ver = [e[1].elapsed_time(e[2]) * 1e-3 for e in per]  # seconds
     t_dr = [e[0].elapsed_time(e[1]) * 1e-3 for e in per]
-    if dist:
-        t = torch.tensor([elapsed, float(tokens)], device="cuda", dtype=torch.float64)
-        mx = t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = t.clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        elapsed, tokens_all = float(mx[0]), float(sm[1])
-    else:
-        tokens_all = float(tokens)
+    from paper_2605_29727_b200.dist import reduce_throughput
+    elapsed, tokens_all, _ = reduce_throughput(elapsed, float(tokens))
     value = tokens_all / elapsed
     # exact kernel count: nodes of the graphs replayed in the timed region
     kd = eng.graph_kernels[id(eng.graph_d)]
@@ -270,13 +263,7 @@ def run_ours(args) -> None:
     e_end.synchronize()
     e2e_time = max(e_start.elapsed_time(e_end) * 1e-3, time.perf_counter() - t0)
     e2e_tokens = sum(r.accepted_len for r in records)
-    e2e_val = e2e_tokens / e2e_time
-    if dist:
-        t = torch.tensor([e2e_time, float(e2e_tokens)], device="cuda", dtype=torch.float64)
-        mx, sm = t.clone(), t.clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        e2e_val = float(sm[1]) / float(mx[0])
+    e2e_val = reduce_throughput(e2e_time, float(e2e_tokens))[2]
     aal_e2e = e2e_tokens / max(1, len(records))
 
     # ---- roofline of the dominant kernel (K4 GEMM) at the timed region's median verify size
