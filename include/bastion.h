@@ -174,6 +174,14 @@ int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* 
 int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* argmax,
                     bst_stream_t stream);
 
+/* L2 prefetch hint: DRAM-idle kernels (attention, epilogues) stream the next
+ * GEMM's weights into L2 while they run (weights never depend on activations). */
+typedef struct {
+  const void* ptr[2];
+  uint64_t bytes[2];
+} bst_prefetch_t;
+int bst_set_prefetch(const bst_prefetch_t* pf); /* applies to the next K3/K5 launch on this thread */
+
 /* ------------------------------------------------------------------------
  * K3 — tree-masked attention over the paged KV cache
  * (mask semantics of linearize, verify_sim.py:336-355; cost PAPER.md:1056-1062).

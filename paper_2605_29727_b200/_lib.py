@@ -50,6 +50,12 @@ class GemmSched(C.Structure):
                 ("partial_floats", C.c_int64)]
 
 
+class Prefetch(C.Structure):
+    """bst_prefetch_t — up to two weight ranges to stream into L2 during the next K3/K5 launch."""
+
+    _fields_ = [("ptr", C.c_void_p * 2), ("bytes", C.c_uint64 * 2)]
+
+
 _P, _I, _I64, _SZ, _D = C.c_void_p, C.c_int, C.c_int64, C.c_size_t, C.c_double
 SIGNATURES = {
     "bst_abi_version": (C.c_int, []),
@@ -79,6 +85,7 @@ SIGNATURES = {
     "bst_verify_rows": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_drafter_rows": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "bst_commit_state": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _I, _P]),
+    "bst_set_prefetch": (_I, [C.POINTER(Prefetch)]),
     "bst_accept": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_kv_compact": (_I, [_P, _I, _I, _I, _I, _I64, _P, _P, _P, _P, _I, _P]),
 }

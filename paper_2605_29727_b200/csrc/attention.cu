@@ -54,6 +54,7 @@ struct AttnArgs {
   float scale_log2;        // softmax scale * log2(e)
   float* ws_o;             // [split][s*n_q][128] unnormalised partial O
   float* ws_ml;            // [split][s*n_q][2] (running max (log2 domain), sum)
+  bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -411,6 +412,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 
   if (warp == 0) {
     if (lane == 0) {
+      issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
+                     gridDim.x * gridDim.y * gridDim.z);
       // PDL: pages entirely below c hold committed K/V the previous kernel does not
       // touch; the page holding slot c onwards is written by qkv_rope right before us.
       const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
@@ -738,6 +741,7 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)A_D);
   a.ws_o = ws;
   a.ws_ml = ws ? ws + (size_t)n_splits * s * n_q * A_D : nullptr;
+  a.pf = take_prefetch();
   cudaStream_t st = as_stream(stream);
   static int variant = -1;
   if (variant < 0) {

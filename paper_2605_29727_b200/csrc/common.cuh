@@ -67,4 +67,7 @@ __host__ __device__ inline double curve_latency(const bst_curve_t& c, long long 
 #endif
 }
 
+// Pending L2-prefetch hint (bst_set_prefetch) consumed by the next K3/K5 launch.
+bst_prefetch_t take_prefetch();
+
 }  // namespace bst

@@ -63,8 +63,9 @@ __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const _
 constexpr int R_THREADS = 1024;
 __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
     const float* __restrict__ partial, bst_gemm_sched_t s, float* resid, int h, const __nv_bfloat16* __restrict__ w,
-    float eps, __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf, int rows) {
+    float eps, __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf, int rows, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   __shared__ float sh[32];
   __shared__ float4 vals[2048];
   const int t = blockIdx.x;
@@ -106,8 +107,9 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
                                 const float* __restrict__ inv_freq, const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                 const int32_t* __restrict__ qrow, __nv_bfloat16* q_out, int64_t q_tok_stride,
                                 __nv_bfloat16* kv, int64_t layer_off, const int32_t* __restrict__ page_table,
-                                int page_size, const int32_t* __restrict__ state, int state_c_idx) {
+                                int page_size, const int32_t* __restrict__ state, int state_c_idx, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -166,7 +168,8 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
 
 // ---------------------------------------------------------------- swiglu
 __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int ffn, __nv_bfloat16* act,
-                              int64_t lda) {
+                              int64_t lda, bst_prefetch_t pf) {
+  if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
   const int t = blockIdx.y;
   sm100::grid_dep_launch();
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (ffn >> 2); g += gridDim.x * blockDim.x) {
@@ -214,7 +217,7 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   if (sched) s = *sched;
   residual_rmsnorm_kernel<<<rows, R_THREADS, 0, as_stream(stream)>>>(
       partial, s, resid, h, static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
-      static_cast<__nv_bfloat16*>(feat), ldf, rows);
+      static_cast<__nv_bfloat16*>(feat), ldf, rows, take_prefetch());
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -230,7 +233,7 @@ extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched,
   qkv_rope_kernel<<<rows, 512, 0, as_stream(stream)>>>(
       partial, *sched, n_q, n_kv, static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm),
       eps, inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride, static_cast<__nv_bfloat16*>(kv),
-      layer_off_elems, page_table, page_size, state, state_c_idx);
+      layer_off_elems, page_table, page_size, state, state_c_idx, take_prefetch());
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -240,7 +243,8 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
   BST_REQUIRE(partial && sched && act, "null pointer argument");
   BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
   dim3 grid((ffn / 4 + 255) / 256, rows);
-  swiglu_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, *sched, ffn, static_cast<__nv_bfloat16*>(act), lda);
+  swiglu_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, *sched, ffn, static_cast<__nv_bfloat16*>(act), lda,
+                                                     take_prefetch());
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

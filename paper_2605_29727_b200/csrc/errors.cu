@@ -16,3 +16,17 @@ void set_error(const char* fmt, ...) {
 
 extern "C" int bst_abi_version(void) { return 1; }
 extern "C" const char* bst_last_error(void) { return bst::g_err; }
+
+namespace bst {
+static thread_local bst_prefetch_t g_pf = {};
+bst_prefetch_t take_prefetch() {
+  bst_prefetch_t p = g_pf;
+  g_pf = bst_prefetch_t{};
+  return p;
+}
+}  // namespace bst
+
+extern "C" int bst_set_prefetch(const bst_prefetch_t* pf) {
+  bst::g_pf = pf ? *pf : bst_prefetch_t{};
+  return BST_OK;
+}

@@ -112,6 +112,16 @@ int cached_tmap(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols,
 }
 
 // ------------------------------------------------------------------ kernel
+__device__ long long* g_gemm_trace = nullptr;  // debug: globaltimer stamps of CTA g_trace_cta
+__device__ int g_trace_cta = 0;
+__device__ __forceinline__ void gtrace(int k) {
+  if (g_gemm_trace && blockIdx.x == g_trace_cta && k < 64) {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_gemm_trace[k] = t;
+  }
+}
+
 struct Seg {
   int tile, kb_lo, kb_hi, slot;
 };
@@ -134,6 +144,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) gtrace(0);
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
   const int bn = s.bn;
@@ -153,6 +164,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = tmem_base_sh;
+  if (threadIdx.x == 0) gtrace(1);
 
   const int64_t u0 = (int64_t)blockIdx.x * s.units / s.grid;
   const int64_t u1 = (int64_t)(blockIdx.x + 1) * s.units / s.grid;
@@ -183,7 +195,9 @@ __global__ void __launch_bounds__(G_THREADS, 1)
         }
         issued = st;
       }
+      gtrace(2);
       sm100::grid_dep_wait();
+      gtrace(3);
       int idx = 0;
       while (next_seg(s, u, u1, seg)) {
         for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb, ++idx) {
@@ -216,6 +230,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       const uint32_t d = tmem + acc * bn;
       for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
         sm100::mbar_wait(&full[stage], phase);
+        if (lane == 0) gtrace(8 + (kb - seg.kb_lo) + j * 24);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           const uint32_t a_addr = base + stage * stage_bytes;
@@ -256,6 +271,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&tempty[acc]);
+      if (lane == 0 && quad == 0) gtrace(4 + j);
       ++j;
     }
   }
@@ -264,6 +280,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, tcols);
   }
+  if (threadIdx.x == 0) gtrace(7);
 }
 
 // ------------------------------------------------------ reduction kernels
@@ -422,5 +439,11 @@ extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sch
   argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
                                                             argmax);
   BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_debug_gemm_trace(void* buf, int cta) {
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_gemm_trace, &buf, sizeof(void*)));
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_trace_cta, &cta, sizeof(int)));
   return BST_OK;
 }

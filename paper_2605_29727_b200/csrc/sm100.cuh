@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "../../include/bastion.h"
+
 namespace bst {
 namespace sm100 {
 
@@ -70,6 +72,22 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
+}
+// Fire-and-forget bulk prefetch into L2 (size multiple of 16 B).
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Split [ptr, ptr+bytes) over `parts` issuers; issuer `idx` prefetches its share in 256 KiB pieces.
+__device__ __forceinline__ void prefetch_share(const void* ptr, uint64_t bytes, int idx, int parts) {
+  if (!ptr || bytes == 0) return;
+  const uint64_t share = ((bytes + parts - 1) / parts + 15) & ~15ull;
+  const uint64_t lo = share * idx;
+  if (lo >= bytes) return;
+  const uint64_t hi = lo + share < bytes ? lo + share : bytes;
+  for (uint64_t o = lo; o < hi; o += (256u << 10)) {
+    const uint64_t n = (hi - o) < (256u << 10) ? (hi - o) : (256u << 10);
+    prefetch_l2(static_cast<const char*>(ptr) + o, (uint32_t)(n & ~15ull));
+  }
 }
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(map) : "memory");
@@ -161,4 +179,9 @@ __device__ __forceinline__ bool elect_one() {
 }
 
 }  // namespace sm100
+
+__device__ __forceinline__ void issue_prefetch(const bst_prefetch_t& pf, int idx, int parts) {
+  sm100::prefetch_share(pf.ptr[0], pf.bytes[0], idx, parts);
+  sm100::prefetch_share(pf.ptr[1], pf.bytes[1], idx, parts);
+}
 }  // namespace bst

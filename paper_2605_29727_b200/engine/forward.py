@@ -24,8 +24,21 @@ from .. import ops
 from .config import DrafterConfig, ModelConfig
 from .weights import DrafterWeights, TargetWeights, rope_inv_freq
 
+import os
+
 PAGE = 64
 MODE_TREE, MODE_CAUSAL, MODE_FULL = 0, 1, 2
+# profiling only: skip kernel families to measure their in-graph cost (results become garbage)
+_ABLATE = set(filter(None, os.environ.get("BST_ABLATE", "").split(",")))
+# L2 weight prefetch during DRAM-idle kernels: off by default (measured no gain: the small
+# GEMMs are bound by per-SM TMA issue + DRAM burst latency, not by DRAM bytes); BST_PREFETCH=1
+_PREFETCH = os.environ.get("BST_PREFETCH", "0") == "1"
+MB = 1 << 20
+
+
+def _pf(*ranges) -> None:
+    if _PREFETCH:
+        ops.set_prefetch(*ranges)
 SKIP_SLOT = -(2**31)
 
 
@@ -95,23 +108,33 @@ class TargetModel:
         x, resid = self.x[:n], self.resid[:n]
         ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
         for li, lw in enumerate(w.layers):
+            nxt_l = w.layers[li + 1] if li + 1 < cfg.L else None
             p = ops.gemm_partial(x, lw.qkv, out=self.partial)
-            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
-                         None, self.q, kv.buf, li * kv.layer_stride, kv.page_table, PAGE, state)
-            ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, kv.page_table, cfg.n_q,
-                          cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
-                          self.attn_ws)
+            if "rope" not in _ABLATE:
+                ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
+                             None, self.q, kv.buf, li * kv.layer_stride, kv.page_table, PAGE, state)
+            if "attn" not in _ABLATE:
+                _pf((lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB))
+                ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, kv.page_table, cfg.n_q,
+                              cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
+                              self.attn_ws)
             p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
-            ops.residual_rmsnorm(p, resid, n, cfg.h, lw.post_norm, eps, x=x)
+            if "resid" not in _ABLATE:
+                _pf((lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
+                ops.residual_rmsnorm(p, resid, n, cfg.h, lw.post_norm, eps, x=x)
             p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
-            ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
+            if "swiglu" not in _ABLATE:
+                _pf((lw.down, 16 * MB))
+                ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
             p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
             nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
             feat = None
             if li in self.feat_layers:
                 j = self.feat_layers.index(li)
                 feat = self.feat[:n, j * cfg.h:(j + 1) * cfg.h]
-            ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
+            if "resid" not in _ABLATE:
+                _pf((nxt_l.qkv, 64 * MB) if nxt_l is not None else (w.lm_head, 48 * MB))
+                ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
         if head == "argmax":
             p = ops.gemm_partial(x, w.lm_head, out=self.partial)
             ops.gemm_argmax(p, out=self.argmax[:n], scratch=self.amx_scratch)

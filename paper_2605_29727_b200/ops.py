@@ -128,3 +128,15 @@ def commit_state(state, accept_meta, committed, max_path, out_tokens, tree_meta=
     _lib.call("bst_commit_state", state.data_ptr(), accept_meta.data_ptr(), committed.data_ptr(), max_path,
               out_tokens.data_ptr(), out_tokens.numel(), _p(tree_meta), _p(surrogate), _p(log_i32), _p(log_f64), cap,
               stream_ptr())
+
+
+def set_prefetch(*ranges) -> None:
+    """L2 prefetch hint for the next K3/K5 launch: up to two (tensor, max_bytes) ranges."""
+    pf = _lib.Prefetch()
+    for i, (t, nbytes) in enumerate(ranges[:2]):
+        if t is None:
+            continue
+        n = min(int(nbytes), t.numel() * t.element_size()) & ~15
+        pf.ptr[i] = t.data_ptr()
+        pf.bytes[i] = n
+    _lib.call("bst_set_prefetch", C.byref(pf))
