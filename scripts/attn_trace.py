@@ -29,6 +29,6 @@ run()
 torch.cuda.synchronize()
 t = tr.view(32, 8).cpu()
 t0 = int(t[0, 0])
-names = ["tma_issued", "mma:full", "mma:p_full", "sm:s_full", "sm:sm_done", "sm:o_done", "sm:p_arrive", "sm:ld_done"]
+names = ["tma_issued", "mma:full", "mma:p_full", "sm:s_full", "sm:sm_done", "sm:o_done", "sm:p_arrive", "sm:max_local"]
 for i in range(min(32, 30)):
     print(i, " ".join(f"{n}={(int(t[i, k]) - t0) / 1000:8.2f}" if int(t[i, k]) else f"{n}=   -    " for k, n in enumerate(names)))
