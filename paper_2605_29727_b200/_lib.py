@@ -119,7 +119,7 @@ def check(rc: int) -> None:
 
 # kernels launched by one call of each C-ABI entry point (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "bst_topk_logits": 4, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_linearize_mask": 1,
+    "bst_topk_logits": 3, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_linearize_mask": 1,
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
     "bst_gemm_argmax": 2, "bst_attention": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,

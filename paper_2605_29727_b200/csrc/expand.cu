@@ -35,6 +35,15 @@ constexpr int EX_MAXG = 127;
 constexpr int EX_MAXK = 128;
 constexpr unsigned short NO_PARENT = 0xFFFF;
 
+__device__ long long* g_ex_trace = nullptr;
+__device__ __forceinline__ void ex_trace(int k) {
+  if (g_ex_trace && threadIdx.x == 0 && k < 16) {
+    long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    g_ex_trace[k] = t;
+  }
+}
+
 struct HeapEntry {
   double rho;
   unsigned long long lo;  // depth<<44 | token<<20 | parent
@@ -116,6 +125,8 @@ struct ExSmem {
   int n_runs, overflow, n_enum, all_enumerated, min_stop, best_idx, max_depth;
   double best_val;
   double tau;
+  double lat_p[2048];  // lattice staged in smem when gamma*k <= 2048
+  int lat_t[2048];
 };
 
 struct ExWs {
@@ -153,8 +164,12 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
   const unsigned int SAT = 1u << 30;
   __shared__ int s_bstar;
   int* cost = reinterpret_cast<int*>(sm.lo);  // [gamma*k] quantized -log2(p), lo is free here
-  for (int pass = 0; pass < 2; ++pass) {
-    const double S = pass == 0 ? 16.0 : 2.0;
+  __shared__ int s_range, s_cross;
+  for (int pass = 0; pass < 3; ++pass) {
+    // pass 0: 1/16-bit bins up to 2^-64 (typical drafter rows); pass 1: up to 2^-256;
+    // pass 2: 1/2-bit bins covering the whole fp64 range
+    const double S = pass < 2 ? 16.0 : 2.0;
+    const int max_range = pass == 0 ? 1024 : EX_BINS;
     // est cost = floor(-log2(p) * S) + 1 >= the true scaled cost, so a path's
     // summed est cost never undercounts: est <= B  =>  rho > 2^(-(B+1)/S).
     for (int e = threadIdx.x; e < gamma * k; e += EX_THREADS) {
@@ -163,6 +178,7 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
       cost[e] = c < 0.0 ? -1 : (c < EX_BINS ? (int)c : EX_BINS);
     }
     for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) { hprev[b] = 0; tot[b] = 0; }
+    if (threadIdx.x == 0) { s_range = max_range; s_cross = 0; }
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int r = 0; r < k; ++r)
@@ -171,34 +187,62 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
     __syncthreads();
     for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) tot[b] = hprev[b];
     __syncthreads();
+    // first bin whose cumulative count (capped per bin at n_max) reaches n_max
+    auto crossing = [&](int range) {
+      const int per = (range + EX_THREADS - 1) / EX_THREADS;
+      const int b0 = threadIdx.x * per;
+      int loc = 0;
+      for (int b = b0; b < min(b0 + per, range); ++b) loc += (int)min((unsigned int)n_max, tot[b]);
+      int total;
+      int run = block_excl_scan(loc, sm.scan, &total);
+      if (total >= n_max) {
+        for (int b = b0; b < min(b0 + per, range); ++b) {
+          run += (int)min((unsigned int)n_max, tot[b]);
+          if (run >= n_max) {
+            atomicMin(&s_range, b + 1);
+            s_cross = 1;
+            break;
+          }
+        }
+      }
+      __syncthreads();
+    };
+    crossing(max_range);
     for (int d = 2; d <= gamma; ++d) {
-      const int* cr = cost + (d - 1) * k;
-      for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) {
+      // the crossing bin B* only moves down as levels are added, so bins above
+      // the current crossing never matter for the remaining levels
+      const int range = s_range;
+      int cr[8];
+      int nk = 0;
+      for (int r = 0; r < k && r < 8; ++r) {
+        cr[r] = cost[(d - 1) * k + r];
+        if (cr[r] >= 0) nk = r + 1;
+      }
+      for (int b = threadIdx.x; b < range; b += EX_THREADS) {
         unsigned long long acc = 0;
-        for (int r = 0; r < k; ++r) {
-          const int ci = cr[r];
-          if (ci < 0) break;  // sorted desc: the rest are 0 as well
-          if (ci <= b) acc += hprev[b - ci];
+        if (k <= 8) {
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+            if (r < nk && cr[r] <= b) acc += hprev[b - cr[r]];
+        } else {
+          for (int r = 0; r < k; ++r) {
+            const int ci = cost[(d - 1) * k + r];
+            if (ci < 0) break;
+            if (ci <= b) acc += hprev[b - ci];
+          }
         }
         hcur[b] = acc > SAT ? SAT : (unsigned int)acc;
       }
       __syncthreads();
-      for (int b = threadIdx.x; b < EX_BINS; b += EX_THREADS) {
+      for (int b = threadIdx.x; b < range; b += EX_THREADS) {
         hprev[b] = hcur[b];
         unsigned long long t = (unsigned long long)tot[b] + hcur[b];
         tot[b] = t > SAT ? SAT : (unsigned int)t;
       }
       __syncthreads();
+      crossing(range);
     }
-    if (threadIdx.x == 0) {
-      unsigned long long cum = 0;
-      int bstar = -1;
-      for (int b = 0; b < EX_BINS; ++b) {
-        cum += tot[b];
-        if (cum >= (unsigned long long)n_max) { bstar = b; break; }
-      }
-      s_bstar = bstar;
-    }
+    if (threadIdx.x == 0) s_bstar = s_cross ? s_range - 1 : -1;
     __syncthreads();
     int bstar = s_bstar;
     __syncthreads();
@@ -226,7 +270,7 @@ __device__ bool enumerate_nodes(const int32_t* tok, const double* prob, int gamm
       if (pi >= n_par) break;
       double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
       for (int r = 0; r < k; ++r) {
-        double v = __dmul_rn(prho, __ldg(pr + r));
+        double v = __dmul_rn(prho, pr[r]);
         if (!(v > 0.0) || v < tau) break;
         ++cnt;
       }
@@ -245,10 +289,10 @@ __device__ bool enumerate_nodes(const int32_t* tok, const double* prob, int gamm
       if (pi >= n_par) break;
       double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
       for (int r = 0; r < k; ++r) {
-        double v = __dmul_rn(prho, __ldg(pr + r));
+        double v = __dmul_rn(prho, pr[r]);
         if (!(v > 0.0) || v < tau) break;
         sm.hi[w] = ~dbits(v);
-        sm.lo[w] = ((unsigned long long)d << 40) | ((unsigned long long)(unsigned)__ldg(tr + r) << 16) |
+        sm.lo[w] = ((unsigned long long)d << 40) | ((unsigned long long)(unsigned)tr[r] << 16) |
                    (unsigned long long)w;
         sm.par[w] = d == 1 ? NO_PARENT : (unsigned short)(prev_lo + pi);
         sm.rnk[w] = (unsigned char)r;
@@ -279,20 +323,26 @@ __device__ void bitonic_sort(ExSmem& sm, int n) {
   while (p2 < n) p2 <<= 1;
   for (int i = n + threadIdx.x; i < p2; i += EX_THREADS) { sm.hi[i] = ~0ull; sm.lo[i] = ~0ull; }
   __syncthreads();
-  for (int kk = 2; kk <= p2; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
-      for (int i = threadIdx.x; i < (p2 >> 1); i += EX_THREADS) {
-        int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-        int b = a + j;
-        bool asc = (a & kk) == 0;
-        unsigned long long ah = sm.hi[a], al = sm.lo[a], bh = sm.hi[b], bl = sm.lo[b];
-        if (key_gt(ah, al, bh, bl) == asc) {
-          sm.hi[a] = bh; sm.lo[a] = bl; sm.hi[b] = ah; sm.lo[b] = al;
+  // only as many warps as there are compare-exchange pairs take part (named barrier)
+  const int active = min(EX_THREADS, max(32, p2 >> 1));
+  if (threadIdx.x < active) {
+    for (int kk = 2; kk <= p2; kk <<= 1) {
+      for (int j = kk >> 1; j > 0; j >>= 1) {
+        for (int i = threadIdx.x; i < (p2 >> 1); i += active) {
+          int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          int b = a + j;
+          bool asc = (a & kk) == 0;
+          unsigned long long ah = sm.hi[a], al = sm.lo[a], bh = sm.hi[b], bl = sm.lo[b];
+          if (key_gt(ah, al, bh, bl) == asc) {
+            sm.hi[a] = bh; sm.lo[a] = bl; sm.hi[b] = ah; sm.lo[b] = al;
+          }
         }
+        if (active == EX_THREADS) __syncthreads();
+        else asm volatile("bar.sync 2, %0;" ::"r"(active));
       }
-      __syncthreads();
     }
   }
+  __syncthreads();
 }
 
 // Repair exact (rho, depth, token) ties by the parent's final position.
@@ -392,12 +442,46 @@ __device__ int heap_expand(const int32_t* tok, const double* prob, int gamma, in
 // ancestor bitmask and children CSR for the first n_nodes rows.
 __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive, int n_max, const bst_plan_t& plan,
                             const bst_tree_t& out, const ExWs& ws, int algo_used, int enumerated, ExSmem& sm) {
+  // Stage rho / parent of rows 0..n_eval in shared memory (the sort arrays are free
+  // now): every sequential walk below then runs at smem latency, not DRAM latency.
+  const bool in_smem = n_eval + 1 <= EX_CAP;
+  double* rho_s = reinterpret_cast<double*>(sm.hi);
+  int* par_s = reinterpret_cast<int*>(sm.lo);
+  int* cnt_s = par_s + EX_CAP;  // [EX_CAP + 2]... lo holds 2*EX_CAP ints
   if (threadIdx.x == 0) {
     out.parent[0] = -1; out.depth[0] = 0; out.token[0] = -1; out.rank[0] = -1; out.rho[0] = 1.0;
+  }
+  if (in_smem) {
+    for (int i = threadIdx.x; i <= n_eval; i += EX_THREADS) {
+      rho_s[i] = i == 0 ? 1.0 : out.rho[i];
+      par_s[i] = i == 0 ? -1 : out.parent[i];
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    // controller.py:85 / draft_tree.py:153 addition order; 8 loads in flight per step
     double a = 1.0;
-    for (int i = 0; i < n_eval; ++i) {  // controller.py:85 / draft_tree.py:153 order
-      a = __dadd_rn(a, out.rho[i + 1]);
-      ws.ahat[i] = a;
+    int i = 0;
+    if (in_smem) {
+      for (; i + 8 <= n_eval; i += 8) {
+        double r[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) r[k] = rho_s[i + 1 + k];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          a = __dadd_rn(a, r[k]);
+          ws.ahat[i + k] = a;
+        }
+      }
+      for (; i < n_eval; ++i) {
+        a = __dadd_rn(a, rho_s[i + 1]);
+        ws.ahat[i] = a;
+      }
+    } else {
+      for (; i < n_eval; ++i) {
+        a = __dadd_rn(a, out.rho[i + 1]);
+        ws.ahat[i] = a;
+      }
     }
   }
   __syncthreads();
@@ -436,7 +520,6 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
     int bi = 0x7fffffff;
     for (int i = threadIdx.x; i < n_expanded; i += EX_THREADS)
       if (shat[i] > bv) { bv = shat[i]; bi = i; }
-    // reduce (max value, then min index)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       double ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -466,7 +549,7 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
     out.meta[4] = enumerated;
     out.surrogate[0] = n_nodes > 0 ? ws.ahat[n_nodes - 1] : 1.0;
   }
-  // ancestor-or-self bitmask rows 0..n_nodes
+  // ancestor-or-self bitmask rows 0..n_nodes (walks parents in smem)
   if (out.anc_mask) {
     const int W = out.mask_words;
     for (int i = threadIdx.x; i <= n_nodes; i += EX_THREADS) {
@@ -475,30 +558,55 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
       int j = i;
       while (j >= 0) {
         row[j >> 5] |= 1u << (j & 31);
-        j = j == 0 ? -1 : out.parent[j];
+        j = j == 0 ? -1 : (in_smem ? par_s[j] : out.parent[j]);
       }
     }
   }
-  // children CSR
+  // children CSR: counts in smem, block exclusive scan, stable fill by child id
   if (out.child_start && out.child_list) {
-    for (int i = threadIdx.x; i <= n_nodes + 1; i += EX_THREADS) ws.counts[i] = 0;
-    __syncthreads();
-    for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) atomicAdd(&ws.counts[out.parent[i]], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int acc = 0;
-      for (int i = 0; i <= n_nodes; ++i) {
-        int c = ws.counts[i];
-        out.child_start[i] = acc;
-        ws.counts[i] = acc;
-        acc += c;
+    if (in_smem && n_nodes + 2 <= EX_CAP) {
+      for (int i = threadIdx.x; i <= n_nodes + 1; i += EX_THREADS) cnt_s[i] = 0;
+      __syncthreads();
+      for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) atomicAdd(&cnt_s[par_s[i]], 1);
+      __syncthreads();
+      const int per = (n_nodes + 1 + EX_THREADS - 1) / EX_THREADS;
+      const int b0 = threadIdx.x * per;
+      int loc = 0;
+      for (int i = b0; i < min(b0 + per, n_nodes + 1); ++i) loc += cnt_s[i];
+      int total;
+      int off = block_excl_scan(loc, sm.scan, &total);
+      for (int i = b0; i < min(b0 + per, n_nodes + 1); ++i) {
+        const int c = cnt_s[i];
+        out.child_start[i] = off;
+        cnt_s[i] = off;
+        off += c;
       }
-      out.child_start[n_nodes + 1] = acc;
-    }
-    __syncthreads();
-    for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) {
-      int slot = atomicAdd(&ws.counts[out.parent[i]], 1);
-      out.child_list[slot] = i;
+      if (threadIdx.x == 0) out.child_start[n_nodes + 1] = total;
+      __syncthreads();
+      for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) {
+        const int slot = atomicAdd(&cnt_s[par_s[i]], 1);
+        out.child_list[slot] = i;
+      }
+    } else {
+      for (int i = threadIdx.x; i <= n_nodes + 1; i += EX_THREADS) ws.counts[i] = 0;
+      __syncthreads();
+      for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) atomicAdd(&ws.counts[out.parent[i]], 1);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        int acc = 0;
+        for (int i = 0; i <= n_nodes; ++i) {
+          int c = ws.counts[i];
+          out.child_start[i] = acc;
+          ws.counts[i] = acc;
+          acc += c;
+        }
+        out.child_start[n_nodes + 1] = acc;
+      }
+      __syncthreads();
+      for (int i = 1 + threadIdx.x; i <= n_nodes; i += EX_THREADS) {
+        int slot = atomicAdd(&ws.counts[out.parent[i]], 1);
+        out.child_list[slot] = i;
+      }
     }
   }
 }
@@ -536,15 +644,24 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
   int algo_used = BST_ALGO_SORT;
   bool ok = false;
   int enumerated = 0;
+  ex_trace(0);
   if (plan.algo != BST_ALGO_HEAP) {
     double tau = estimate_tau(prob, gamma, k, limit, sm);
+    const bool staged = gamma * k <= 2048;
+    if (staged)
+      for (int e = threadIdx.x; e < gamma * k; e += EX_THREADS) { sm.lat_p[e] = prob[e]; sm.lat_t[e] = tok[e]; }
     __syncthreads();
-    ok = enumerate_nodes(tok, prob, gamma, k, tau > 0.0 ? tau : 4.9406564584124654e-324, sm);
+    ex_trace(1);
+    ok = enumerate_nodes(staged ? sm.lat_t : tok, staged ? sm.lat_p : prob, gamma, k,
+                         tau > 0.0 ? tau : 4.9406564584124654e-324, sm);
+    ex_trace(2);
     if (ok) {
       const int n = sm.n_enum;
       enumerated = n;
       bitonic_sort(sm, n);
+      ex_trace(3);
       fix_ties(sm, n);
+      ex_trace(4);
       n_eval = min(limit, n);
       for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
         unsigned long long lo = sm.lo[i];
@@ -570,7 +687,10 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
     n_eval = s_n;
   }
   __syncthreads();
+  ex_trace(5);
   finish_tree(n_eval, adaptive, true, n_max, plan, out, ws, algo_used, enumerated, sm);
+  __syncthreads();
+  ex_trace(6);
 }
 
 // ------------------------------------------------------------------- beam
@@ -731,5 +851,10 @@ extern "C" int bst_expand_dev(const int32_t* tok, const double* prob, int gamma,
   expand_best_first_kernel<<<1, EX_THREADS, smem, as_stream(stream)>>>(tok, prob, gamma, k, p, plan_dev, n_cap, *out,
                                                                         w, heap_in_smem);
   BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_debug_expand_trace(void* buf) {
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_ex_trace, &buf, sizeof(void*)));
   return BST_OK;
 }

@@ -6,9 +6,13 @@
 // lattice equals top_k_truncate applied to the fp64 rows this kernel also
 // emits (probs_full) — bit for bit.
 //
-// Four short launches per call, all grid-parallel over (chunk, row):
-//   A: per-chunk fp32 max                  B: per-chunk fp64 sum exp(l - m)
-//   C: probs + per-chunk top-K             D: per-row merge of chunk candidates
+// Logits (hot path): k1_fast_chunk (per chunk: max, fp64 sum, top-(K+1) by
+// logit) -> k1_fast_finalize (per row: m, Z, exact fp64 probs of the K
+// survivors, (prob desc, token asc) order, boundary check) -> k1_fast_fallback
+// (exact full-row selection, only for rows whose K/K+1 boundary logits are
+// distinct but < 1e-12 apart).  fp64 MarginalBlock rows are probs_full.
+// fp64 probability input (top_k_truncate): exact chunked selection on the
+// probabilities themselves (k1_chunk_select + k1_merge).
 // The row is split in CHUNK-element chunks so gamma=16 rows of V=151936 fill
 // ~600 CTAs (4 waves of 148 SMs) instead of 16.
 #include <cuda_bf16.h>
@@ -27,6 +31,9 @@ struct TopkWs {
   double* psum;    // [gamma][chunks]
   double* cprob;   // [gamma][chunks][k]
   int32_t* ctok;   // [gamma][chunks][k]
+  unsigned long long* ckeys;  // [gamma][chunks][k+1] (fast logits path)
+  double* stats;   // [gamma][2] (m, Z)
+  int* fallback;   // [gamma]
 };
 
 static size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
@@ -43,6 +50,12 @@ static TopkWs carve(void* ws, int gamma, int chunks, int k, size_t* total) {
   off += align_up(sizeof(double) * gamma * chunks * k);
   w.ctok = reinterpret_cast<int32_t*>(p + off);
   off += align_up(sizeof(int32_t) * gamma * chunks * k);
+  w.ckeys = reinterpret_cast<unsigned long long*>(p + off);
+  off += align_up(sizeof(unsigned long long) * gamma * chunks * (k + 1));
+  w.stats = reinterpret_cast<double*>(p + off);
+  off += align_up(sizeof(double) * gamma * 2);
+  w.fallback = reinterpret_cast<int*>(p + off);
+  off += align_up(sizeof(int) * gamma);
   *total = off;
   return w;
 }
@@ -226,6 +239,227 @@ __global__ void __launch_bounds__(TK_THREADS) k1_merge(const double* cprob, cons
   block_extract(p, t, TK_PER_THREAD, k, prob_out + (int64_t)row * k, tok_out + (int64_t)row * k);
 }
 
+
+// ===========================================================================
+// Fast path for logits (default): top-(K+1) by (logit desc, token asc) per
+// chunk, then exact fp64 probabilities for the survivors only.
+// prob_v = exp64(l_v - m) / Z is non-decreasing in l_v, so the top-K by
+// (prob desc, token asc) equals the top-K by (logit desc, token asc) unless two
+// DISTINCT logits at the K boundary are within 1e-12 (where fp64 rounding could
+// tie or swap them) — that row then takes the exact full-row path.
+// ===========================================================================
+constexpr int TK_KP_MAX = 65;
+
+__device__ __forceinline__ unsigned long long logit_key(float l, int tok) {
+  unsigned int b = __float_as_uint(l);
+  b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+  return ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)tok);
+}
+__device__ __forceinline__ float key_logit(unsigned long long k) {
+  unsigned int b = (unsigned int)(k >> 32);
+  b = (b & 0x80000000u) ? (b & 0x7FFFFFFFu) : ~b;
+  return __uint_as_float(b);
+}
+__device__ __forceinline__ int key_tok(unsigned long long k) { return (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFu)); }
+
+// block-wide: top-n keys (descending) of per-thread candidate lists
+__device__ void block_top_keys(unsigned long long (&c)[TK_PER_THREAD], int n, unsigned long long* out) {
+  __shared__ unsigned long long wbest[TK_THREADS / 32];
+  __shared__ unsigned long long gbest;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int r = 0; r < n; ++r) {
+    unsigned long long b = 0;
+#pragma unroll
+    for (int i = 0; i < TK_PER_THREAD; ++i) b = c[i] > b ? c[i] : b;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+      b = ob > b ? ob : b;
+    }
+    if (lane == 0) wbest[warp] = b;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long g = 0;
+      for (int w = 0; w < TK_THREADS / 32; ++w) g = wbest[w] > g ? wbest[w] : g;
+      gbest = g;
+      out[r] = g;
+    }
+    __syncthreads();
+    const unsigned long long g = gbest;
+#pragma unroll
+    for (int i = 0; i < TK_PER_THREAD; ++i)
+      if (c[i] == g) c[i] = 0;  // keys are unique (token in the low bits)
+  }
+}
+
+// A: per (chunk, row): fp32 max m_c, fp64 S_c = sum exp(l - m_c), top-(K+1) keys
+__global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(const void* logits, int dtype, int vocab, int64_t stride,
+                                                            int kp, float* pmax, double* psum,
+                                                            unsigned long long* ckeys) {
+  const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
+  const int64_t base = (int64_t)row * stride;
+  float l[TK_PER_THREAD];
+  unsigned long long key[TK_PER_THREAD];
+  float m = -INFINITY;
+#pragma unroll
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    const int v = chunk * TK_CHUNK + i * TK_THREADS + threadIdx.x;
+    if (v < vocab) {
+      l[i] = load_logit(logits, dtype, base + v);
+      key[i] = logit_key(l[i], v);
+      m = fmaxf(m, l[i]);
+    } else {
+      l[i] = -INFINITY;
+      key[i] = 0;
+    }
+  }
+  __shared__ float wm[TK_THREADS / 32];
+  __shared__ double ws_[TK_THREADS / 32];
+  __shared__ float sm_m;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float r = wm[0];
+    for (int w = 1; w < TK_THREADS / 32; ++w) r = fmaxf(r, wm[w]);
+    sm_m = r;
+  }
+  __syncthreads();
+  const double mc = (double)sm_m;
+  double sacc = 0.0;
+#pragma unroll
+  for (int i = 0; i < TK_PER_THREAD; ++i)
+    if (key[i]) sacc = __dadd_rn(sacc, exp((double)l[i] - mc));
+  sacc = warp_sum(sacc);
+  if ((threadIdx.x & 31) == 0) ws_[threadIdx.x >> 5] = sacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double r = 0.0;
+    for (int w = 0; w < TK_THREADS / 32; ++w) r = __dadd_rn(r, ws_[w]);
+    pmax[row * chunks + chunk] = sm_m;
+    psum[row * chunks + chunk] = r;
+  }
+  block_top_keys(key, kp, ckeys + ((int64_t)row * chunks + chunk) * kp);
+}
+
+// B: per row: m, Z (fixed order), global top-(K+1), exact fp64 probs, boundary check
+__global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax, const double* psum,
+                                                               const unsigned long long* ckeys, int chunks, int kp,
+                                                               int k, int32_t* tok_out, double* prob_out,
+                                                               double* stats, int* fallback) {
+  const int row = blockIdx.x;
+  const int n = chunks * kp;
+  unsigned long long c[TK_PER_THREAD];
+#pragma unroll
+  for (int i = 0; i < TK_PER_THREAD; ++i) {
+    const int j = i * TK_THREADS + threadIdx.x;
+    c[i] = j < n ? ckeys[(int64_t)row * n + j] : 0ull;
+  }
+  __shared__ unsigned long long top[TK_KP_MAX];
+  block_top_keys(c, kp, top);
+  if (threadIdx.x == 0) {
+    float mf = -INFINITY;
+    for (int j = 0; j < chunks; ++j) mf = fmaxf(mf, pmax[row * chunks + j]);
+    const double m = (double)mf;
+    double z = 0.0;
+    for (int j = 0; j < chunks; ++j)
+      z = __dadd_rn(z, __dmul_rn(exp((double)pmax[row * chunks + j] - m), psum[row * chunks + j]));
+    stats[row * 2] = m;
+    stats[row * 2 + 1] = z;
+    // boundary: the K-th and (K+1)-th by logit must be equal or >= 1e-12 apart
+    int fb = 0;
+    if (kp > k && top[k] != 0ull) {
+      const double gap = (double)key_logit(top[k - 1]) - (double)key_logit(top[k]);
+      if (gap > 0.0 && gap < 1e-12) fb = 1;
+    }
+    fallback[row] = fb;
+    // exact probabilities, then (prob desc, token asc) insertion sort of the K survivors
+    double p[TK_KP_MAX];
+    int t[TK_KP_MAX];
+    for (int j = 0; j < k; ++j) {
+      t[j] = key_tok(top[j]);
+      p[j] = __ddiv_rn(exp((double)key_logit(top[j]) - m), z);
+    }
+    for (int a = 1; a < k; ++a) {
+      const double pa = p[a];
+      const int ta = t[a];
+      int b = a - 1;
+      while (b >= 0 && (p[b] < pa || (p[b] == pa && t[b] > ta))) {
+        p[b + 1] = p[b];
+        t[b + 1] = t[b];
+        --b;
+      }
+      p[b + 1] = pa;
+      t[b + 1] = ta;
+    }
+    for (int j = 0; j < k; ++j) {
+      tok_out[row * k + j] = t[j];
+      prob_out[row * k + j] = p[j];
+    }
+  }
+}
+
+// Full fp64 rows (MarginalBlock export) with the same m and Z.
+__global__ void __launch_bounds__(TK_THREADS) k1_full_rows(const void* logits, int dtype, int vocab, int64_t stride,
+                                                           const double* stats, double* probs_full) {
+  const int row = blockIdx.y;
+  const double m = stats[row * 2], z = stats[row * 2 + 1];
+  for (int v = blockIdx.x * TK_THREADS + threadIdx.x; v < vocab; v += gridDim.x * TK_THREADS)
+    probs_full[(int64_t)row * vocab + v] =
+        __ddiv_rn(exp((double)load_logit(logits, dtype, (int64_t)row * stride + v) - m), z);
+}
+
+// Exact fallback: rows flagged by the boundary check redo the selection on the
+// fp64 probabilities of the whole row (single CTA per flagged row).
+__global__ void __launch_bounds__(TK_THREADS) k1_fast_fallback(const void* logits, int dtype, int vocab,
+                                                               int64_t stride, const double* stats, const int* fallback,
+                                                               int k, int32_t* tok_out, double* prob_out) {
+  const int row = blockIdx.x;
+  if (!fallback[row]) return;
+  const double m = stats[row * 2], z = stats[row * 2 + 1];
+  // running top-k over the row: per 4096-element block, merge the block's top-k with the current list
+  __shared__ double cur_p[TK_MAX_K];
+  __shared__ int cur_t[TK_MAX_K];
+  __shared__ double blk_p[TK_MAX_K];
+  __shared__ int32_t blk_t[TK_MAX_K];
+  if (threadIdx.x == 0)
+    for (int j = 0; j < k; ++j) { cur_p[j] = -1.0; cur_t[j] = 0x7fffffff; }
+  __syncthreads();
+  for (int b0 = 0; b0 < vocab; b0 += TK_CHUNK) {
+    double p[TK_PER_THREAD];
+    int t[TK_PER_THREAD];
+    for (int i = 0; i < TK_PER_THREAD; ++i) {
+      const int v = b0 + i * TK_THREADS + threadIdx.x;
+      if (v < vocab) {
+        p[i] = __ddiv_rn(exp((double)load_logit(logits, dtype, (int64_t)row * stride + v) - m), z);
+        t[i] = v;
+      } else {
+        p[i] = -1.0;
+        t[i] = -1;
+      }
+    }
+    block_extract(p, t, TK_PER_THREAD, min(k, vocab - b0), blk_p, blk_t);
+    if (threadIdx.x == 0) {
+      const int nb = min(k, vocab - b0);
+      double mp[2 * TK_MAX_K];
+      int mt[2 * TK_MAX_K];
+      int a = 0, b = 0, o = 0;
+      while (o < k && (a < k || b < nb)) {
+        const bool take_a = b >= nb || (a < k && better(cur_p[a], cur_t[a], blk_p[b], blk_t[b]));
+        mp[o] = take_a ? cur_p[a] : blk_p[b];
+        mt[o] = take_a ? cur_t[a] : blk_t[b];
+        if (take_a) ++a; else ++b;
+        ++o;
+      }
+      for (int j = 0; j < k; ++j) { cur_p[j] = mp[j]; cur_t[j] = mt[j]; }
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int j = 0; j < k; ++j) { tok_out[row * k + j] = cur_t[j]; prob_out[row * k + j] = cur_p[j]; }
+}
+
 static int run_topk(const void* logits, int dtype, const double* probs_in, int gamma, int vocab, int64_t stride,
                     int k, int32_t* tok, double* prob, double* probs_full, void* ws, size_t ws_bytes,
                     cudaStream_t st) {
@@ -240,6 +474,17 @@ static int run_topk(const void* logits, int dtype, const double* probs_in, int g
   TopkWs w = carve(ws, gamma, chunks, k, &need);
   BST_REQUIRE(ws != nullptr && ws_bytes >= need, "workspace too small: %zu < %zu", ws_bytes, need);
   dim3 grid(chunks, gamma);
+  const int kp = k + 1 <= vocab ? k + 1 : k;
+  if (probs_in == nullptr && kp < TK_KP_MAX && (int64_t)chunks * kp <= TK_CHUNK) {
+    k1_fast_chunk<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, kp, w.pmax, w.psum, w.ckeys);
+    k1_fast_finalize<<<gamma, TK_THREADS, 0, st>>>(w.pmax, w.psum, w.ckeys, chunks, kp, k, tok, prob, w.stats,
+                                                   w.fallback);
+    k1_fast_fallback<<<gamma, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.stats, w.fallback, k, tok, prob);
+    if (probs_full) k1_full_rows<<<dim3(chunks, gamma), TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.stats,
+                                                                            probs_full);
+    BST_LAUNCH_CHECK();
+    return BST_OK;
+  }
   if (probs_in == nullptr) {
     k1_chunk_max<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax);
     k1_chunk_sum<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax, w.psum);
