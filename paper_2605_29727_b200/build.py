@@ -19,7 +19,8 @@ BUILD = PKG / "_build"
 LIB = PKG / "libbastion.so"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-BASE = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}",
+TRACE = ["-DBST_TRACE"] if os.environ.get("BST_TRACE") == "1" else []  # phase tracing builds
+BASE = TRACE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}",
         "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-diag-suppress", "550,177"]
 # fp64 controller arithmetic must not be contracted into FMAs (bit parity with Python floats)
 PER_FILE = {"expand.cu": ["-fmad=false"]}

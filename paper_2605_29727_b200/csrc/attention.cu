@@ -362,11 +362,17 @@ __device__ __forceinline__ long long gtimer() {
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
   return t;
 }
+#ifdef BST_TRACE  // phase tracing (scripts/attn_trace.py); compiled out by default
 #define TRACE(i, k)                                                                                   \
   do {                                                                                                \
     if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 32)            \
       g_attn_trace[(i) * 8 + (k)] = gtimer();                                                         \
   } while (0)
+#else
+#define TRACE(i, k) \
+  do {              \
+  } while (0)
+#endif
 
 constexpr int T_THREADS = 192;
 constexpr int T_STAGES = 4;

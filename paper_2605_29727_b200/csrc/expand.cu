@@ -37,11 +37,15 @@ constexpr unsigned short NO_PARENT = 0xFFFF;
 
 __device__ long long* g_ex_trace = nullptr;
 __device__ __forceinline__ void ex_trace(int k) {
+#ifdef BST_TRACE  // phase tracing (scripts/expand_trace.py); compiled out by default
   if (g_ex_trace && threadIdx.x == 0 && k < 16) {
     long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     g_ex_trace[k] = t;
   }
+#else
+  (void)k;
+#endif
 }
 
 struct HeapEntry {

@@ -115,11 +115,15 @@ int cached_tmap(CUtensorMap* out, const void* ptr, uint64_t rows, uint64_t cols,
 __device__ long long* g_gemm_trace = nullptr;  // debug: globaltimer stamps of CTA g_trace_cta
 __device__ int g_trace_cta = 0;
 __device__ __forceinline__ void gtrace(int k) {
+#ifdef BST_TRACE  // phase tracing (scripts/gemm_trace.py); compiled out by default
   if (g_gemm_trace && blockIdx.x == g_trace_cta && k < 64) {
     long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     g_gemm_trace[k] = t;
   }
+#else
+  (void)k;
+#endif
 }
 
 struct Seg {
