@@ -377,12 +377,12 @@ __device__ __forceinline__ long long gtimer() {
 constexpr int T_THREADS = 192;
 constexpr int T_STAGES = 4;
 constexpr int T_Q_BYTES = 128 * A_D * 2;   // 32 KiB: two [128 rows][64] SW128 halves
-constexpr int T_P_BYTES = 128 * A_PAGE * 2; // 16 KiB: [128 rows][64 keys]
+constexpr int T_P_BYTES = 2 * 128 * A_PAGE * 2; // 2 x 16 KiB: double-buffered [128 rows][64 keys]
 constexpr float T_RESCALE = 8.f;            // log2 units
 
 __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done, q_ready;
+  __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
   sm100::grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -406,7 +406,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     for (int i = 0; i < T_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
     for (int i = 0; i < 2; ++i) { sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&s_free[i], 4); }
     sm100::mbar_init(&p_full, 4);
-    sm100::mbar_init(&o_done, 1);
+    sm100::mbar_init(&o_done[0], 1);
+    sm100::mbar_init(&o_done[1], 1);
     sm100::mbar_init(&q_ready, 4);
     sm100::fence_mbar_init();
   }
@@ -475,11 +476,11 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
           const uint32_t vb = sKV + stj * A_STAGE_BYTES + A_TILE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = sm100::desc_k_sw128(sP + kk * 32);
+            const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
             const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
             sm100::umma_f16(tmem + 128, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
           }
-          sm100::umma_commit(&o_done);
+          sm100::umma_commit(&o_done[j & 1]);
           sm100::umma_commit(&empty[stj]);
         }
         __syncwarp();
@@ -567,11 +568,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       }
       const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
       if (threadIdx.x == 64) TRACE(i, 4);
-      if (i >= 1) sm100::mbar_wait(&o_done, (i - 1) & 1);  // PV(i-1) done: O stable, P free
+      // P buffer i&1 was last read by PV(i-2); O only needs PV(i-1) when it is rescaled
+      const bool need_o = __any_sync(0xffffffffu, rescale && i >= 1);
+      if (need_o) sm100::mbar_wait(&o_done[(i - 1) & 1], ((i - 1) >> 1) & 1);
+      else if (i >= 2) sm100::mbar_wait(&o_done[i & 1], ((i - 2) >> 1) & 1);
       if (threadIdx.x == 64) TRACE(i, 5);
       sm100::tc_fence_after();
       // tcgen05.ld/st are warp-collective: rescale if any row of the warp needs it
-      if (__any_sync(0xffffffffu, rescale && i >= 1)) {
+      if (need_o) {
         const float f = (rescale && i >= 1) ? alpha : 1.f;
 #pragma unroll 1
         for (int cc = 0; cc < 8; ++cc) {
@@ -587,7 +591,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       m_run = m_ref;
 #pragma unroll
       for (int cq = 0; cq < 8; ++cq)
-        *reinterpret_cast<uint4*>(gP + row * 128 + ((cq ^ (row & 7)) << 4)) =
+        *reinterpret_cast<uint4*>(gP + (i & 1) * (128 * 128) + row * 128 + ((cq ^ (row & 7)) << 4)) =
             make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
       sm100::fence_async_shared();
       sm100::tc_fence_before();
@@ -598,7 +602,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     // ---------------- epilogue
     float o[128];
     if (n_tiles > 0) {
-      sm100::mbar_wait(&o_done, (n_tiles - 1) & 1);
+      sm100::mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       sm100::tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {

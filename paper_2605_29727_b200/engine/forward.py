@@ -62,7 +62,7 @@ def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
     best = 0
     for s in range(1, max_rows + 1):
         rb = math.ceil(g * s / 128)
-        splits = max(1, 148 // (cfg.n_kv * rb))
+        splits = max(1, 296 // (cfg.n_kv * rb))
         splits = min(splits, pages)
         pps = math.ceil(pages / splits)
         splits = math.ceil(pages / pps)
