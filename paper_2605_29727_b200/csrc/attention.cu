@@ -128,6 +128,8 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ex2(-inf) = +0
   return y;
 }
 
+__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
 __device__ __forceinline__ bool visible(const AttnArgs& a, int tok, int slot, const uint32_t* mrow) {
   if (slot >= a.n_keys) return false;
   if (a.mode == 2) return true;
@@ -658,7 +660,6 @@ constexpr int F_KV_BYTES = F_KT * A_D * 2;      // 32 KiB (K or V)
 constexpr int F_STAGE_BYTES = 2 * F_KV_BYTES;   // 64 KiB
 constexpr int F_P_BYTES = 128 * F_KT * 2;       // 32 KiB
 
-__device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
 
 __global__ void __launch_bounds__(F_THREADS, 1) attn_fa_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -931,6 +932,271 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_fa_kernel(const __grid_cons
   }
 }
 
+__global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full[2], o_done[2], q_ready;
+  __shared__ uint32_t tmem_sh;
+  __shared__ float xm[2][128], xl[2][128];
+  sm100::grid_dep_launch();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
+  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
+  const uint32_t sQ = base, sP = base + T_Q_BYTES, sKV = sP + T_P_BYTES;
+  uint8_t* gQ = smem;
+  uint8_t* gP = smem + T_Q_BYTES;
+  uint8_t* gKV = gP + T_P_BYTES;
+
+  const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
+  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
+  const int n_keys = c_ctx + a.keys_after_c;
+  const int R = a.group * a.s;
+  const int page0 = split * a.pages_per_split;
+  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
+  const int n_tiles = max(min(page0 + a.pages_per_split, n_pages_keys) - page0, 0);
+
+  if (threadIdx.x == 0) {
+    sm100::prefetch_tmap(&tmKV);
+    for (int i = 0; i < T_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) {
+      sm100::mbar_init(&s_full[i], 1);
+      sm100::mbar_init(&s_free[i], 4);
+      sm100::mbar_init(&p_full[i], 4);
+      sm100::mbar_init(&o_done[i], 1);
+    }
+    sm100::mbar_init(&q_ready, 8);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
+                     gridDim.x * gridDim.y * gridDim.z);
+      // PDL: pages entirely below c hold committed K/V the previous kernel does not
+      // touch; the page holding slot c onwards is written by qkv_rope right before us.
+      const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
+      bool waited = false;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i % T_STAGES;
+        if (i >= T_STAGES) sm100::mbar_wait(&empty[st], ((i / T_STAGES) & 1) ^ 1);
+        if (!waited && (i >= safe_tiles || i >= T_STAGES)) {
+          sm100::grid_dep_wait();
+          waited = true;
+        }
+        const int phys = a.page_table[page0 + i];
+        const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
+        const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
+        uint8_t* dst = gKV + st * A_STAGE_BYTES;
+        sm100::mbar_expect_tx(&full[st], A_STAGE_BYTES);
+        sm100::tma_load_2d(dst, &tmKV, &full[st], 0, (int)rowK);
+        sm100::tma_load_2d(dst + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowK);
+        sm100::tma_load_2d(dst + A_TILE_BYTES, &tmKV, &full[st], 0, (int)rowV);
+        sm100::tma_load_2d(dst + A_TILE_BYTES + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowV);
+        TRACE(i, 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = sm100::idesc_bf16(128, A_PAGE);
+    const uint32_t idO = sm100::idesc_bf16_bmn(128, A_D);
+    sm100::mbar_wait(&q_ready, 0);
+    for (int i = 0; i <= n_tiles; ++i) {
+      if (i < n_tiles) {
+        const int st = i % T_STAGES, b = i & 1;
+        sm100::mbar_wait(&full[st], (i / T_STAGES) & 1);
+        if (lane == 0) TRACE(i, 1);
+        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t kb = sKV + st * A_STAGE_BYTES;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint64_t ad = sm100::desc_k_sw128(sQ + (j >> 2) * (128 * 128) + (j & 3) * 32);
+            const uint64_t bd = sm100::desc_k_sw128(kb + (j >> 2) * (A_PAGE * 128) + (j & 3) * 32);
+            sm100::umma_f16(tmem + b * A_PAGE, ad, bd, idS, j > 0 ? 1u : 0u);
+          }
+          sm100::umma_commit(&s_full[b]);
+        }
+        __syncwarp();
+      }
+      if (i >= 1) {
+        const int j = i - 1, stj = j % T_STAGES;
+        sm100::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+        if (lane == 0) TRACE(j, 2);
+        sm100::tc_fence_after();
+        if (sm100::elect_one()) {
+          const uint32_t vb = sKV + stj * A_STAGE_BYTES + A_TILE_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
+            const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
+            sm100::umma_f16(tmem + 128 + (j & 1) * A_D, ad, bd, idO, (j > 1 || kk > 0) ? 1u : 0u);
+          }
+          sm100::umma_commit(&o_done[j & 1]);
+          sm100::umma_commit(&empty[stj]);
+        }
+        __syncwarp();
+      }
+    }
+  } else {
+    // ---------------- two groups x one thread per query row; group g takes tiles g, g+2, ...
+    const int g = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const int rg = rb * 128 + row;
+    const bool valid = rg < R;
+    const int rr = valid ? rg : 0;
+    const int tok = rr / a.group;
+    const int qh = head * a.group + rr % a.group;
+    const uint32_t* mrow = a.mode == 0 ? a.anc + (int64_t)tok * a.mask_words : nullptr;
+    const int mode = a.mode, mwords = a.mask_words;
+    const float scale = a.scale_log2;
+    sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
+    {  // each group stages one 64-dim half of the row
+      const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
+        *reinterpret_cast<int4*>(gQ + g * (128 * 128) + row * 128 + ((q ^ (row & 7)) << 4)) = v;
+      }
+    }
+    sm100::fence_async_shared();
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&q_ready);
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const uint32_t o_col = 128 + g * A_D;
+    float m_run = -INFINITY, l_run = 0.f;
+    int u = 0;
+    for (int i = g; i < n_tiles; i += 2, ++u) {
+      sm100::mbar_wait(&s_full[g], u & 1);
+      sm100::tc_fence_after();
+      float sv[64];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        float t16[16];
+        sm100::tmem_ld16(lane_base + g * A_PAGE + 16 * k, t16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) sv[16 * k + e] = t16[e];
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&s_free[g]);
+      const int slot0 = (page0 + i) * A_PAGE;
+      const uint64_t vis = valid ? row_vis64(mode, c_ctx, n_keys, tok, slot0, mrow, mwords) : 0ull;
+      float mx8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+      if (__all_sync(0xffffffffu, vis == ~0ull)) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          sv[k] *= scale;
+          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) {
+          const float v = ((vis >> k) & 1ull) ? sv[k] * scale : -INFINITY;
+          sv[k] = v;
+          mx8[k & 7] = fmaxf(mx8[k & 7], v);
+        }
+      }
+      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float m_new = fmaxf(m_run, mt);
+      const bool rescale = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + T_RESCALE);
+      const float m_ref = rescale ? m_new : m_run;
+      const float alpha = (rescale && m_run != -INFINITY) ? ex2(m_run - m_ref) : (rescale ? 0.f : 1.f);
+      const float msub = m_ref == -INFINITY ? 0.f : m_ref;
+      float rs8[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) rs8[k] = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int k = 0; k < 64; k += 2) {
+        const float p0 = ex2(sv[k] - msub);
+        const float p1 = ex2(sv[k + 1] - msub);
+        rs8[(k >> 1) & 7] += p0 + p1;
+        pk[k >> 1] = pack_bf16(p0, p1);
+      }
+      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      // this group's previous PV (tile i-2) must be done before P/O are touched
+      if (u >= 1) sm100::mbar_wait(&o_done[g], (u - 1) & 1);
+      sm100::tc_fence_after();
+      if (__any_sync(0xffffffffu, rescale && u >= 1)) {
+        const float f = (rescale && u >= 1) ? alpha : 1.f;
+#pragma unroll 1
+        for (int cc = 0; cc < 8; ++cc) {
+          float ov[16];
+          sm100::tmem_ld16(lane_base + o_col + 16 * cc, ov);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) ov[e] *= f;
+          sm100::tmem_st16(lane_base + o_col + 16 * cc, ov);
+        }
+        sm100::tmem_st_wait();
+      }
+      l_run = rescale ? l_run * alpha + rs : l_run + rs;
+      m_run = m_ref;
+#pragma unroll
+      for (int cq = 0; cq < 8; ++cq)
+        *reinterpret_cast<uint4*>(gP + g * (128 * 128) + row * 128 + ((cq ^ (row & 7)) << 4)) =
+            make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
+      sm100::fence_async_shared();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&p_full[g]);
+    }
+    // ---------------- merge the two groups; thread (g, row) writes dims [64 g, 64 g + 64)
+    if (u >= 1) sm100::mbar_wait(&o_done[g], (u - 1) & 1);
+    xm[g][row] = m_run;
+    xl[g][row] = l_run;
+    sm100::tc_fence_before();
+    named_bar_sync(1, 256);
+    sm100::tc_fence_after();
+    const float mA = xm[0][row], mB = xm[1][row];
+    const float M = fmaxf(mA, mB);
+    const float wA = (mA == -INFINITY) ? 0.f : ex2(mA - M), wB = (mB == -INFINITY) ? 0.f : ex2(mB - M);
+    const float L = wA * xl[0][row] + wB * xl[1][row];
+    const bool hasA = n_tiles >= 1, hasB = n_tiles >= 2;
+    float o[64];
+#pragma unroll
+    for (int cc = 0; cc < 4; ++cc) {
+      float ta[16], tb[16];
+      if (hasA) sm100::tmem_ld16(lane_base + 128 + 64 * g + 16 * cc, ta);
+      if (hasB) sm100::tmem_ld16(lane_base + 128 + A_D + 64 * g + 16 * cc, tb);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
+    }
+    if (valid) {
+      if (a.n_splits == 1) {
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                             pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+      } else {
+        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D + 64 * g);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        if (g == 0) {
+          a.ws_ml[r * 2 + 0] = M;
+          a.ws_ml[r * 2 + 1] = L;
+        }
+      }
+    }
+  }
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 512);
+  }
+}
+
 // merge flash-decoding splits: one warp per (token, q-head) row, single pass
 // with online rescaling, 4 splits in flight per iteration
 __global__ void attn_combine_kernel(AttnArgs a) {
@@ -1050,7 +1316,7 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
     // default: tcgen05 64-key kernel (attn_tc_kernel).  BST_ATTN=mma selects the
     // mma.sync kernel, BST_ATTN=fa the 128-key two-warpgroup kernel (experimental:
     // fails the engine's greedy-preservation test, under investigation).
-    variant = (e && e[0] == 'm') ? 1 : ((e && e[0] == 'f') ? 0 : 2);
+    variant = (e && e[0] == 'm') ? 1 : ((e && e[0] == 'f') ? 0 : ((e && e[0] == 't' && e[2] == '1') ? 2 : 3));
   }
   static bool attr = false;
   const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
@@ -1060,25 +1326,31 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
     BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mma));
     BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     BST_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fa));
+    BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     attr = true;
   }
-  if (variant == 1)
+  // default: single-group kernel for short per-CTA page runs, two alternating
+  // softmax groups once a CTA walks >= 8 tiles (long context)
+  const int v = variant == 3 ? (pps >= 8 ? 3 : 2) : variant;
+  if (v == 1)
     attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
   else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_kv, n_splits, row_blocks);
-    cfg.blockDim = dim3(variant == 0 ? F_THREADS : T_THREADS);
-    cfg.dynamicSmemBytes = variant == 0 ? smem_fa : smem_tc;
+    cfg.blockDim = dim3(v == 2 ? T_THREADS : F_THREADS);
+    cfg.dynamicSmemBytes = v == 0 ? smem_fa : smem_tc;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (variant == 0)
+    if (v == 0)
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_fa_kernel, tm, a));
-    else
+    else if (v == 2)
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, a));
+    else
+      BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc2_kernel, tm, a));
   }
   if (n_splits > 1) {
     const int rows_total = s * n_q;
