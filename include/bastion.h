@@ -187,6 +187,9 @@ int bst_set_prefetch(const bst_prefetch_t* pf); /* applies to the next K3/K5 lau
  * (mask semantics of linearize, verify_sim.py:336-355; cost PAPER.md:1056-1062).
  * mode 0 TREE (prefix + ancestor bitmask), 1 CAUSAL (chunked prefill),
  * 2 FULL (drafter block).  c = state[c_idx] when state is non-null.
+ * ws (n_splits > 1): the first 4 KiB hold split-arrival counters and must be
+ * zero before the first call (each call leaves them zero); the rest holds the
+ * per-split partial rows.  One ws per concurrently running call.
  * ---------------------------------------------------------------------- */
 int bst_attention(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
                   int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,

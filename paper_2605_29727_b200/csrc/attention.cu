@@ -31,6 +31,7 @@ constexpr int A_STAGES = 3;
 constexpr int A_TILE_BYTES = A_PAGE * A_D * 2;      // 16 KiB per K or V tile
 constexpr int A_STAGE_BYTES = 2 * A_TILE_BYTES;      // K + V
 constexpr int A_ROWS_PER_CTA = A_WARPS * 16;
+constexpr size_t A_WS_CNT_BYTES = 4096;  // workspace head: split-arrival counters (zero-initialised once)
 
 struct AttnArgs {
   const __nv_bfloat16* q;  // [s][n_q][128]
@@ -54,6 +55,8 @@ struct AttnArgs {
   float scale_log2;        // softmax scale * log2(e)
   float* ws_o;             // [split][s*n_q][128] unnormalised partial O
   float* ws_ml;            // [split][s*n_q][2] (running max (log2 domain), sum)
+  unsigned long long* cnt; // [row_blocks][n_kv] split barrier words (generation | arrivals)
+  int merge;               // 1: splits merged in-kernel (one-wave grid), 0: attn_combine_kernel
   bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
 };
 
@@ -128,7 +131,181 @@ __device__ __forceinline__ float ex2(float x) {  // MUFU.EX2, ex2(-inf) = +0
   return y;
 }
 
+// 2^x on the FMA pipe (x <= 0; -inf -> 0): round-to-nearest split by the 1.5 * 2^23
+// trick, degree-3 fit of 2^f on [-1/2, 1/2] (max rel. error 7.6e-5, far below the bf16
+// rounding P goes through), exponent added as integer bits.  Takes part of the
+// softmax's exponentials off the MUFU pipe.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -126.f);
+  const float t = x + 12582912.f;
+  const float f = x - (t - 12582912.f);
+  float p = fmaf(f, 0.05517030f, 0.24260803f);
+  p = fmaf(f, p, 0.69326091f);
+  p = fmaf(f, p, 0.99992830f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 __device__ __forceinline__ void named_bar_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n)); }
+
+__device__ long long* g_attn_trace = nullptr;  // debug: [32 tiles][8] globaltimer stamps of CTA (0,0,0)
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ int g_attn_trace_y = 0;               // debug: which split's CTA (0, y, 0) is traced
+#ifdef BST_TRACE  // phase tracing (scripts/attn_trace.py); compiled out by default
+#define TRACE(i, k)                                                                                   \
+  do {                                                                                                \
+    if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == g_attn_trace_y && blockIdx.z == 0 && (i) < 32) \
+      g_attn_trace[(i) * 8 + (k)] = gtimer();                                                         \
+  } while (0)
+#define TRACE_MAX(k)                                                                                  \
+  do {                                                                                                \
+    if (g_attn_trace) atomicMax(reinterpret_cast<unsigned long long*>(g_attn_trace) + 29 * 8 + (k),   \
+                                (unsigned long long)gtimer());                                        \
+  } while (0)
+#else
+#define TRACE(i, k) \
+  do {              \
+  } while (0)
+#define TRACE_MAX(k) \
+  do {               \
+  } while (0)
+#endif
+
+__device__ __forceinline__ unsigned long long ld_acquire_gpu64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long atom_add_acq_rel_gpu(unsigned long long* p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.acq_rel.gpu.global.add.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release_gpu(unsigned long long* p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ long long gtimer_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// In-kernel flash-decoding merge (a.merge == 1).  The NT epilogue threads of a CTA
+// have staged its unnormalised partial O in shared memory, `stg` = [128 rows][128]
+// fp32 with 16-byte chunks swizzled by row % 8, and written (m, l) to ws_ml.
+// 1. warp-per-row coalesced copy of the partial rows to ws_o (L2-resident);
+// 2. arrive on the (head, row-block) counter and wait until every split has arrived:
+//    the grid is one wave (host checks grid <= #SMs at one CTA per SM) and every CTA
+//    has started before a dependent kernel can launch (griddepcontrol at entry), so
+//    all splits are co-resident;
+// 3. merge rows [split * per, split * per + per) of the row block across splits
+//    (fixed split order: deterministic) and store bf16;
+// 4. second arrival; the last one resets the counter to zero for the next launch.
+template <int NT>
+__device__ void split_merge(const AttnArgs& a, const float* stg, int head, int split, int rb, int t) {
+  constexpr int NW = NT / 32;
+  const int warp = t >> 5, lane = t & 31;
+  const int R = a.group * a.s;
+  const int Rb = min(128, R - rb * 128);
+  const int64_t rows_all = (int64_t)a.s * a.n_q;
+  for (int r = warp; r < Rb; r += NW) {
+    const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+    const int64_t gr = split * rows_all + (int64_t)tok * a.n_q + qh;
+    const float4 v = *reinterpret_cast<const float4*>(stg + r * A_D + ((lane ^ (r & 7)) << 2));
+    __stcg(reinterpret_cast<float4*>(a.ws_o + gr * A_D) + lane, v);
+  }
+  // generation barrier over the splits of this (head, row block): the counter word is
+  // (generation << 32 | arrivals); the last arrival clears the arrivals and bumps the
+  // generation in one release RMW, the others spin (acquire) until the generation moves.
+  named_bar_sync(1, NT);
+  unsigned long long* cnt = a.cnt + rb * a.n_kv + head;
+  if (t == 0) {
+    const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
+    TRACE_MAX(3);
+    if ((unsigned)(old & 0xffffffffu) == (unsigned)a.n_splits - 1u) {
+      red_add_release_gpu(cnt, (1ull << 32) - (unsigned long long)a.n_splits);
+    } else {
+      const unsigned gen = (unsigned)(old >> 32);
+      const long long t0 = gtimer_ns();
+      while ((unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen) {
+        if (gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived: fail, do not hang
+      }
+    }
+  }
+  if (t == 0) TRACE_MAX(4);
+  named_bar_sync(1, NT);
+  // thread item = (row, DI-dim slice); the loads of up to 20 splits are issued at once
+  // (DI = 8 for the 192-thread kernel, 4 for the 384-thread one: register budget)
+  constexpr int MS = 20, DI = NT == 128 ? 8 : 4, IPR = A_D / DI;
+  const int per = (Rb + a.n_splits - 1) / a.n_splits;
+  const int r0 = split * per, r1 = min(r0 + per, Rb);
+  for (int it = t; it < (r1 - r0) * IPR; it += NT) {
+    const int r = r0 + it / IPR, d0 = (it % IPR) * DI;
+    const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+    const int64_t base = (int64_t)tok * a.n_q + qh;
+    float M = -INFINITY, L = 0.f, acc[DI];
+#pragma unroll
+    for (int e = 0; e < DI; ++e) acc[e] = 0.f;
+    for (int j0 = 0; j0 < a.n_splits; j0 += MS) {
+      float2 ml[MS];
+      float4 va[MS][DI / 4];
+#pragma unroll
+      for (int u = 0; u < MS; ++u) {
+        if (j0 + u < a.n_splits) {
+          const int64_t gr = (j0 + u) * rows_all + base;
+          ml[u] = __ldcg(reinterpret_cast<const float2*>(a.ws_ml + gr * 2));
+#pragma unroll
+          for (int h = 0; h < DI / 4; ++h) va[u][h] = __ldcg(reinterpret_cast<const float4*>(a.ws_o + gr * A_D + d0) + h);
+        } else {
+          ml[u] = make_float2(-INFINITY, 0.f);
+#pragma unroll
+          for (int h = 0; h < DI / 4; ++h) va[u][h] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float Mn = M;
+#pragma unroll
+      for (int u = 0; u < MS; ++u) Mn = fmaxf(Mn, ml[u].x);
+      if (Mn == -INFINITY) continue;
+      const float sc = M == -INFINITY ? 0.f : ex2(M - Mn);
+      L *= sc;
+#pragma unroll
+      for (int e = 0; e < DI; ++e) acc[e] *= sc;
+#pragma unroll
+      for (int u = 0; u < MS; ++u) {
+        const float w = ml[u].x == -INFINITY ? 0.f : ex2(ml[u].x - Mn);
+        L += w * ml[u].y;
+#pragma unroll
+        for (int h = 0; h < DI / 4; ++h) {
+          acc[4 * h + 0] += w * va[u][h].x;
+          acc[4 * h + 1] += w * va[u][h].y;
+          acc[4 * h + 2] += w * va[u][h].z;
+          acc[4 * h + 3] += w * va[u][h].w;
+        }
+      }
+      M = Mn;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    __nv_bfloat16* op = a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + d0;
+    if constexpr (DI == 8) {
+      *reinterpret_cast<uint4*>(op) = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                                                 pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+    } else {
+      *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+    }
+  }
+}
+
+// Pages [page0, page0 + n_tiles) of this split: the live pages (those holding keys
+// < n_keys, read from device state at run time) are balanced over the splits, so a
+// graph captured for the capacity still gives every split the same share.
+__device__ __forceinline__ void split_pages(const AttnArgs& a, int n_keys, int split, int& page0, int& n_tiles) {
+  const int live = (n_keys + A_PAGE - 1) / A_PAGE;
+  page0 = split * live / a.n_splits;
+  n_tiles = (split + 1) * live / a.n_splits - page0;
+}
 
 __device__ __forceinline__ bool visible(const AttnArgs& a, int tok, int slot, const uint32_t* mrow) {
   if (slot >= a.n_keys) return false;
@@ -358,24 +535,6 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 // P -> smem (K-major, 128B swizzle), epilogue.  TMEM: S double buffer (2 x 64
 // columns) + O (128 columns).  V is consumed as an MN-major UMMA operand.
 // ===========================================================================
-__device__ long long* g_attn_trace = nullptr;  // debug: [32 tiles][8] globaltimer stamps of CTA (0,0,0)
-__device__ __forceinline__ long long gtimer() {
-  long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-#ifdef BST_TRACE  // phase tracing (scripts/attn_trace.py); compiled out by default
-#define TRACE(i, k)                                                                                   \
-  do {                                                                                                \
-    if (g_attn_trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && (i) < 32)            \
-      g_attn_trace[(i) * 8 + (k)] = gtimer();                                                         \
-  } while (0)
-#else
-#define TRACE(i, k) \
-  do {              \
-  } while (0)
-#endif
-
 constexpr int T_THREADS = 192;
 constexpr int T_STAGES = 4;
 constexpr int T_Q_BYTES = 128 * A_D * 2;   // 32 KiB: two [128 rows][64] SW128 halves
@@ -387,6 +546,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) TRACE(31, 0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
@@ -399,9 +559,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
   const int R = a.group * a.s;
-  const int page0 = split * a.pages_per_split;
-  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
-  const int n_tiles = max(min(page0 + a.pages_per_split, n_pages_keys) - page0, 0);
+  int page0, n_tiles;
+  split_pages(a, n_keys, split, page0, n_tiles);
 
   if (threadIdx.x == 0) {
     sm100::prefetch_tmap(&tmKV);
@@ -418,6 +577,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   __syncthreads();
   sm100::tc_fence_after();
   const uint32_t tmem = tmem_sh;
+  if (threadIdx.x == 0) TRACE(31, 1);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -501,6 +661,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     const int mode = a.mode, mwords = a.mask_words;
     const float scale = a.scale_log2;
     sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
+    if (threadIdx.x == 64) TRACE(31, 2);
+    if (threadIdx.x == 64) TRACE_MAX(0);
     {  // stage Q row (256 B) into the swizzled K-major tile
       const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D);
 #pragma unroll
@@ -512,6 +674,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     sm100::fence_async_shared();
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&q_ready);
+    if (threadIdx.x == 64) TRACE(31, 3);
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     float m_run = -INFINITY, l_run = 0.f;
     for (int i = 0; i < n_tiles; ++i) {
@@ -605,6 +768,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     float o[128];
     if (n_tiles > 0) {
       sm100::mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
+      if (threadIdx.x == 64) TRACE(31, 4);
       sm100::tc_fence_after();
 #pragma unroll
       for (int cc = 0; cc < 8; ++cc) {
@@ -617,7 +781,21 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 #pragma unroll
       for (int e = 0; e < 128; ++e) o[e] = 0.f;
     }
-    if (valid) {
+    if (a.n_splits > 1 && a.merge) {
+      float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        *reinterpret_cast<float4*>(stg + row * A_D + ((q ^ (row & 7)) << 2)) =
+            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      if (valid) {
+        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        *reinterpret_cast<float2*>(a.ws_ml + r * 2) = make_float2(m_run, l_run);
+      }
+      named_bar_sync(1, 128);
+      if (threadIdx.x == 64) TRACE(31, 5);
+      if (threadIdx.x == 64) TRACE_MAX(1);
+      split_merge<128>(a, stg, head, split, rb, threadIdx.x - 64);
+    } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
         uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D);
@@ -634,6 +812,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
         a.ws_ml[r * 2 + 1] = l_run;
       }
     }
+    if (threadIdx.x == 64) TRACE(31, 6);
+    if (threadIdx.x == 64) TRACE_MAX(2);
   }
   sm100::tc_fence_before();
   __syncthreads();
@@ -932,31 +1112,41 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_fa_kernel(const __grid_cons
   }
 }
 
-__global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
+// K and V pages stream through separate rings: a K stage is released when its S
+// MMA completes, a V stage when its PV MMA completes, so K runs further ahead of
+// the softmax than a joint K+V ring of the same size allows.
+constexpr int T2_KS = 5, T2_VS = 4;
+constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
+constexpr int T2_THREADS = F_THREADS + 64;  // + warp 10: V producer, warp 11: PV issuer
+
+__global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full[2], o_done[2], q_ready;
+  __shared__ __align__(8) uint64_t fullK[T2_KS], emptyK[T2_KS], fullV[T2_VS], emptyV[T2_VS], s_full[2], s_free[2],
+      p_full[2], o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
   __shared__ float xm[2][128], xl[2][128];
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) TRACE(31, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-  const uint32_t sQ = base, sP = base + T_Q_BYTES, sKV = sP + T_P_BYTES;
+  const uint32_t sQ = base, sP = base + T_Q_BYTES, sK = sP + T_P_BYTES, sV = sK + T2_KS * A_TILE_BYTES;
+  const uint32_t sOnes = sV + T2_VS * A_TILE_BYTES;  // [16][64] bf16 ones: B operand of the row-sum MMA
   uint8_t* gQ = smem;
   uint8_t* gP = smem + T_Q_BYTES;
-  uint8_t* gKV = gP + T_P_BYTES;
+  uint8_t* gKV = gP + T_P_BYTES;  // K ring, then V ring; reused as the merge staging buffer
 
   const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
   const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
   const int R = a.group * a.s;
-  const int page0 = split * a.pages_per_split;
-  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
-  const int n_tiles = max(min(page0 + a.pages_per_split, n_pages_keys) - page0, 0);
+  int page0, n_tiles;
+  split_pages(a, n_keys, split, page0, n_tiles);
 
   if (threadIdx.x == 0) {
     sm100::prefetch_tmap(&tmKV);
-    for (int i = 0; i < T_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < T2_KS; ++i) { sm100::mbar_init(&fullK[i], 1); sm100::mbar_init(&emptyK[i], 1); }
+    for (int i = 0; i < T2_VS; ++i) { sm100::mbar_init(&fullV[i], 1); sm100::mbar_init(&emptyV[i], 1); }
     for (int i = 0; i < 2; ++i) {
       sm100::mbar_init(&s_full[i], 1);
       sm100::mbar_init(&s_free[i], 4);
@@ -972,74 +1162,88 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
   sm100::tc_fence_after();
   const uint32_t tmem = tmem_sh;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 10) {
     if (lane == 0) {
-      issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
-                     gridDim.x * gridDim.y * gridDim.z);
+      const bool isK = warp == 0;
+      if (isK)
+        issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
+                       gridDim.x * gridDim.y * gridDim.z);
+      const int ns = isK ? T2_KS : T2_VS;
+      uint64_t* fb = isK ? fullK : fullV;
+      uint64_t* eb = isK ? emptyK : emptyV;
+      uint8_t* ring = isK ? gKV : gKV + T2_KS * A_TILE_BYTES;
       // PDL: pages entirely below c hold committed K/V the previous kernel does not
       // touch; the page holding slot c onwards is written by qkv_rope right before us.
       const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
       bool waited = false;
       for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % T_STAGES;
-        if (i >= T_STAGES) sm100::mbar_wait(&empty[st], ((i / T_STAGES) & 1) ^ 1);
-        if (!waited && (i >= safe_tiles || i >= T_STAGES)) {
+        const int st = i % ns;
+        if (i >= ns) sm100::mbar_wait(&eb[st], ((i / ns) & 1) ^ 1);
+        if (!waited && (i >= safe_tiles || i >= ns)) {
           sm100::grid_dep_wait();
           waited = true;
         }
         const int phys = a.page_table[page0 + i];
-        const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
-        const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
-        uint8_t* dst = gKV + st * A_STAGE_BYTES;
-        sm100::mbar_expect_tx(&full[st], A_STAGE_BYTES);
-        sm100::tma_load_2d(dst, &tmKV, &full[st], 0, (int)rowK);
-        sm100::tma_load_2d(dst + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowK);
-        sm100::tma_load_2d(dst + A_TILE_BYTES, &tmKV, &full[st], 0, (int)rowV);
-        sm100::tma_load_2d(dst + A_TILE_BYTES + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowV);
-        TRACE(i, 0);
+        const int64_t row = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + (isK ? 0 : 1)) * a.n_kv + head) * A_PAGE;
+        uint8_t* dst = ring + st * A_TILE_BYTES;
+        sm100::mbar_expect_tx(&fb[st], A_TILE_BYTES);
+        sm100::tma_load_2d(dst, &tmKV, &fb[st], 0, (int)row);
+        sm100::tma_load_2d(dst + A_PAGE * 128, &tmKV, &fb[st], 64, (int)row);
+        if (isK) TRACE(i, 0);
       }
     }
   } else if (warp == 1) {
     const uint32_t idS = sm100::idesc_bf16(128, A_PAGE);
-    const uint32_t idO = sm100::idesc_bf16_bmn(128, A_D);
     sm100::mbar_wait(&q_ready, 0);
-    for (int i = 0; i <= n_tiles; ++i) {
-      if (i < n_tiles) {
-        const int st = i % T_STAGES, b = i & 1;
-        sm100::mbar_wait(&full[st], (i / T_STAGES) & 1);
-        if (lane == 0) TRACE(i, 1);
-        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          const uint32_t kb = sKV + st * A_STAGE_BYTES;
+    // S issuer: S(i) (group i & 1) as soon as K(i) has landed and the group has read
+    // S(i - 2) out of TMEM.  PV runs on its own issuing warp (warp 11), so neither kind
+    // of MMA waits behind the other and the two softmax groups stay decoupled.
+    for (int i = 0; i < n_tiles; ++i) {
+      const int st = i % T2_KS, b = i & 1;
+      sm100::mbar_wait(&fullK[st], (i / T2_KS) & 1);
+      if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
+      if (lane == 0) TRACE(i, 1);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t kb = sK + st * A_TILE_BYTES;
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint64_t ad = sm100::desc_k_sw128(sQ + (j >> 2) * (128 * 128) + (j & 3) * 32);
-            const uint64_t bd = sm100::desc_k_sw128(kb + (j >> 2) * (A_PAGE * 128) + (j & 3) * 32);
-            sm100::umma_f16(tmem + b * A_PAGE, ad, bd, idS, j > 0 ? 1u : 0u);
-          }
-          sm100::umma_commit(&s_full[b]);
+        for (int j = 0; j < 8; ++j) {
+          const uint64_t ad = sm100::desc_k_sw128(sQ + (j >> 2) * (128 * 128) + (j & 3) * 32);
+          const uint64_t bd = sm100::desc_k_sw128(kb + (j >> 2) * (A_PAGE * 128) + (j & 3) * 32);
+          sm100::umma_f16(tmem + b * A_PAGE, ad, bd, idS, j > 0 ? 1u : 0u);
         }
-        __syncwarp();
+        sm100::umma_commit(&s_full[b]);
+        sm100::umma_commit(&emptyK[st]);
       }
-      if (i >= 1) {
-        const int j = i - 1, stj = j % T_STAGES;
-        sm100::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
-        if (lane == 0) TRACE(j, 2);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          const uint32_t vb = sKV + stj * A_STAGE_BYTES + A_TILE_BYTES;
+      __syncwarp();
+    }
+  } else if (warp == 11) {
+    const uint32_t idO = sm100::idesc_bf16_bmn(128, A_D);
+    const uint32_t idL = sm100::idesc_bf16(128, 16);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int stj = j % T2_VS;
+      sm100::mbar_wait(&p_full[j & 1], (j >> 1) & 1);
+      sm100::mbar_wait(&fullV[stj], (j / T2_VS) & 1);
+      if (lane == 0) TRACE(j, 2);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t vb = sV + stj * A_TILE_BYTES;
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
-            const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
-            sm100::umma_f16(tmem + 128 + (j & 1) * A_D, ad, bd, idO, (j > 1 || kk > 0) ? 1u : 0u);
-          }
-          sm100::umma_commit(&o_done[j & 1]);
-          sm100::umma_commit(&empty[stj]);
+        for (int kk = 0; kk < 4; ++kk) {
+          const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
+          const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
+          sm100::umma_f16(tmem + 128 + (j & 1) * A_D, ad, bd, idO, (j > 1 || kk > 0) ? 1u : 0u);
         }
-        __syncwarp();
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // row sums of P: l += P x ones (the same bf16 P as the numerator)
+          const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
+          const uint64_t bd = sm100::desc_k_sw128(sOnes + kk * 32);
+          sm100::umma_f16(tmem + T2_LCOL + (j & 1) * 16, ad, bd, idL, (j > 1 || kk > 0) ? 1u : 0u);
+        }
+        sm100::umma_commit(&o_done[j & 1]);
+        sm100::umma_commit(&emptyV[stj]);
       }
+      __syncwarp();
     }
   } else {
     // ---------------- two groups x one thread per query row; group g takes tiles g, g+2, ...
@@ -1055,6 +1259,8 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
     const int mode = a.mode, mwords = a.mask_words;
     const float scale = a.scale_log2;
     sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
+    if (threadIdx.x == 64) TRACE(31, 2);
+    if (threadIdx.x == 64) TRACE_MAX(0);
     {  // each group stages one 64-dim half of the row
       const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
 #pragma unroll
@@ -1063,15 +1269,19 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
         *reinterpret_cast<int4*>(gQ + g * (128 * 128) + row * 128 + ((q ^ (row & 7)) << 4)) = v;
       }
     }
+    *reinterpret_cast<uint2*>(gKV + (T2_KS + T2_VS) * A_TILE_BYTES + (threadIdx.x - 64) * 8) =
+        make_uint2(0x3F803F80u, 0x3F803F80u);  // bf16 1.0 x 4
     sm100::fence_async_shared();
     __syncwarp();
     if (lane == 0) sm100::mbar_arrive(&q_ready);
+    if (threadIdx.x == 64) TRACE(31, 3);
     const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
     const uint32_t o_col = 128 + g * A_D;
-    float m_run = -INFINITY, l_run = 0.f;
+    float m_run = -INFINITY;
     int u = 0;
     for (int i = g; i < n_tiles; i += 2, ++u) {
       sm100::mbar_wait(&s_full[g], u & 1);
+      if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 3);
       sm100::tc_fence_after();
       float sv[64];
 #pragma unroll
@@ -1084,46 +1294,39 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&s_free[g]);
+      if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 7);
       const int slot0 = (page0 + i) * A_PAGE;
       const uint64_t vis = valid ? row_vis64(mode, c_ctx, n_keys, tok, slot0, mrow, mwords) : 0ull;
+      // max over the raw scores (scale > 0 commutes with max); masked keys -> -inf
+      if (!__all_sync(0xffffffffu, vis == ~0ull)) {
+#pragma unroll
+        for (int k = 0; k < 64; ++k) sv[k] = ((vis >> k) & 1ull) ? sv[k] : -INFINITY;
+      }
       float mx8[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
-      if (__all_sync(0xffffffffu, vis == ~0ull)) {
+      for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(fmaxf(sv[k], sv[k + 8]), fmaxf(sv[k + 16], sv[k + 24]));
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          sv[k] *= scale;
-          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const float v = ((vis >> k) & 1ull) ? sv[k] * scale : -INFINITY;
-          sv[k] = v;
-          mx8[k & 7] = fmaxf(mx8[k & 7], v);
-        }
-      }
-      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      for (int k = 0; k < 8; ++k) mx8[k] = fmaxf(mx8[k], fmaxf(fmaxf(sv[k + 32], sv[k + 40]), fmaxf(sv[k + 48], sv[k + 56])));
+      const float mt = scale * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_new = fmaxf(m_run, mt);
       const bool rescale = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + T_RESCALE);
       const float m_ref = rescale ? m_new : m_run;
       const float alpha = (rescale && m_run != -INFINITY) ? ex2(m_run - m_ref) : (rescale ? 0.f : 1.f);
-      const float msub = m_ref == -INFINITY ? 0.f : m_ref;
-      float rs8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) rs8[k] = 0.f;
+      const float nsub = m_ref == -INFINITY ? 0.f : -m_ref;
       uint32_t pk[32];
 #pragma unroll
       for (int k = 0; k < 64; k += 2) {
-        const float p0 = ex2(sv[k] - msub);
-        const float p1 = ex2(sv[k + 1] - msub);
-        rs8[(k >> 1) & 7] += p0 + p1;
+        const float x0 = fmaf(sv[k], scale, nsub), x1 = fmaf(sv[k + 1], scale, nsub);
+        // every fourth exponential on the FMA pipe, the rest on MUFU
+        const float p0 = ex2(x0);
+        const float p1 = (k & 2) ? ex2_poly(x1) : ex2(x1);
         pk[k >> 1] = pack_bf16(p0, p1);
       }
-      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
+      if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 4);
       // this group's previous PV (tile i-2) must be done before P/O are touched
       if (u >= 1) sm100::mbar_wait(&o_done[g], (u - 1) & 1);
+      if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 5);
       sm100::tc_fence_after();
       if (__any_sync(0xffffffffu, rescale && u >= 1)) {
         const float f = (rescale && u >= 1) ? alpha : 1.f;
@@ -1135,9 +1338,13 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
           for (int e = 0; e < 16; ++e) ov[e] *= f;
           sm100::tmem_st16(lane_base + o_col + 16 * cc, ov);
         }
+        float lv[16];
+        sm100::tmem_ld16(lane_base + T2_LCOL + 16 * g, lv);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) lv[e] *= f;
+        sm100::tmem_st16(lane_base + T2_LCOL + 16 * g, lv);
         sm100::tmem_st_wait();
       }
-      l_run = rescale ? l_run * alpha + rs : l_run + rs;
       m_run = m_ref;
 #pragma unroll
       for (int cq = 0; cq < 8; ++cq)
@@ -1147,19 +1354,25 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&p_full[g]);
+      if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 6);
     }
     // ---------------- merge the two groups; thread (g, row) writes dims [64 g, 64 g + 64)
     if (u >= 1) sm100::mbar_wait(&o_done[g], (u - 1) & 1);
     xm[g][row] = m_run;
-    xl[g][row] = l_run;
     sm100::tc_fence_before();
     named_bar_sync(1, 256);
     sm100::tc_fence_after();
     const float mA = xm[0][row], mB = xm[1][row];
     const float M = fmaxf(mA, mB);
     const float wA = (mA == -INFINITY) ? 0.f : ex2(mA - M), wB = (mB == -INFINITY) ? 0.f : ex2(mB - M);
-    const float L = wA * xl[0][row] + wB * xl[1][row];
     const bool hasA = n_tiles >= 1, hasB = n_tiles >= 2;
+    float L = 0.f;
+    {
+      float la[16], lb[16];
+      if (hasA) sm100::tmem_ld16(lane_base + T2_LCOL, la);
+      if (hasB) sm100::tmem_ld16(lane_base + T2_LCOL + 16, lb);
+      L = (hasA ? wA * la[0] : 0.f) + (hasB ? wB * lb[0] : 0.f);
+    }
     float o[64];
 #pragma unroll
     for (int cc = 0; cc < 4; ++cc) {
@@ -1169,7 +1382,21 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
 #pragma unroll
       for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
     }
-    if (valid) {
+    if (a.n_splits > 1 && a.merge) {
+      float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once both groups' last PV is done
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
+            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      if (valid && g == 0) {
+        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        *reinterpret_cast<float2*>(a.ws_ml + r * 2) = make_float2(M, L);
+      }
+      named_bar_sync(1, 256);
+      if (threadIdx.x == 64) TRACE(31, 5);
+      if (threadIdx.x == 64) TRACE_MAX(1);
+      split_merge<256>(a, stg, head, split, rb, threadIdx.x - 64);
+    } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
         uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
@@ -1189,6 +1416,8 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
       }
     }
   }
+  if (threadIdx.x == 64) TRACE_MAX(2);
+  if (threadIdx.x == 0) TRACE(31, 0);
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -1201,6 +1430,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_tc2_kernel(const __grid_con
 // with online rescaling, 4 splits in flight per iteration
 __global__ void attn_combine_kernel(AttnArgs a) {
   sm100::grid_dep_launch();
+  if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 0);
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   const int rows = a.s * a.n_q;
@@ -1243,6 +1473,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   const int tok = row / a.n_q, qh = row % a.n_q;
   __nv_bfloat16* op = a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + lane * 4;
   *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+  if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 1);
 }
 
 }  // namespace bst
@@ -1275,8 +1506,9 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   pps += pps & 1;  // the default kernel walks 128-key tiles (page pairs)
   n_splits = (pages + pps - 1) / pps;
   if (n_splits > 1) {
-    const size_t need = (size_t)n_splits * s * n_q * (A_D + 2) * sizeof(float);
+    const size_t need = A_WS_CNT_BYTES + (size_t)n_splits * s * n_q * (A_D + 2) * sizeof(float);
     BST_REQUIRE(ws && ws_bytes >= need, "attention workspace too small: %zu < %zu", ws_bytes, need);
+    BST_REQUIRE(n_kv * row_blocks * sizeof(unsigned long long) <= A_WS_CNT_BYTES, "too many (head, row-block) pairs");
   }
   CUtensorMap tm;
   const uint64_t rows = (uint64_t)n_layers * n_pages_total * 2 * n_kv * A_PAGE;
@@ -1306,8 +1538,9 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   a.n_splits = n_splits;
   a.row_blocks = row_blocks;
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)A_D);
-  a.ws_o = ws;
-  a.ws_ml = ws ? ws + (size_t)n_splits * s * n_q * A_D : nullptr;
+  a.cnt = reinterpret_cast<unsigned long long*>(ws);
+  a.ws_o = ws ? ws + A_WS_CNT_BYTES / sizeof(float) : nullptr;
+  a.ws_ml = ws ? a.ws_o + (size_t)n_splits * s * n_q * A_D : nullptr;
   a.pf = take_prefetch();
   cudaStream_t st = as_stream(stream);
   static int variant = -1;
@@ -1318,27 +1551,43 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
     // fails the engine's greedy-preservation test, under investigation).
     variant = (e && e[0] == 'm') ? 1 : ((e && e[0] == 'f') ? 0 : ((e && e[0] == 't' && e[2] == '1') ? 2 : 3));
   }
+  static int tc2_min = -1;
+  if (tc2_min < 0) {
+    const char* e = getenv("BST_TC2_MIN");
+    tc2_min = e ? atoi(e) : 8;
+  }
   static bool attr = false;
   const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
   const int smem_tc = T_Q_BYTES + T_P_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
   const int smem_fa = T_Q_BYTES + F_P_BYTES + F_STAGES * F_STAGE_BYTES + 1024;
+  const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
   if (!attr) {
     BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mma));
     BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     BST_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fa));
-    BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
+    BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc2));
     attr = true;
   }
   // default: single-group kernel for short per-CTA page runs, two alternating
   // softmax groups once a CTA walks >= 8 tiles (long context)
-  const int v = variant == 3 ? (pps >= 8 ? 3 : 2) : variant;
+  const int v = variant == 3 ? (pps >= tc2_min ? 3 : 2) : variant;
+  // splits merge in-kernel when the whole grid is one wave (one CTA per SM)
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    BST_CUDA(cudaGetDevice(&dev));
+    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  static int no_merge = -1;
+  if (no_merge < 0) no_merge = getenv("BST_ATTN_COMBINE") ? 1 : 0;
+  a.merge = (n_splits > 1 && (v == 2 || v == 3) && !no_merge && n_kv * n_splits * row_blocks <= n_sm) ? 1 : 0;
   if (v == 1)
     attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
   else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_kv, n_splits, row_blocks);
-    cfg.blockDim = dim3(v == 2 ? T_THREADS : F_THREADS);
-    cfg.dynamicSmemBytes = v == 0 ? smem_fa : smem_tc;
+    cfg.blockDim = dim3(v == 2 ? T_THREADS : (v == 3 ? T2_THREADS : F_THREADS));
+    cfg.dynamicSmemBytes = v == 0 ? smem_fa : (v == 3 ? smem_tc2 : smem_tc);
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -1352,8 +1601,9 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
     else
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc2_kernel, tm, a));
   }
-  if (n_splits > 1) {
+  if (n_splits > 1 && !a.merge) {
     const int rows_total = s * n_q;
+    // plain launch: a PDL launch of the combine measured slower in the verify graph
     attn_combine_kernel<<<(rows_total + 7) / 8, 256, 0, st>>>(a);
   }
   BST_LAUNCH_CHECK();
@@ -1361,10 +1611,36 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
 }
 
 extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {
-  return (size_t)(n_splits < 1 ? 1 : n_splits) * s * n_q * (128 + 2) * sizeof(float);
+  return bst::A_WS_CNT_BYTES + (size_t)(n_splits < 1 ? 1 : n_splits) * s * n_q * (128 + 2) * sizeof(float);
+}
+
+extern "C" int bst_debug_attn_trace_cta(int y) {
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_attn_trace_y, &y, sizeof(int)));
+  return BST_OK;
 }
 
 extern "C" int bst_debug_attn_trace(void* buf) {
   BST_CUDA(cudaMemcpyToSymbol(bst::g_attn_trace, &buf, sizeof(void*)));
   return BST_OK;
+}
+
+// debug: how many clusters of `cluster` attention CTAs (dynamic smem `smem`) fit at once
+extern "C" int bst_debug_cluster_occupancy(int cluster, int smem) {
+  using namespace bst;
+  BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(8, cluster, 1);
+  cfg.blockDim = dim3(T_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = cluster;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  BST_CUDA(cudaOccupancyMaxActiveClusters(&n, attn_tc_kernel, &cfg));
+  return n;
 }

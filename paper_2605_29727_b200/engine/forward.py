@@ -68,7 +68,7 @@ def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
         splits = math.ceil(pages / pps)
         if splits > 1:
             best = max(best, splits * s * cfg.n_q * 130)
-    return max(best, 1)
+    return best + 1024  # + the 4 KiB split-counter head (zero-initialised, kept zero by K3)
 
 
 def _max_partial(shapes, max_rows: int) -> int:
@@ -97,7 +97,7 @@ class TargetModel:
         self.amx_scratch = torch.zeros(R, dtype=torch.int64, device=dev)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h)]
         self.partial = torch.empty(_max_partial(shapes, R), **f32)
-        self.attn_ws = torch.empty(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
+        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
         self.logits = None
 
     def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
@@ -170,7 +170,7 @@ class DrafterModel:
         self.qrow = torch.zeros(R, **i32)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h), (h, n_feat * h)]
         self.partial = torch.empty(_max_partial(shapes, R), **f32)
-        self.attn_ws = torch.empty(_attn_ws_floats(cfg, self.B, self.kv.n_pages), **f32)
+        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, self.B, self.kv.n_pages), **f32)
         self.logits = torch.empty(dcfg.gamma, cfg.V, **f32)
 
     def _ctx_rows(self, n: int, x_ctx: torch.Tensor, state: torch.Tensor) -> None:

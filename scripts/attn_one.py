@@ -16,7 +16,7 @@ q = torch.randn(s, n_q * 128, device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
 words = (s + 31) // 32
 anc = torch.full((s, words), -1, dtype=torch.int32, device="cuda")
-ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+ws = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
 for _ in range(3):
     ops.attention(q, out, kv.buf, 1, kv.n_pages, 0, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0, anc.view(-1),
                   words, ws)

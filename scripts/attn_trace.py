@@ -18,7 +18,7 @@ q = torch.randn(s, n_q * 128, device="cuda").to(torch.bfloat16)
 out = torch.empty_like(q)
 words = (s + 31) // 32
 anc = torch.full((s, words), -1, dtype=torch.int32, device="cuda")
-ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+ws = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
 run = lambda: ops.attention(q, out, kv.buf, 1, kv.n_pages, 0, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0,
                             anc.view(-1), words, ws)
 run()
@@ -28,7 +28,9 @@ lib.bst_debug_attn_trace(tr.data_ptr())
 run()
 torch.cuda.synchronize()
 t = tr.view(32, 8).cpu()
-t0 = int(t[0, 0])
+t0 = int(t[31, 1])  # kernel entry of the traced CTA
+print("entry->depwait/q_ready/staged/exit:", [round((int(t[31, k]) - t0) / 1000, 2) for k in (2, 3, 5, 0)])
+print("all CTAs max depwait/staged/end/arrive/spin_done:", [round((int(t[29, k]) - t0) / 1000, 2) for k in range(5)])
 names = ["tma_issued", "mma:full", "mma:p_full", "sm:s_full", "sm:sm_done", "sm:o_done", "sm:p_arrive", "sm:max_local"]
 for i in range(min(32, 30)):
     print(i, " ".join(f"{n}={(int(t[i, k]) - t0) / 1000:8.2f}" if int(t[i, k]) else f"{n}=   -    " for k, n in enumerate(names)))

@@ -33,7 +33,7 @@ for c in [int(x) for x in (sys.argv[1:] or ["2048", "32768"])]:
         for i in range(s):
             anc[i, 0] |= 1
             anc[i, i // 32] |= (1 << (i % 32)) if (i % 32) != 31 else -(1 << 31)
-        ws = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+        ws = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
         ts = []
         for it in range(23):
             flush.zero_()

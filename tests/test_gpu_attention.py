@@ -63,7 +63,7 @@ def test_tree_attention(n_q, n_kv, c, s, splits):
     words = (s + 31) // 32
     packed = torch.from_numpy(pack_mask(anc.cpu().numpy(), words)).cuda()
     out = torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16)
-    ws = torch.empty(8 << 20, device="cuda", dtype=torch.float32)
+    ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
     ops.attention(q, out, kv.buf, 2, kv.n_pages, 1, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0, packed.view(-1),
                   words, ws, n_splits=splits)
     vis = torch.zeros(s, c + s, dtype=torch.bool, device="cuda")
@@ -83,7 +83,7 @@ def test_causal_and_full_attention_with_device_c(mode, c, s):
     kv, q = _setup(n_q, n_kv, c, s, seed=7 + c)
     state = torch.tensor([c, 0, 0, 0, 0, 0, 0, 0], dtype=torch.int32, device="cuda")
     out = torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16)
-    ws = torch.empty(8 << 20, device="cuda", dtype=torch.float32)
+    ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
     ops.attention(q, out, kv.buf, 2, kv.n_pages, 1, kv.page_table, n_q, n_kv, s, 0, s, c + s + 64, state, mode,
                   None, 0, ws)
     vis = torch.zeros(s, c + s, dtype=torch.bool, device="cuda")
