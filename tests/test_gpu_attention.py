@@ -49,7 +49,7 @@ def _ref(q, kv, layer, n_q, n_kv, c, s, visible):
 
 
 @pytest.mark.parametrize("n_q,n_kv", [(32, 8), (4, 2)])
-@pytest.mark.parametrize("c,s", [(0, 1), (5, 17), (2048, 17), (300, 65), (1000, 256), (4096, 33)])
+@pytest.mark.parametrize("c,s", [(0, 1), (5, 17), (2048, 17), (300, 65), (1000, 256), (4096, 33), (20000, 17), (9000, 100)])
 @pytest.mark.parametrize("splits", [0, 1])
 def test_tree_attention(n_q, n_kv, c, s, splits):
     from oracle import specplan_port as O
