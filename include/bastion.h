@@ -195,6 +195,16 @@ int bst_attention(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_
                   int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
                   int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
                   const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes, bst_stream_t stream);
+/* Batched K3: n_req requests of s query rows each in one launch (config 3).
+ * Request r owns q/out rows [r*s, r*s+s), page_table[r*req_pages ...], state
+ * words state[r*req_state ...] (c = state[r*req_state + c_idx]) and ancestor-mask
+ * rows anc[(r*s + i) * mask_words ...].  ws: bst_attention_workspace(n_q, s, n_splits)
+ * times n_req (plus the shared 4 KiB counter head). */
+int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                        int n_layers, int n_pages_total, int layer, const int32_t* page_table, int req_pages, int n_q,
+                        int n_kv, int n_req, int s, int keys_after_c, int max_keys, const int32_t* state, int req_state,
+                        int c_idx, int mode, const uint32_t* anc, int mask_words, int n_splits, float* ws,
+                        size_t ws_bytes, bst_stream_t stream);
 size_t bst_attention_workspace(int n_q, int s, int n_splits);
 
 /* ------------------------------------------------------------------------
@@ -211,6 +221,14 @@ int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched, int rows, 
                  const int32_t* slot,
                  const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv, int64_t layer_off_elems,
                  const int32_t* page_table, int page_size, const int32_t* state, int state_c_idx, bst_stream_t stream);
+/* batched requests (req_rows > 0): row t belongs to request r = (t % req_span) / req_rows,
+ * positions/slots are relative to c_r = state[r*req_state + c_idx] and slots are offset by
+ * r*req_slots (request r's page range in a shared page table). */
+int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
+                       const void* q_norm, const void* k_norm, float eps, const float* inv_freq, const int32_t* pos,
+                       const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv,
+                       int64_t layer_off_elems, const int32_t* page_table, int page_size, const int32_t* state,
+                       int state_c_idx, int req_rows, int req_span, int req_state, int req_slots, bst_stream_t stream);
 int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act, int64_t lda,
                bst_stream_t stream);
 int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx, const int32_t* count, int max_rows, int cols,
@@ -230,6 +248,11 @@ int bst_verify_rows(const int32_t* state, const int32_t* tree_token, const int32
  * ctx rows i < n_new at pos/slot i - n_new, the rest skipped. */
 int bst_drafter_rows(const int32_t* state, int gamma, int mask_token, int ctx_rows, int32_t* tokens, int32_t* pos,
                      int32_t* slot, int32_t* qrow, bst_stream_t stream);
+/* batched drafter rows: request r's gamma+1 block rows at [r*(gamma+1), ...) (qrow = row),
+ * its ctx_rows context rows at [n_req*(gamma+1) + r*ctx_rows, ...); state words of
+ * request r at state[r*req_state ...]. */
+int bst_drafter_rows_batch(const int32_t* state, int req_state, int n_req, int gamma, int mask_token, int ctx_rows,
+                           int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* qrow, bst_stream_t stream);
 /* after bst_accept: append committed tokens to out_tokens, c += len,
  * n_new = len, bonus = meta[1]; log this cycle (tree meta, len, c, bonus,
  * surrogate) at log[state[BST_ST_CYCLE]] (8 int32 + 1 f64 per cycle). */

@@ -75,15 +75,20 @@ SIGNATURES = {
     "bst_expand_dev": (_I, [_P, _P, _I, _I, _P, _I, _I, _I, C.POINTER(Tree), _P, _SZ, _P]),
     "bst_attention": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I,
                            _P, _SZ, _P]),
+    "bst_attention_batch": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I,
+                                 _P, _I, _I, _P, _SZ, _P]),
     "bst_attention_workspace": (_SZ, [_I, _I, _I]),
     "bst_embed_rmsnorm": (_I, [_P, _I, _P, _I, _P, C.c_float, _P, _P, _I64, _P]),
     "bst_residual_rmsnorm": (_I, [_P, _P, _P, _I, _I, _P, C.c_float, _P, _I64, _P, _I64, _P]),
     "bst_qkv_rope": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64, _P, _I64,
                           _P, _I, _P, _I, _P]),
+    "bst_qkv_rope_batch": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64,
+                                _P, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P]),
     "bst_swiglu": (_I, [_P, C.POINTER(GemmSched), _I, _I, _P, _I64, _P]),
     "bst_gather_rows": (_I, [_P, _I64, _P, _P, _I, _I, _P, _I64, _P]),
     "bst_verify_rows": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_drafter_rows": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "bst_drafter_rows_batch": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "bst_commit_state": (_I, [_P, _P, _P, _I, _P, _I, _P, _P, _P, _P, _I, _P]),
     "bst_set_prefetch": (_I, [C.POINTER(Prefetch)]),
     "bst_accept": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
@@ -121,8 +126,9 @@ def check(rc: int) -> None:
 KERNELS_PER_CALL = {
     "bst_topk_logits": 3, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_linearize_mask": 1,
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
-    "bst_gemm_argmax": 2, "bst_attention": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
+    "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,
+    "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1,
 }
 launch_count = 0
 

@@ -57,6 +57,10 @@ struct AttnArgs {
   float* ws_ml;            // [split][s*n_q][2] (running max (log2 domain), sum)
   unsigned long long* cnt; // [row_blocks][n_kv] split barrier words (generation | arrivals)
   int merge;               // 1: splits merged in-kernel (one-wave grid), 0: attn_combine_kernel
+  // batched requests (blockIdx.z = req * row_blocks + rb): request req owns query rows
+  // [req * s, req * s + s), page-table entries [req * req_pages, ...), state words
+  // [req * req_state, ...) and ws partials [req][split][s * n_q]
+  int n_req, req_pages, req_state;
   bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
 };
 
@@ -205,7 +209,7 @@ __device__ __forceinline__ long long gtimer_ns() {
 //    (fixed split order: deterministic) and store bf16;
 // 4. second arrival; the last one resets the counter to zero for the next launch.
 template <int NT>
-__device__ void split_merge(const AttnArgs& a, const float* stg, int head, int split, int rb, int t) {
+__device__ void split_merge(const AttnArgs& a, const float* stg, int head, int split, int req, int rb, int t) {
   constexpr int NW = NT / 32;
   const int warp = t >> 5, lane = t & 31;
   const int R = a.group * a.s;
@@ -213,7 +217,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   const int64_t rows_all = (int64_t)a.s * a.n_q;
   for (int r = warp; r < Rb; r += NW) {
     const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
-    const int64_t gr = split * rows_all + (int64_t)tok * a.n_q + qh;
+    const int64_t gr = ((int64_t)req * a.n_splits + split) * rows_all + (int64_t)tok * a.n_q + qh;
     const float4 v = *reinterpret_cast<const float4*>(stg + r * A_D + ((lane ^ (r & 7)) << 2));
     __stcg(reinterpret_cast<float4*>(a.ws_o + gr * A_D) + lane, v);
   }
@@ -221,7 +225,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   // (generation << 32 | arrivals); the last arrival clears the arrivals and bumps the
   // generation in one release RMW, the others spin (acquire) until the generation moves.
   named_bar_sync(1, NT);
-  unsigned long long* cnt = a.cnt + rb * a.n_kv + head;
+  unsigned long long* cnt = a.cnt + ((int64_t)req * a.row_blocks + rb) * a.n_kv + head;
   if (t == 0) {
     const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
     TRACE_MAX(3);
@@ -245,7 +249,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   for (int it = t; it < (r1 - r0) * IPR; it += NT) {
     const int r = r0 + it / IPR, d0 = (it % IPR) * DI;
     const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
-    const int64_t base = (int64_t)tok * a.n_q + qh;
+    const int64_t base = (int64_t)req * a.n_splits * rows_all + (int64_t)tok * a.n_q + qh;
     float M = -INFINITY, L = 0.f, acc[DI];
 #pragma unroll
     for (int e = 0; e < DI; ++e) acc[e] = 0.f;
@@ -288,7 +292,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
       M = Mn;
     }
     const float inv = L > 0.f ? 1.f / L : 0.f;
-    __nv_bfloat16* op = a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + d0;
+    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + d0;
     if constexpr (DI == 8) {
       *reinterpret_cast<uint4*>(op) = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
                                                  pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
@@ -296,6 +300,14 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
       *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
     }
   }
+}
+
+// Slots the previous kernel cannot be writing, so their pages may be loaded before
+// griddepcontrol.wait: the committed prefix below c, except that in FULL mode (the
+// drafter block) the keys_after_c context slots just below c are written by the
+// preceding qkv_rope as well (newly committed tokens' context K/V).
+__device__ __forceinline__ int pdl_safe_slots(const AttnArgs& a, int c_ctx) {
+  return max(c_ctx - (a.mode == 2 ? a.keys_after_c : 0), 0);
 }
 
 // Pages [page0, page0 + n_tiles) of this split: the live pages (those holding keys
@@ -555,8 +567,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   uint8_t* gP = smem + T_Q_BYTES;
   uint8_t* gKV = gP + T_P_BYTES;
 
-  const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
-  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
+  const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
+  const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
   const int R = a.group * a.s;
   int page0, n_tiles;
@@ -585,7 +597,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
                      gridDim.x * gridDim.y * gridDim.z);
       // PDL: pages entirely below c hold committed K/V the previous kernel does not
       // touch; the page holding slot c onwards is written by qkv_rope right before us.
-      const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
+      const int safe_tiles = max(min(pdl_safe_slots(a, c_ctx) / A_PAGE - page0, n_tiles), 0);
       bool waited = false;
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i % T_STAGES;
@@ -594,7 +606,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
           sm100::grid_dep_wait();
           waited = true;
         }
-        const int phys = a.page_table[page0 + i];
+        const int phys = a.page_table[(int64_t)req * a.req_pages + page0 + i];
         const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
         const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
         uint8_t* dst = gKV + st * A_STAGE_BYTES;
@@ -657,14 +669,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     const int rr = valid ? rg : 0;
     const int tok = rr / a.group;
     const int qh = head * a.group + rr % a.group;
-    const uint32_t* mrow = a.mode == 0 ? a.anc + (int64_t)tok * a.mask_words : nullptr;
+    const uint32_t* mrow = a.mode == 0 ? a.anc + ((int64_t)req * a.s + tok) * a.mask_words : nullptr;
     const int mode = a.mode, mwords = a.mask_words;
     const float scale = a.scale_log2;
     sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
     if (threadIdx.x == 64) TRACE(31, 2);
     if (threadIdx.x == 64) TRACE_MAX(0);
     {  // stage Q row (256 B) into the swizzled K-major tile
-      const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D);
+      const int4* src = reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
@@ -788,23 +800,23 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
         *reinterpret_cast<float4*>(stg + row * A_D + ((q ^ (row & 7)) << 2)) =
             make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
       if (valid) {
-        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
         *reinterpret_cast<float2*>(a.ws_ml + r * 2) = make_float2(m_run, l_run);
       }
       named_bar_sync(1, 128);
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
-      split_merge<128>(a, stg, head, split, rb, threadIdx.x - 64);
+      split_merge<128>(a, stg, head, split, req, rb, threadIdx.x - 64);
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D);
+        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D);
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
                              pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
       } else {
-        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
         float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D);
 #pragma unroll
         for (int q = 0; q < 32; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
@@ -884,7 +896,7 @@ __global__ void __launch_bounds__(F_THREADS, 1) attn_fa_kernel(const __grid_cons
     if (lane == 0) {
       issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
                      gridDim.x * gridDim.y * gridDim.z);
-      const int safe_tiles = max(min((c_ctx / A_PAGE - page0) >> 1, n_tiles), 0);
+      const int safe_tiles = max(min((pdl_safe_slots(a, c_ctx) / A_PAGE - page0) >> 1, n_tiles), 0);
       bool waited = false;
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i % F_STAGES;
@@ -1136,8 +1148,8 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   uint8_t* gP = smem + T_Q_BYTES;
   uint8_t* gKV = gP + T_P_BYTES;  // K ring, then V ring; reused as the merge staging buffer
 
-  const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
-  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
+  const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
+  const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
   const int R = a.group * a.s;
   int page0, n_tiles;
@@ -1174,7 +1186,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       uint8_t* ring = isK ? gKV : gKV + T2_KS * A_TILE_BYTES;
       // PDL: pages entirely below c hold committed K/V the previous kernel does not
       // touch; the page holding slot c onwards is written by qkv_rope right before us.
-      const int safe_tiles = max(min(c_ctx / A_PAGE - page0, n_tiles), 0);
+      const int safe_tiles = max(min(pdl_safe_slots(a, c_ctx) / A_PAGE - page0, n_tiles), 0);
       bool waited = false;
       for (int i = 0; i < n_tiles; ++i) {
         const int st = i % ns;
@@ -1183,7 +1195,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
           sm100::grid_dep_wait();
           waited = true;
         }
-        const int phys = a.page_table[page0 + i];
+        const int phys = a.page_table[(int64_t)req * a.req_pages + page0 + i];
         const int64_t row = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + (isK ? 0 : 1)) * a.n_kv + head) * A_PAGE;
         uint8_t* dst = ring + st * A_TILE_BYTES;
         sm100::mbar_expect_tx(&fb[st], A_TILE_BYTES);
@@ -1255,14 +1267,14 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
     const int rr = valid ? rg : 0;
     const int tok = rr / a.group;
     const int qh = head * a.group + rr % a.group;
-    const uint32_t* mrow = a.mode == 0 ? a.anc + (int64_t)tok * a.mask_words : nullptr;
+    const uint32_t* mrow = a.mode == 0 ? a.anc + ((int64_t)req * a.s + tok) * a.mask_words : nullptr;
     const int mode = a.mode, mwords = a.mask_words;
     const float scale = a.scale_log2;
     sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
     if (threadIdx.x == 64) TRACE(31, 2);
     if (threadIdx.x == 64) TRACE_MAX(0);
     {  // each group stages one 64-dim half of the row
-      const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
+      const int4* src = reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
@@ -1389,23 +1401,23 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
         *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
             make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
       if (valid && g == 0) {
-        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
         *reinterpret_cast<float2*>(a.ws_ml + r * 2) = make_float2(M, L);
       }
       named_bar_sync(1, 256);
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
-      split_merge<256>(a, stg, head, split, rb, threadIdx.x - 64);
+      split_merge<256>(a, stg, head, split, req, rb, threadIdx.x - 64);
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
+        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
                              pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
       } else {
-        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
+        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
         float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D + 64 * g);
 #pragma unroll
         for (int q = 0; q < 16; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
@@ -1431,7 +1443,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
 __global__ void attn_combine_kernel(AttnArgs a) {
   sm100::grid_dep_launch();
   if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 0);
-  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+  const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), req = blockIdx.y;
   const int lane = threadIdx.x & 31;
   const int rows = a.s * a.n_q;
   if (row >= rows) return;
@@ -1444,7 +1456,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
     for (int j = 0; j < 4; ++j) {
       const int sp = sp0 + j;
       if (sp < a.n_splits) {
-        const int64_t r = (int64_t)sp * rows + row;
+        const int64_t r = ((int64_t)req * a.n_splits + sp) * rows + row;
         m[j] = a.ws_ml[r * 2];
         l[j] = a.ws_ml[r * 2 + 1];
         v[j] = *reinterpret_cast<const float4*>(a.ws_o + r * A_D + lane * 4);
@@ -1471,20 +1483,22 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   const int tok = row / a.n_q, qh = row % a.n_q;
-  __nv_bfloat16* op = a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + lane * 4;
+  __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + lane * 4;
   *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 1);
 }
 
 }  // namespace bst
 
-extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
-                             int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv,
-                             int s, int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
-                             const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
-                             bst_stream_t stream) {
-  using namespace bst;
+namespace bst {
+static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                          int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
+                          int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
+                          const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes, int n_req,
+                          int req_pages, int req_state, bst_stream_t stream) {
   BST_REQUIRE(q && out && kv_cache && page_table, "null pointer argument");
+  BST_REQUIRE(n_req >= 1 && (n_req == 1 || (req_pages >= 1 && (state == nullptr || req_state >= 1))),
+              "batched attention needs per-request page and state strides");
   BST_REQUIRE(n_kv >= 1 && n_q % n_kv == 0, "n_q must be a multiple of n_kv");
   BST_REQUIRE(s >= 1 && c >= 0 && keys_after_c >= 0, "bad sizes");
   BST_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (tree), 1 (causal) or 2 (full)");
@@ -1495,10 +1509,11 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   const int row_blocks = (R + A_ROWS_PER_CTA - 1) / A_ROWS_PER_CTA;
   const int pages = (max_keys + A_PAGE - 1) / A_PAGE;
   BST_REQUIRE(pages <= n_pages_total, "context exceeds the page table");
+  if (n_req > 1) BST_REQUIRE(req_pages >= pages, "request page slice (%d) smaller than the context (%d pages)", req_pages, pages);
   if (n_splits <= 0) {
     // one wave of CTAs: per-tile work (GQA group x tokens rows against 64 keys)
     // dominates a CTA's fixed cost, so spread the pages over every SM
-    int want = 148 / (n_kv * row_blocks);
+    int want = 148 / (n_kv * row_blocks * n_req);
     n_splits = want < 1 ? 1 : want;
   }
   if (n_splits > pages) n_splits = pages;
@@ -1506,9 +1521,8 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   pps += pps & 1;  // the default kernel walks 128-key tiles (page pairs)
   n_splits = (pages + pps - 1) / pps;
   if (n_splits > 1) {
-    const size_t need = A_WS_CNT_BYTES + (size_t)n_splits * s * n_q * (A_D + 2) * sizeof(float);
+    const size_t need = A_WS_CNT_BYTES + (size_t)n_req * n_splits * s * n_q * (A_D + 2) * sizeof(float);
     BST_REQUIRE(ws && ws_bytes >= need, "attention workspace too small: %zu < %zu", ws_bytes, need);
-    BST_REQUIRE(n_kv * row_blocks * sizeof(unsigned long long) <= A_WS_CNT_BYTES, "too many (head, row-block) pairs");
   }
   CUtensorMap tm;
   const uint64_t rows = (uint64_t)n_layers * n_pages_total * 2 * n_kv * A_PAGE;
@@ -1540,7 +1554,10 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   a.scale_log2 = 1.4426950408889634f / sqrtf((float)A_D);
   a.cnt = reinterpret_cast<unsigned long long*>(ws);
   a.ws_o = ws ? ws + A_WS_CNT_BYTES / sizeof(float) : nullptr;
-  a.ws_ml = ws ? a.ws_o + (size_t)n_splits * s * n_q * A_D : nullptr;
+  a.ws_ml = ws ? a.ws_o + (size_t)n_req * n_splits * s * n_q * A_D : nullptr;
+  a.n_req = n_req;
+  a.req_pages = req_pages;
+  a.req_state = req_state;
   a.pf = take_prefetch();
   cudaStream_t st = as_stream(stream);
   static int variant = -1;
@@ -1580,12 +1597,14 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   }
   static int no_merge = -1;
   if (no_merge < 0) no_merge = getenv("BST_ATTN_COMBINE") ? 1 : 0;
-  a.merge = (n_splits > 1 && (v == 2 || v == 3) && !no_merge && n_kv * n_splits * row_blocks <= n_sm) ? 1 : 0;
+  a.merge = (n_splits > 1 && (v == 2 || v == 3) && !no_merge && n_kv * n_splits * row_blocks * n_req <= n_sm &&
+             n_kv * row_blocks * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES) ? 1 : 0;
+  BST_REQUIRE(n_req == 1 || v == 2 || v == 3, "batched attention runs on the tcgen05 kernels only");
   if (v == 1)
     attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
   else {
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(n_kv, n_splits, row_blocks);
+    cfg.gridDim = dim3(n_kv, n_splits, row_blocks * n_req);
     cfg.blockDim = dim3(v == 2 ? T_THREADS : (v == 3 ? T2_THREADS : F_THREADS));
     cfg.dynamicSmemBytes = v == 0 ? smem_fa : (v == 3 ? smem_tc2 : smem_tc);
     cfg.stream = st;
@@ -1604,10 +1623,33 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
   if (n_splits > 1 && !a.merge) {
     const int rows_total = s * n_q;
     // plain launch: a PDL launch of the combine measured slower in the verify graph
-    attn_combine_kernel<<<(rows_total + 7) / 8, 256, 0, st>>>(a);
+    attn_combine_kernel<<<dim3((rows_total + 7) / 8, n_req), 256, 0, st>>>(a);
   }
   BST_LAUNCH_CHECK();
   return BST_OK;
+}
+
+}  // namespace bst
+
+extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                             int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv,
+                             int s, int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
+                             const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
+                             bst_stream_t stream) {
+  return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
+                             n_q, n_kv, s, c, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
+                             ws, ws_bytes, 1, 0, 0, stream);
+}
+
+extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
+                                   const void* kv_cache, int n_layers, int n_pages_total, int layer,
+                                   const int32_t* page_table, int req_pages, int n_q, int n_kv, int n_req, int s,
+                                   int keys_after_c, int max_keys, const int32_t* state, int req_state, int c_idx,
+                                   int mode, const uint32_t* anc, int mask_words, int n_splits, float* ws,
+                                   size_t ws_bytes, bst_stream_t stream) {
+  return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
+                             n_q, n_kv, s, 0, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
+                             ws, ws_bytes, n_req, req_pages, req_state, stream);
 }
 
 extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {

@@ -107,15 +107,19 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
                                 const float* __restrict__ inv_freq, const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
                                 const int32_t* __restrict__ qrow, __nv_bfloat16* q_out, int64_t q_tok_stride,
                                 __nv_bfloat16* kv, int64_t layer_off, const int32_t* __restrict__ page_table,
-                                int page_size, const int32_t* __restrict__ state, int state_c_idx, bst_prefetch_t pf) {
+                                int page_size, const int32_t* __restrict__ state, int state_c_idx, bst_prefetch_t pf,
+                                int req_rows, int req_span, int req_state, int req_slots) {
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  const int c0 = state ? state[state_c_idx] : 0;
+  // batched requests: row t belongs to request (t % req_span) / req_rows, whose
+  // context length is state[r * req_state + c_idx] and whose slots start at r * req_slots
+  const int r = req_rows > 0 ? (t % req_span) / req_rows : 0;
+  const int c0 = state ? state[r * req_state + state_c_idx] : 0;
   const int p = pos[t] + c0;
-  const int sl = slot[t] == INT_MIN ? -1 : slot[t] + c0;
+  const int sl = slot[t] == INT_MIN ? -1 : slot[t] + c0 + r * req_slots;
   const int qr = qrow ? qrow[t] : t;
   // rotary angles for this lane's 4 dims (i in [0,64) pairs with i+64)
   float cs[4], sn[4];
@@ -222,20 +226,31 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   return BST_OK;
 }
 
-extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
-                            const void* q_norm, const void* k_norm, float eps, const float* inv_freq, const int32_t* pos,
-                            const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv,
-                            int64_t layer_off_elems, const int32_t* page_table, int page_size, const int32_t* state,
-                            int state_c_idx, bst_stream_t stream) {
+extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
+                                  const void* q_norm, const void* k_norm, float eps, const float* inv_freq,
+                                  const int32_t* pos, const int32_t* slot, const int32_t* qrow, void* q_out,
+                                  int64_t q_tok_stride, void* kv, int64_t layer_off_elems, const int32_t* page_table,
+                                  int page_size, const int32_t* state, int state_c_idx, int req_rows, int req_span,
+                                  int req_state, int req_slots, bst_stream_t stream) {
   BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
               "null pointer argument");
   BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
   qkv_rope_kernel<<<rows, 512, 0, as_stream(stream)>>>(
       partial, *sched, n_q, n_kv, static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm),
       eps, inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride, static_cast<__nv_bfloat16*>(kv),
-      layer_off_elems, page_table, page_size, state, state_c_idx, take_prefetch());
+      layer_off_elems, page_table, page_size, state, state_c_idx, take_prefetch(), req_rows, req_span > 0 ? req_span : 1, req_state, req_slots);
   BST_LAUNCH_CHECK();
   return BST_OK;
+}
+
+extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
+                            const void* q_norm, const void* k_norm, float eps, const float* inv_freq, const int32_t* pos,
+                            const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv,
+                            int64_t layer_off_elems, const int32_t* page_table, int page_size, const int32_t* state,
+                            int state_c_idx, bst_stream_t stream) {
+  return bst_qkv_rope_batch(partial, sched, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out,
+                            q_tok_stride, kv, layer_off_elems, page_table, page_size, state, state_c_idx, 0, 1, 0, 0,
+                            stream);
 }
 
 extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act,
@@ -288,6 +303,28 @@ __global__ void drafter_rows_kernel(const int32_t* state, int gamma, int mask_to
     qrow[i] = -1;
   }
 }
+// batched drafter rows: request r's gamma+1 query rows at [r*(gamma+1), ...), its
+// ctx_rows context rows at [n_req*(gamma+1) + r*ctx_rows, ...); qrow = the q-buffer row
+__global__ void drafter_rows_batch_kernel(const int32_t* state, int req_state, int n_req, int gamma, int mask_token,
+                                          int ctx_rows, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* qrow) {
+  const int r = blockIdx.x;
+  const int n_new = state[r * req_state + BST_ST_NNEW];
+  const int i = threadIdx.x;
+  if (i <= gamma) {
+    const int t = r * (gamma + 1) + i;
+    tokens[t] = i == 0 ? state[r * req_state + BST_ST_BONUS] : mask_token;
+    pos[t] = i;
+    slot[t] = i;
+    qrow[t] = t;
+  } else if (i < gamma + 1 + ctx_rows) {
+    const int j = i - gamma - 1;
+    const int t = n_req * (gamma + 1) + r * ctx_rows + j;
+    tokens[t] = 0;
+    pos[t] = j - n_new;
+    slot[t] = j < n_new ? j - n_new : INT_MIN;
+    qrow[t] = -1;
+  }
+}
 __global__ void commit_state_kernel(int32_t* state, const int32_t* meta, const int32_t* committed, int max_path,
                                     int32_t* out_tokens, int out_cap, const int32_t* tree_meta,
                                     const double* surrogate, int32_t* log_i32, double* log_f64, int log_cap) {
@@ -331,6 +368,17 @@ extern "C" int bst_drafter_rows(const int32_t* state, int gamma, int mask_token,
   BST_REQUIRE(state && tokens && pos && slot && qrow, "null pointer argument");
   BST_REQUIRE(gamma + 1 + ctx_rows <= 1024, "too many drafter rows");
   drafter_rows_kernel<<<1, 1024, 0, as_stream(stream)>>>(state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+extern "C" int bst_drafter_rows_batch(const int32_t* state, int req_state, int n_req, int gamma, int mask_token,
+                                      int ctx_rows, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* qrow,
+                                      bst_stream_t stream) {
+  BST_REQUIRE(state && tokens && pos && slot && qrow && n_req >= 1, "null pointer argument");
+  BST_REQUIRE(gamma + 1 + ctx_rows <= 1024, "too many drafter rows");
+  drafter_rows_batch_kernel<<<n_req, 1024, 0, as_stream(stream)>>>(state, req_state, n_req, gamma, mask_token, ctx_rows,
+                                                                   tokens, pos, slot, qrow);
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -1,0 +1,254 @@
+"""BatchEngine — many independent decode streams on one GPU (BASELINE config 3).
+
+SURVEY §8(e): requests share nothing, so a GPU batches its shard of
+requests: their draft blocks and their trees are concatenated along the row
+dimension of the K4 GEMMs (weights are streamed once per row chunk instead of
+once per request) and K3 runs over every request of a chunk in one launch
+(``bst_attention_batch``: per-request context length, page range and ancestor
+mask).  Each request keeps its own device state, lattice, tree, accept walk, KV
+compaction and committed stream — the per-request controllers stay independent.
+
+Layout
+  * one paged KV pool per model; request r owns pages [r*P, (r+1)*P) of the
+    identity page table (P = pages per request);
+  * verify rows: request r's tree occupies rows [r*S, r*S+S) of its chunk
+    (S = N+1 for a fixed budget N; fixed-N trees always have N nodes here);
+  * draft rows: a chunk's n*(gamma+1) block rows, then its n*(gamma+1) context rows.
+
+A whole cycle (draft all chunks -> K1 -> K2 per request -> verify all chunks ->
+accept/compact/gather/commit per request) is one CUDA graph with no host sync:
+fixed budgets make every shape static.  Token streams are identical to running
+each request alone through ``B200Engine`` (tests/test_gpu_batch.py).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+
+import numpy as np
+import torch
+
+from .. import _lib, ops
+from ..device import graph_kernel_nodes
+from ..draft_tree import DeviceTree, expand_device_plan
+from ..lattice import topk_logits_into
+from ..verify_sim import accept_device
+from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
+from .decode import MAX_ROWS, ST_BONUS, ST_C, ST_COMMITTED, ST_CYCLE
+from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
+from .weights import DrafterWeights, TargetWeights
+
+
+class BatchEngine:
+    def __init__(self, cfg: ModelConfig = QWEN3_8B, dcfg: DrafterConfig | None = None, n_req: int = 8,
+                 n_fixed: int = 64, max_ctx: int = 4096, seed: int = 0, top_k: int = 8, device=None,
+                 max_cycles: int = 1024):
+        if not torch.cuda.is_available():
+            raise RuntimeError("BatchEngine needs a CUDA device; there is no CPU fallback")
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        if dev.index is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+        self.dev = dev
+        torch.cuda.set_device(dev)
+        dcfg = dcfg or DrafterConfig()
+        feat = dcfg.feat_layers or default_feat_layers(cfg.L)
+        self.dcfg = DrafterConfig(layers=dcfg.layers, gamma=dcfg.gamma, feat_layers=feat, mask_token=dcfg.mask_token,
+                                  logit_scale=dcfg.logit_scale)
+        self.cfg, self.n_req, self.top_k = cfg, n_req, top_k
+        self.gamma = self.dcfg.gamma
+        self.N = n_fixed
+        self.S = n_fixed + 1
+        if self.S > MAX_ROWS:
+            raise ValueError(f"fixed budget must be <= {MAX_ROWS - 1}")
+        G1 = self.gamma + 1
+        self.G1 = G1
+        self.chunk_v = max(1, MAX_ROWS // self.S)          # requests per verify chunk
+        self.chunk_d = max(1, MAX_ROWS // (2 * G1))        # requests per draft chunk
+        self.max_ctx = max_ctx
+        self.req_pages = math.ceil((max_ctx + MAX_ROWS + PAGE) / PAGE)
+        slots = n_req * self.req_pages * PAGE
+        self.tw = TargetWeights.random(cfg, seed, dev)
+        self.dw = DrafterWeights.random(cfg, self.dcfg, len(feat), seed, dev)
+        self.target = TargetModel(cfg, self.tw, slots, MAX_ROWS, feat, dev)
+        self.drafter = DrafterModel(cfg, self.dcfg, self.dw, self.tw, slots, len(feat), dev, n_req_max=self.chunk_d)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.state = torch.zeros(n_req, 8, **i32)
+        self.out_tokens = torch.zeros(n_req, max_ctx + MAX_ROWS, **i32)
+        self.lat_tok = torch.zeros(n_req * G1, top_k, **i32)
+        self.lat_prob = torch.zeros(n_req * G1, top_k, dtype=torch.float64, device=dev)
+        self.trees = [DeviceTree(self.S - 1, dev) for _ in range(n_req)]
+        self.mask_words = self.trees[0].mask_words
+        self.anc = torch.zeros(n_req, self.S * self.mask_words, **i32)  # contiguous ancestor masks (batched K3)
+        for r, tr in enumerate(self.trees):
+            tr.anc_mask = self.anc[r]
+        n_feat = len(feat) * cfg.h
+        self.feat = torch.zeros(n_req * G1, n_feat, dtype=torch.bfloat16, device=dev)  # drafter context features
+        self.path = torch.zeros(n_req, G1, **i32)
+        self.committed = torch.zeros(n_req, G1, **i32)
+        self.acc_meta = torch.zeros(n_req, 4, **i32)
+        self.log_i32 = torch.zeros(n_req, max_cycles * 8, **i32)
+        self.log_f64 = torch.zeros(n_req, max_cycles, dtype=torch.float64, device=dev)
+        self.plan_dev = torch.zeros(n_req, C.sizeof(_lib.Plan), dtype=torch.uint8, device=dev)
+        self.policy = _lib.POLICY_FIXED
+        self.set_policy("fixed")
+        self.stream = torch.cuda.Stream(dev)
+        self.graph = None
+        self.graph_kernels = 0
+        self.use_graphs = True
+        torch.cuda.synchronize()
+
+    def set_policy(self, kind: str, estimator=None, latencies=None) -> None:
+        """Per-request K2 plans: fixed-N (N = n_fixed) or adaptive Algorithm 1 with N_max = n_fixed,
+        each request reading its own context length from its state row (independent controllers)."""
+        if kind == "fixed":
+            plans = [_lib.Plan(policy=_lib.POLICY_FIXED, n_max=self.N) for _ in range(self.n_req)]
+            self.policy = _lib.POLICY_FIXED
+        elif kind == "adaptive":
+            if estimator is None or latencies is None:
+                raise ValueError("adaptive policy needs an estimator and cycle latencies")
+            curve = estimator.curve(0).device_struct()
+            p = estimator.params
+            plans = [_lib.Plan(policy=_lib.POLICY_ADAPTIVE, n_max=self.N, curve=curve,
+                               fixed_cost=latencies.t_draft + latencies.t_aux, l_ar=latencies.l_ar,
+                               state=self.state[r].data_ptr(), c_idx=ST_C, d_flops_lin=4 * p.L * p.h_q,
+                               d_bytes_const=p.bp * p.L * 2 * p.h_kv, d_bytes_lin=p.bp * p.L * 2 * p.n_q)
+                     for r in range(self.n_req)]
+            self.policy = _lib.POLICY_ADAPTIVE
+        else:
+            raise ValueError(f"unsupported batch policy {kind!r}")
+        raw = b"".join(bytes(pl) for pl in plans)
+        self.plan_dev.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8).view(self.n_req, -1))
+        self.graph = None  # the policy is a launch parameter of K2
+
+    def set_attention_splits(self, n: int) -> None:
+        """Pin the K3 split count of both models (0 = automatic); parity tests use 1."""
+        self.target.attn_splits = n
+        self.drafter.attn_splits = n
+
+    def _pt(self, r0: int) -> torch.Tensor:
+        return self.target.kv.page_table[r0 * self.req_pages:]
+
+    def _dpt(self, r0: int) -> torch.Tensor:
+        return self.drafter.kv.page_table[r0 * self.req_pages:]
+
+    # ------------------------------------------------------------------ setup
+    def reset(self, prompts) -> None:
+        """Prefill every request's prompt[:-1] into its page range; prompt[-1] becomes its pending root."""
+        if len(prompts) != self.n_req:
+            raise ValueError(f"need {self.n_req} prompts, got {len(prompts)}")
+        t, d = self.target, self.drafter
+        with torch.cuda.stream(self.stream):
+            for r, prompt in enumerate(prompts):
+                prompt = [int(x) for x in prompt]
+                if not prompt or len(prompt) > self.max_ctx:
+                    raise ValueError("prompt must hold 1..max_ctx tokens")
+                P = len(prompt)
+                st = self.state[r]
+                for start in range(0, P - 1, MAX_ROWS):
+                    n = min(MAX_ROWS, P - 1 - start)
+                    st.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+                    t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
+                    ar = torch.arange(n, dtype=torch.int32, device=self.dev)
+                    t.pos[:n].copy_(ar)
+                    t.slot[:n].copy_(ar)
+                    t.forward(n, st, MODE_CAUSAL, keys_after_c=n, head=None, c_host=start, pt=self._pt(r))
+                    d.feat_in[:n].copy_(t.feat[:n])
+                    d.pos[:n].copy_(ar)
+                    d.slot[:n].copy_(ar)
+                    d.prefill_ctx(n, st, pt=self._dpt(r))
+                st.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+        self.stream.synchronize()
+
+    # ------------------------------------------------------------------ cycle
+    def _cycle_body(self) -> None:
+        G1, S, rp, n_req = self.G1, self.S, self.req_pages, self.n_req
+        t, d = self.target, self.drafter
+        # phase 1: draft every request (chunks of chunk_d), K1 over all block rows, K2 per request
+        for r0 in range(0, n_req, self.chunk_d):
+            n = min(self.chunk_d, n_req - r0)
+            logits = d.forward_batch(self.state[r0:r0 + n], n, self._dpt(r0), rp,
+                                     feat=self.feat[r0 * G1:(r0 + n) * G1])
+            topk_logits_into(logits, self.top_k, self.lat_tok[r0 * G1:(r0 + n) * G1],
+                             self.lat_prob[r0 * G1:(r0 + n) * G1], None)
+        for r, tr in enumerate(self.trees):
+            rows = slice(r * G1 + 1, (r + 1) * G1)  # block row 0 is the bonus position
+            expand_device_plan(self.lat_tok[rows], self.lat_prob[rows], self.plan_dev[r], self.policy, self.N, tr)
+        # phase 2: verify every request (chunks of chunk_v), then accept / compact / gather / commit
+        for r0 in range(0, n_req, self.chunk_v):
+            n = min(self.chunk_v, n_req - r0)
+            for i in range(n):
+                tr = self.trees[r0 + i]
+                ops.verify_rows(self.state[r0 + i], tr.token, tr.depth, tr.meta, S, t.tokens[i * S:],
+                                t.pos[i * S:], t.slot[i * S:])
+            t.forward(n * S, self.state[r0:r0 + n], MODE_TREE, keys_after_c=S, anc=self.anc[r0:r0 + n],
+                      mask_words=self.mask_words, head="argmax", pt=self._pt(r0), batch=(n, S, rp))
+            for i in range(n):
+                r = r0 + i
+                tr = self.trees[r]
+                accept_device(tr.token, tr.child_start, tr.child_list, t.argmax[i * S:(i + 1) * S], G1,
+                              self.path[r], self.committed[r], self.acc_meta[r])
+                kv = t.kv
+                ops.kv_compact(kv.buf, self.cfg.L, self.cfg.n_kv, PAGE, kv.layer_stride, self._pt(r), self.state[r],
+                               self.path[r], self.acc_meta[r], G1)
+                ops.gather_rows(t.feat[i * S:(i + 1) * S], self.path[r], self.acc_meta[r], G1,
+                                self.feat[r * G1:(r + 1) * G1])
+                ops.commit_state(self.state[r], self.acc_meta[r], self.committed[r], G1, self.out_tokens[r],
+                                 tr.meta, tr.surrogate, self.log_i32[r], self.log_f64[r])
+
+    def _capture(self) -> torch.cuda.CUDAGraph:
+        saved = self.state.clone()
+        with torch.cuda.stream(self.stream):
+            self._cycle_body()  # warm-up: workspaces, tensor maps, kernel attributes
+        self.stream.synchronize()
+        self.state.copy_(saved)
+        g = torch.cuda.CUDAGraph(keep_graph=True)
+        with torch.cuda.graph(g, stream=self.stream):
+            self._cycle_body()
+        self.graph_kernels = graph_kernel_nodes(g)
+        g.instantiate()
+        self.stream.synchronize()
+        self.state.copy_(saved)
+        torch.cuda.synchronize()
+        return g
+
+    def cycle(self) -> None:
+        """One draft -> expand -> verify -> accept cycle for every request (asynchronous)."""
+        if not self.use_graphs:
+            with torch.cuda.stream(self.stream):
+                self._cycle_body()
+            return
+        if self.graph is None:
+            self.graph = self._capture()
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+
+    def committed_counts(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.state[:, ST_COMMITTED].cpu().numpy()
+
+    def run(self, max_new_tokens: int, check_every: int = 8) -> np.ndarray:
+        """Cycle until every request has committed >= max_new_tokens tokens; returns the counts."""
+        while True:
+            for _ in range(check_every):
+                self.cycle()
+            counts = self.committed_counts()
+            if counts.min() >= max_new_tokens:
+                return counts
+
+    def tokens(self, r: int) -> list[int]:
+        self.stream.synchronize()
+        n = int(self.state[r, ST_COMMITTED].item())
+        return self.out_tokens[r, :n].cpu().tolist()
+
+    def contexts(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.state[:, ST_C].cpu().numpy()
+
+    def cycles(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.state[:, ST_CYCLE].cpu().numpy()
+
+    def roots(self) -> np.ndarray:
+        self.stream.synchronize()
+        return self.state[:, ST_BONUS].cpu().numpy()

@@ -98,26 +98,45 @@ class TargetModel:
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h)]
         self.partial = torch.empty(_max_partial(shapes, R), **f32)
         self.attn_ws = torch.zeros(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
+        self.attn_splits = 0  # K3 split count (0: automatic); parity tests pin it
         self.logits = None
 
     def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
-                head: str | None = "argmax", c_host: int = 0) -> None:
-        """Run `rows` query rows (tokens/pos/slot buffers already filled, relative to c = state[0])."""
+                head: str | None = "argmax", c_host: int = 0, pt: torch.Tensor | None = None,
+                batch: tuple[int, int, int] | None = None) -> None:
+        """Run `rows` query rows (tokens/pos/slot buffers already filled, relative to c = state[0]).
+
+        pt: page-table view (a request's page range in a shared pool; default the whole table).
+        batch = (n_req, S, req_pages): rows are n_req requests of S rows each; request r's
+        state is state[r] (8 words), its pages pt[r*req_pages:], its mask rows anc[r*S:]."""
         cfg, w, kv = self.cfg, self.w, self.kv
         n, eps = rows, cfg.eps
+        pt = kv.page_table if pt is None else pt
         x, resid = self.x[:n], self.resid[:n]
         ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
         for li, lw in enumerate(w.layers):
             nxt_l = w.layers[li + 1] if li + 1 < cfg.L else None
             p = ops.gemm_partial(x, lw.qkv, out=self.partial)
             if "rope" not in _ABLATE:
-                ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
-                             None, self.q, kv.buf, li * kv.layer_stride, kv.page_table, PAGE, state)
+                if batch is None:
+                    ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
+                                 self.slot, None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state)
+                else:
+                    nr, S, rp = batch
+                    ops.qkv_rope_batch(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
+                                       self.slot, None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state, S,
+                                       nr * S, state.stride(0), rp * PAGE)
             if "attn" not in _ABLATE:
                 _pf((lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB))
-                ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, kv.page_table, cfg.n_q,
-                              cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
-                              self.attn_ws)
+                if batch is None:
+                    ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, cfg.n_q,
+                                  cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
+                                  self.attn_ws, n_splits=self.attn_splits)
+                else:
+                    nr, S, rp = batch
+                    ops.attention_batch(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, rp, cfg.n_q,
+                                        cfg.n_kv, nr, S, keys_after_c, rp * PAGE, state, state.stride(0), mode, anc,
+                                        mask_words, self.attn_ws, n_splits=self.attn_splits)
             p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
             if "resid" not in _ABLATE:
                 _pf((lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
@@ -147,49 +166,53 @@ class DrafterModel:
     """Block drafter: gamma+1 query rows ([bonus] + gamma masks) + gamma+1 context rows."""
 
     def __init__(self, cfg: ModelConfig, dcfg: DrafterConfig, w: DrafterWeights, target: TargetWeights,
-                 max_slots: int, n_feat: int, dev, prefill_rows: int = 256) -> None:
+                 max_slots: int, n_feat: int, dev, prefill_rows: int = 256, n_req_max: int = 1) -> None:
         self.cfg, self.dcfg, self.w, self.tw, self.dev = cfg, dcfg, w, target, dev
         self.kv = PagedKV(dcfg.layers, cfg.n_kv, max_slots, dev)
         self.inv_freq = rope_inv_freq(cfg, dev)
         self.B = dcfg.gamma + 1
         self.CR = dcfg.gamma + 1
+        self.n_req_max = n_req_max
         self.mask_token = dcfg.mask_token if dcfg.mask_token >= 0 else cfg.V - 1
-        R = max(self.B + self.CR, prefill_rows)
+        R = max((self.B + self.CR) * n_req_max, prefill_rows)
+        QB = self.B * n_req_max
         h = cfg.h
         f32, bf = dict(dtype=torch.float32, device=dev), dict(dtype=torch.bfloat16, device=dev)
         i32 = dict(dtype=torch.int32, device=dev)
-        self.resid = torch.empty(self.B, h, **f32)
+        self.resid = torch.empty(QB, h, **f32)
         self.X = torch.zeros(R, h, **bf)
-        self.q = torch.empty(self.B, cfg.h_q, **bf)
-        self.attn = torch.empty(self.B, cfg.h_q, **bf)
-        self.act = torch.empty(self.B, cfg.h_ffn, **bf)
-        self.feat_in = torch.zeros(max(self.CR, prefill_rows), n_feat * h, **bf)
+        self.q = torch.empty(QB, cfg.h_q, **bf)
+        self.attn = torch.empty(QB, cfg.h_q, **bf)
+        self.act = torch.empty(QB, cfg.h_ffn, **bf)
+        self.feat_in = torch.zeros(max(self.CR * n_req_max, prefill_rows), n_feat * h, **bf)
         self.tokens = torch.zeros(R, **i32)
         self.pos = torch.zeros(R, **i32)
         self.slot = torch.zeros(R, **i32)
         self.qrow = torch.zeros(R, **i32)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h), (h, n_feat * h)]
         self.partial = torch.empty(_max_partial(shapes, R), **f32)
-        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, self.B, self.kv.n_pages), **f32)
+        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, QB, self.kv.n_pages), **f32)
+        self.attn_splits = 0
         self.logits = torch.empty(dcfg.gamma, cfg.V, **f32)
+        self.logits_b = torch.empty(QB, cfg.V, **f32) if n_req_max > 1 else None
 
-    def _ctx_rows(self, n: int, x_ctx: torch.Tensor, state: torch.Tensor) -> None:
+    def _ctx_rows(self, n: int, x_ctx: torch.Tensor, state: torch.Tensor, feat: torch.Tensor | None = None) -> None:
         """fc + hidden_norm of n feature rows -> x_ctx (context inputs of every drafter layer)."""
         cfg = self.cfg
-        p = ops.gemm_partial(self.feat_in[:n], self.w.fc, out=self.partial)
+        p = ops.gemm_partial(self.feat_in[:n] if feat is None else feat[:n], self.w.fc, out=self.partial)
         ops.residual_rmsnorm(p, None, n, cfg.h, self.w.hidden_norm, cfg.eps, x=x_ctx)
 
-    def prefill_ctx(self, n: int, state: torch.Tensor) -> None:
+    def prefill_ctx(self, n: int, state: torch.Tensor, pt: torch.Tensor | None = None) -> None:
         """Write context K/V for n prompt rows (features in feat_in[:n], pos/slot = 0..n-1 relative to c)."""
         cfg = self.cfg
+        pt = self.kv.page_table if pt is None else pt
         x = self.X[:n]
         self._ctx_rows(n, x, state)
         self.qrow[:n].fill_(-1)
         for li, lw in enumerate(self.w.layers):
             p = ops.gemm_partial(x, lw.qkv, out=self.partial)
             ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, cfg.eps, self.inv_freq, self.pos,
-                         self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, self.kv.page_table,
-                         PAGE, state)
+                         self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, pt, PAGE, state)
 
     def forward(self, state: torch.Tensor) -> torch.Tensor:
         """Draft one block: returns logits [gamma, V] fp32 for future positions c+1..c+gamma."""
@@ -197,24 +220,60 @@ class DrafterModel:
         eps, M = cfg.eps, B + CR
         ops.drafter_rows(state, self.dcfg.gamma, self.mask_token, CR, self.tokens, self.pos, self.slot, self.qrow)
         self._ctx_rows(CR, self.X[B:M], state)
-        xb, resid = self.X[:B], self.resid
+        xb, resid = self.X[:B], self.resid[:B]
         ops.embed_rmsnorm(self.tokens, B, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
         for li, lw in enumerate(w.layers):
             p = ops.gemm_partial(self.X[:M], lw.qkv, out=self.partial)
             ops.qkv_rope(p, M, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
                          self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, self.kv.page_table, PAGE, state)
-            ops.attention(self.q, self.attn, self.kv.buf, self.dcfg.layers, self.kv.n_pages, li, self.kv.page_table,
-                          cfg.n_q, cfg.n_kv, B, 0, B, self.kv.max_slots, state, MODE_FULL, None, 0, self.attn_ws)
-            p = ops.gemm_partial(self.attn, lw.o, out=self.partial)
+            ops.attention(self.q[:B], self.attn[:B], self.kv.buf, self.dcfg.layers, self.kv.n_pages, li,
+                          self.kv.page_table, cfg.n_q, cfg.n_kv, B, 0, B, self.kv.max_slots, state, MODE_FULL, None, 0,
+                          self.attn_ws, n_splits=self.attn_splits)
+            p = ops.gemm_partial(self.attn[:B], lw.o, out=self.partial)
             ops.residual_rmsnorm(p, resid, B, cfg.h, lw.post_norm, eps, x=xb)
             p = ops.gemm_partial(xb, lw.gate_up, out=self.partial)
-            ops.swiglu(p, B, cfg.h_ffn, self.act)
-            p = ops.gemm_partial(self.act, lw.down, out=self.partial)
+            ops.swiglu(p, B, cfg.h_ffn, self.act[:B])
+            p = ops.gemm_partial(self.act[:B], lw.down, out=self.partial)
             nxt = w.layers[li + 1].in_norm if li + 1 < len(w.layers) else w.final_norm
             ops.residual_rmsnorm(p, resid, B, cfg.h, nxt, eps, x=xb)
         p = ops.gemm_partial(self.X[1:B], self.tw.lm_head, out=self.partial)
         _reduce_into(p, self.logits)
         return self.logits
+
+    def forward_batch(self, state: torch.Tensor, n: int, pt: torch.Tensor, req_pages: int,
+                      feat: torch.Tensor | None = None) -> torch.Tensor:
+        """Draft one block for n requests at once (state[r] = request r's 8 state words,
+        pages pt[r*req_pages:], context features feat_in[r*CR:(r+1)*CR]).
+
+        Rows: the n*(gamma+1) block rows first (request-major), then the n*CR context rows.
+        Returns fp32 logits [n*(gamma+1), V]; request r's draft rows are 1..gamma of its block."""
+        cfg, w, B, CR = self.cfg, self.w, self.B, self.CR
+        eps = cfg.eps
+        QB, M = n * B, n * (B + CR)
+        rs = state.stride(0)
+        ops.drafter_rows_batch(state, rs, n, self.dcfg.gamma, self.mask_token, CR, self.tokens, self.pos, self.slot,
+                               self.qrow)
+        self._ctx_rows(n * CR, self.X[QB:M], state, feat)
+        xb, resid = self.X[:QB], self.resid[:QB]
+        ops.embed_rmsnorm(self.tokens, QB, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
+        for li, lw in enumerate(w.layers):
+            p = ops.gemm_partial(self.X[:M], lw.qkv, out=self.partial)
+            ops.qkv_rope_batch(p, M, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
+                               self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, pt, PAGE, state,
+                               B, QB, rs, req_pages * PAGE)
+            ops.attention_batch(self.q[:QB], self.attn[:QB], self.kv.buf, self.dcfg.layers, self.kv.n_pages, li, pt,
+                                req_pages, cfg.n_q, cfg.n_kv, n, B, B, req_pages * PAGE, state, rs, MODE_FULL, None,
+                                0, self.attn_ws, n_splits=self.attn_splits)
+            p = ops.gemm_partial(self.attn[:QB], lw.o, out=self.partial)
+            ops.residual_rmsnorm(p, resid, QB, cfg.h, lw.post_norm, eps, x=xb)
+            p = ops.gemm_partial(xb, lw.gate_up, out=self.partial)
+            ops.swiglu(p, QB, cfg.h_ffn, self.act[:QB])
+            p = ops.gemm_partial(self.act[:QB], lw.down, out=self.partial)
+            nxt = w.layers[li + 1].in_norm if li + 1 < len(w.layers) else w.final_norm
+            ops.residual_rmsnorm(p, resid, QB, cfg.h, nxt, eps, x=xb)
+        p = ops.gemm_partial(xb, self.tw.lm_head, out=self.partial)
+        _reduce_into(p, self.logits_b[:QB])
+        return self.logits_b[:QB]
 
 
 def _reduce_into(p: ops.PartialOut, y: torch.Tensor) -> None:

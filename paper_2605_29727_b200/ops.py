@@ -77,6 +77,16 @@ def attention(q, out, kv, n_layers, n_pages, layer, page_table, n_q, n_kv, s, c,
               _p(anc), mask_words, n_splits, _p(ws), 0 if ws is None else ws.numel() * 4, stream_ptr())
 
 
+def attention_batch(q, out, kv, n_layers, n_pages, layer, page_table, req_pages, n_q, n_kv, n_req, s, keys_after_c,
+                    max_keys, state, req_state, mode, anc=None, mask_words=0, ws=None, n_splits=0):
+    """Batched K3: n_req requests of s rows each (request r: rows [r*s, r*s+s), pages
+    page_table[r*req_pages:], c = state[r*req_state], mask rows anc[(r*s + i)*mask_words:])."""
+    _lib.call("bst_attention_batch", q.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0), kv.data_ptr(),
+              n_layers, n_pages, layer, page_table.data_ptr(), req_pages, n_q, n_kv, n_req, s, keys_after_c,
+              max_keys, _p(state), req_state, 0, mode, _p(anc), mask_words, n_splits, _p(ws),
+              0 if ws is None else ws.numel() * 4, stream_ptr())
+
+
 def embed_rmsnorm(tokens, rows, emb, w, eps, resid, x):
     _lib.call("bst_embed_rmsnorm", tokens.data_ptr(), rows, emb.data_ptr(), emb.shape[1], w.data_ptr(),
               C.c_float(eps), resid.data_ptr(), x.data_ptr(), x.stride(0), stream_ptr())
@@ -95,6 +105,14 @@ def qkv_rope(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos,
               k_norm.data_ptr(), C.c_float(eps), inv_freq.data_ptr(), pos.data_ptr(), slot.data_ptr(), _p(qrow),
               q_out.data_ptr(), q_out.stride(0), kv.data_ptr(), layer_off, page_table.data_ptr(), page_size,
               _p(state), 0, stream_ptr())
+
+
+def qkv_rope_batch(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv,
+                   layer_off, page_table, page_size, state, req_rows, req_span, req_state, req_slots):
+    _lib.call("bst_qkv_rope_batch", p.buf.data_ptr(), C.byref(p.sched), rows, n_q, n_kv, q_norm.data_ptr(),
+              k_norm.data_ptr(), C.c_float(eps), inv_freq.data_ptr(), pos.data_ptr(), slot.data_ptr(), _p(qrow),
+              q_out.data_ptr(), q_out.stride(0), kv.data_ptr(), layer_off, page_table.data_ptr(), page_size,
+              _p(state), 0, req_rows, req_span, req_state, req_slots, stream_ptr())
 
 
 def swiglu(p: PartialOut, rows, ffn, act):
@@ -120,6 +138,11 @@ def verify_rows(state, tree_token, tree_depth, meta, rows, tokens, pos, slot):
 def drafter_rows(state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow):
     _lib.call("bst_drafter_rows", state.data_ptr(), gamma, mask_token, ctx_rows, tokens.data_ptr(), pos.data_ptr(),
               slot.data_ptr(), qrow.data_ptr(), stream_ptr())
+
+
+def drafter_rows_batch(state, req_state, n_req, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow):
+    _lib.call("bst_drafter_rows_batch", state.data_ptr(), req_state, n_req, gamma, mask_token, ctx_rows,
+              tokens.data_ptr(), pos.data_ptr(), slot.data_ptr(), qrow.data_ptr(), stream_ptr())
 
 
 def commit_state(state, accept_meta, committed, max_path, out_tokens, tree_meta=None, surrogate=None, log_i32=None,

@@ -1,0 +1,72 @@
+"""Config 3: the batched multi-request engine must commit exactly the
+token streams each request produces alone in B200Engine — batching only changes
+how rows are grouped into launches, never a request's arithmetic (K4 results are
+row-independent; K3 splits are pinned to 1 in both engines)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _prompts(n, length, V):
+    return [np.random.default_rng(100 + r).integers(0, V - 1, length + 7 * r).tolist() for r in range(n)]
+
+
+def _single_streams(cfg, dcfg, prompts, n_fixed, cycles, max_ctx):
+    from paper_2605_29727_b200.engine.decode import B200Engine
+    eng = B200Engine(cfg, dcfg, max_ctx=max_ctx, seed=0, n_cap=max(64, n_fixed))
+    eng.target.attn_splits = 1
+    eng.drafter.attn_splits = 1
+    eng.set_policy("fixed", n=n_fixed)
+    out = []
+    for p in prompts:
+        eng.reset(p)
+        for _ in range(cycles):
+            eng.cycle()
+        eng.stream.synchronize()  # the verify graph of the last cycle runs on the engine stream
+        # committed stream + per-cycle acceptance surrogate (fp64, from the drafter marginals)
+        out.append((eng.tokens(), eng.log_f64[:cycles].cpu().numpy().copy()))
+    del eng
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("n_req,n_fixed,graphs", [(5, 12, True), (3, 100, False), (16, 4, True)])
+def test_batch_engine_matches_single_requests_tiny(n_req, n_fixed, graphs):
+    from paper_2605_29727_b200.engine.batch import BatchEngine
+    from paper_2605_29727_b200.engine.config import TINY, DrafterConfig
+    dcfg = DrafterConfig(layers=2, gamma=8, logit_scale=4.0)
+    prompts = _prompts(n_req, 150, TINY.V)
+    cycles = 6
+    ref = _single_streams(TINY, dcfg, prompts, n_fixed, cycles, 640)
+    be = BatchEngine(TINY, dcfg, n_req=n_req, n_fixed=n_fixed, max_ctx=640, seed=0)
+    be.set_attention_splits(1)
+    be.use_graphs = graphs
+    be.reset(prompts)
+    for _ in range(cycles):
+        be.cycle()
+    assert (be.cycles() == cycles).all()
+    for r in range(n_req):
+        toks, sur = ref[r]
+        assert be.tokens(r) == toks, f"request {r} diverged"
+        assert len(toks) >= cycles  # every cycle commits at least the bonus token
+        # bit-identical drafts: the batched drafter + K1 + K2 give the same surrogate every cycle
+        assert np.array_equal(be.log_f64[r, :cycles].cpu().numpy(), sur)
+
+
+def test_batch_engine_qwen_shape_two_requests():
+    from paper_2605_29727_b200.engine.batch import BatchEngine
+    from paper_2605_29727_b200.engine.config import QWEN3_8B, DrafterConfig
+    dcfg = DrafterConfig(layers=5, gamma=16, logit_scale=6.0)
+    prompts = _prompts(2, 300, QWEN3_8B.V)
+    ref = _single_streams(QWEN3_8B, dcfg, prompts, 16, 3, 1024)
+    be = BatchEngine(QWEN3_8B, dcfg, n_req=2, n_fixed=16, max_ctx=1024, seed=0)
+    be.set_attention_splits(1)
+    be.reset(prompts)
+    for _ in range(3):
+        be.cycle()
+    for r in range(2):
+        assert be.tokens(r) == ref[r][0]
+        assert np.array_equal(be.log_f64[r, :3].cpu().numpy(), ref[r][1])
