@@ -78,6 +78,7 @@ SIGNATURES = {
     "bst_attention_batch": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _I, _P, _I, _I, _I,
                                  _P, _I, _I, _P, _SZ, _P]),
     "bst_attention_workspace": (_SZ, [_I, _I, _I]),
+    "bst_attention_set_variant": (_I, [_I]),
     "bst_embed_rmsnorm": (_I, [_P, _I, _P, _I, _P, C.c_float, _P, _P, _I64, _P]),
     "bst_residual_rmsnorm": (_I, [_P, _P, _P, _I, _I, _P, C.c_float, _P, _I64, _P, _I64, _P]),
     "bst_qkv_rope": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64, _P, _I64,

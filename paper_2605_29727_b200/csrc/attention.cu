@@ -61,6 +61,7 @@ struct AttnArgs {
   // [req * s, req * s + s), page-table entries [req * req_pages, ...), state words
   // [req * req_state, ...) and ws partials [req][split][s * n_q]
   int n_req, req_pages, req_state;
+  int rows_per_block;      // key-major kernel: query rows per CTA (row blocks balanced over R)
   bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
 };
 
@@ -158,6 +159,7 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 __device__ int g_attn_trace_y = 0;               // debug: which split's CTA (0, y, 0) is traced
+__device__ int g_kt_ablate = 0;                  // debug (profiling only): skip key-major softmax phases
 #ifdef BST_TRACE  // phase tracing (scripts/attn_trace.py); compiled out by default
 #define TRACE(i, k)                                                                                   \
   do {                                                                                                \
@@ -169,7 +171,15 @@ __device__ int g_attn_trace_y = 0;               // debug: which split's CTA (0,
     if (g_attn_trace) atomicMax(reinterpret_cast<unsigned long long*>(g_attn_trace) + 29 * 8 + (k),   \
                                 (unsigned long long)gtimer());                                        \
   } while (0)
+#define TRACE_MIN(k)                                                                                  \
+  do {                                                                                                \
+    if (g_attn_trace) atomicMin(reinterpret_cast<unsigned long long*>(g_attn_trace) + 28 * 8 + (k),   \
+                                (unsigned long long)gtimer());                                        \
+  } while (0)
 #else
+#define TRACE_MIN(k) \
+  do {               \
+  } while (0)
 #define TRACE(i, k) \
   do {              \
   } while (0)
@@ -208,15 +218,15 @@ __device__ __forceinline__ long long gtimer_ns() {
 // 3. merge rows [split * per, split * per + per) of the row block across splits
 //    (fixed split order: deterministic) and store bf16;
 // 4. second arrival; the last one resets the counter to zero for the next launch.
-template <int NT>
-__device__ void split_merge(const AttnArgs& a, const float* stg, int head, int split, int req, int rb, int t) {
+// STAGED = false: the caller has already written its partial rows to ws_o / ws_ml.
+template <int NT, bool STAGED = true>
+__device__ void split_merge(const AttnArgs& a, const float* stg, int head, int split, int req, int rb, int row0, int Rb,
+                            int t) {
   constexpr int NW = NT / 32;
   const int warp = t >> 5, lane = t & 31;
-  const int R = a.group * a.s;
-  const int Rb = min(128, R - rb * 128);
   const int64_t rows_all = (int64_t)a.s * a.n_q;
-  for (int r = warp; r < Rb; r += NW) {
-    const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+  for (int r = warp; STAGED && r < Rb; r += NW) {
+    const int rg = row0 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
     const int64_t gr = ((int64_t)req * a.n_splits + split) * rows_all + (int64_t)tok * a.n_q + qh;
     const float4 v = *reinterpret_cast<const float4*>(stg + r * A_D + ((lane ^ (r & 7)) << 2));
     __stcg(reinterpret_cast<float4*>(a.ws_o + gr * A_D) + lane, v);
@@ -225,6 +235,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   // (generation << 32 | arrivals); the last arrival clears the arrivals and bumps the
   // generation in one release RMW, the others spin (acquire) until the generation moves.
   named_bar_sync(1, NT);
+  if (t == 0) TRACE(30, 2);
   unsigned long long* cnt = a.cnt + ((int64_t)req * a.row_blocks + rb) * a.n_kv + head;
   if (t == 0) {
     const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
@@ -234,12 +245,13 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
     } else {
       const unsigned gen = (unsigned)(old >> 32);
       const long long t0 = gtimer_ns();
-      while ((unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen) {
-        if (gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived: fail, do not hang
+      for (uint32_t it = 1; (unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen; ++it) {
+        if ((it & 1023u) == 0 && gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived: fail, do not hang
       }
     }
   }
   if (t == 0) TRACE_MAX(4);
+  if (t == 0) TRACE(30, 3);
   named_bar_sync(1, NT);
   // thread item = (row, DI-dim slice); the loads of up to 20 splits are issued at once
   // (DI = 8 for the 192-thread kernel, 4 for the 384-thread one: register budget)
@@ -248,7 +260,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   const int r0 = split * per, r1 = min(r0 + per, Rb);
   for (int it = t; it < (r1 - r0) * IPR; it += NT) {
     const int r = r0 + it / IPR, d0 = (it % IPR) * DI;
-    const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+    const int rg = row0 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
     const int64_t base = (int64_t)req * a.n_splits * rows_all + (int64_t)tok * a.n_q + qh;
     float M = -INFINITY, L = 0.f, acc[DI];
 #pragma unroll
@@ -291,6 +303,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
       }
       M = Mn;
     }
+    if (t == 0) TRACE(30, 4);
     const float inv = L > 0.f ? 1.f / L : 0.f;
     __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + d0;
     if constexpr (DI == 8) {
@@ -806,7 +819,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       named_bar_sync(1, 128);
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
-      split_merge<128>(a, stg, head, split, req, rb, threadIdx.x - 64);
+      split_merge<128>(a, stg, head, split, req, rb, rb * 128, min(128, R - rb * 128), threadIdx.x - 64);
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
@@ -1407,7 +1420,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       named_bar_sync(1, 256);
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
-      split_merge<256>(a, stg, head, split, req, rb, threadIdx.x - 64);
+      split_merge<256>(a, stg, head, split, req, rb, rb * 128, min(128, R - rb * 128), threadIdx.x - 64);
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
@@ -1432,6 +1445,684 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   if (threadIdx.x == 0) TRACE(31, 0);
   sm100::tc_fence_before();
   __syncthreads();
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc(tmem, 512);
+  }
+}
+
+// ===========================================================================
+// Key-major tcgen05 variant (default): S^T = K Q^T, so a TMEM lane holds one KEY and
+// its columns hold every query row of the CTA.  Decode-time trees have few rows
+// (GQA group x tree tokens, e.g. 4 x 17 = 68), which in the row-major kernels above
+// leave most TMEM lanes / softmax threads idle and serialise 64 exponentials per
+// thread per tile; here all 128 lanes (4 warps, one per SM sub-partition) are busy
+// for any row count and each thread does one exponential per row.
+//   * 128-key tiles (two 64-slot pages), K and V in separate 2-stage TMA rings.
+//   * S^T: M = 128 keys, N = NP (rows rounded up to 16), K = 128 dims; double buffer.
+//   * softmax against a per-row REFERENCE maximum (smem), not a per-tile max: the
+//     fast path is p = 2^(s*scale - ref) with no cross-lane reduction; one barrier
+//     with an OR reduction per tile detects any row whose score exceeds its reference
+//     by > 2^KT_OVF, and only then (always on a row's first visible tile) the slow path
+//     reduces per-row tile maxima (redux.sync.max.f32 + 4-warp smem), raises the
+//     references, rescales those rows of O/l in TMEM and recomputes P.  Any reference
+//     within the headroom gives the same softmax (the factor cancels in O / l).
+//   * P^T is written key-major (MN-major A operand): [row half][128 keys][128 B].
+//   * O += P V (A and B MN-major) and l += P 1 (a second MMA against a ones matrix),
+//     so the row sums use the same bf16 P as the numerator and need no shuffles.
+// warp 0: K TMA, warp 1: TMEM owner + S issuer, warps 2-9: softmax (warp w owns TMEM
+// lanes 32 (w % 4) ..; two warps per SM sub-partition split the rows), warp 10: V TMA,
+// warp 11: PV issuer.
+// ===========================================================================
+constexpr int KT_SM_WARPS = 8;                     // softmax warps 2 .. 9
+constexpr int KT_VTMA_WARP = 10, KT_PV_WARP = 11;
+constexpr int KT_THREADS = 384;
+constexpr int KT_KEYS = 128;
+constexpr int KT_TILE_BYTES = KT_KEYS * A_D * 2;  // 32 KiB: K or V of one tile
+constexpr int KT_KS = 2, KT_VS = 2;
+constexpr int KT_P_BYTES = 128 * KT_KEYS * 2;     // one P^T buffer: [2 row halves][128 keys][128 B]
+constexpr int KT_ONES_BYTES = 16 * 128;           // [16][64 keys] bf16 ones (every K step reads the same block)
+// per row count: Q [2 dim halves][NP rows][128 B]; P^T double-buffered while it fits
+__host__ __device__ constexpr int kt_pbufs(int nch) { return nch <= 6 ? 2 : 1; }
+__host__ __device__ constexpr int kt_smem(int nch) {
+  return nch * 16 * 256 + kt_pbufs(nch) * KT_P_BYTES + KT_ONES_BYTES + 4 * KT_TILE_BYTES + 1024;
+}
+constexpr int KT_O_COL = 256, KT_L_COL = 384;     // TMEM: S 0-255 (two buffers), O, l
+constexpr float KT_OVF = 48.f;                     // log2 headroom above the reference
+
+__device__ __forceinline__ float redux_max(float v) {
+  float r;
+  asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+  return r;
+}
+// named barrier over `n` threads returning whether any thread's predicate was true
+__device__ __forceinline__ bool bar_or(int id, int n, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred q, o;\n\t"
+      "setp.ne.u32 q, %1, 0;\n\t"
+      "barrier.red.or.pred o, %2, %3, q;\n\t"
+      "selp.u32 %0, 1, 0, o;\n\t}"
+      : "=r"(r)
+      : "r"((uint32_t)pred), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float r;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+
+// Global split merge of the key-major kernel.  Partials live in a head-major, dim-chunk
+// major layout so both the writers (one query row per thread) and the readers are
+// coalesced: ws_o float4 index ((req, split, head) * 32 + d4) * R + row, ws_ml float2
+// index (req, split, head) * R + row (row = the GQA row index inside the head).  The
+// arrival protocol is split_merge's generation counter.
+__device__ __forceinline__ int64_t kt_ws_base(const AttnArgs& a, int req, int split, int head) {
+  return ((int64_t)req * a.n_splits + split) * a.n_kv + head;
+}
+__device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req, int rb, int row0, int Rb, int t) {
+  const int R = a.group * a.s;
+  named_bar_sync(1, 256);
+  unsigned long long* cnt = a.cnt + ((int64_t)req * a.row_blocks + rb) * a.n_kv + head;
+  if (t == 0) {
+    const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
+    TRACE_MAX(3);
+    if ((unsigned)(old & 0xffffffffu) == (unsigned)a.n_splits - 1u) {
+      red_add_release_gpu(cnt, (1ull << 32) - (unsigned long long)a.n_splits);
+    } else {
+      const unsigned gen = (unsigned)(old >> 32);
+      const long long t0 = gtimer_ns();
+      for (uint32_t it = 1; (unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen; ++it) {
+        if ((it & 1023u) == 0 && gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived
+      }
+    }
+  }
+  if (t == 0) TRACE_MAX(4);
+  named_bar_sync(1, 256);
+  const int ns = a.n_splits;
+  const int per = (Rb + ns - 1) / ns, r0 = split * per, nr = min(r0 + per, Rb) - r0;
+  const float2* ml_all = reinterpret_cast<const float2*>(a.ws_ml);
+  const float4* o_all = reinterpret_cast<const float4*>(a.ws_o);
+  for (int it = t; it < nr * 32; it += 256) {
+    const int rr = row0 + r0 + it % nr, d4 = it / nr;  // lanes walk rows: coalesced
+    float M = -INFINITY, L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j0 = 0; j0 < ns; j0 += 16) {
+      float2 ml[16];
+      float4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (j0 + u < ns) {
+          const int64_t b = kt_ws_base(a, req, j0 + u, head);
+          ml[u] = __ldcg(ml_all + b * R + rr);
+          v[u] = __ldcg(o_all + (b * 32 + d4) * R + rr);
+        } else {
+          ml[u] = make_float2(-INFINITY, 0.f);
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float Mn = M;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) Mn = fmaxf(Mn, ml[u].x);
+      if (Mn == -INFINITY) continue;
+      const float sc = M == -INFINITY ? 0.f : ex2(M - Mn);
+      L *= sc;
+      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float w = ml[u].x == -INFINITY ? 0.f : ex2(ml[u].x - Mn);
+        L += w * ml[u].y;
+        acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
+      }
+      M = Mn;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const int tok = rr / a.group, qh = head * a.group + rr % a.group;
+    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
+    *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  }
+}
+
+// ---- distributed shared memory (thread-block clusters)
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// p = 2^(s * scale - ref) for the NP rows of this thread's key (all chunks loaded from
+// TMEM with one wait); masked entries -> 0.  Returns the largest exponent (overflow
+// check).  Unmasked tiles run every fourth exponential on the FMA pipe (ex2_poly).
+template <int NCH, bool MASKED, int NA>
+__device__ __forceinline__ float kt_tile(uint32_t taddr, const float* nmref, float scale, const uint32_t (&vis)[NA],
+                                         uint32_t (&pk)[NA][8]) {
+  static_assert(NCH <= NA, "chunk count exceeds the register arrays");
+  uint32_t r[NCH > 0 ? NCH : 1][16];
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) sm100::tmem_ld16_nw(taddr + 16 * c, r[c]);
+  sm100::tmem_ld_wait();
+  float em = -INFINITY;
+#pragma unroll
+  for (int c = 0; c < NCH; ++c) {
+    const float4* nm4 = reinterpret_cast<const float4*>(nmref + 16 * c);
+    float d[16];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 v = nm4[q];
+      d[4 * q + 0] = fmaf(__uint_as_float(r[c][4 * q + 0]), scale, v.x);
+      d[4 * q + 1] = fmaf(__uint_as_float(r[c][4 * q + 1]), scale, v.y);
+      d[4 * q + 2] = fmaf(__uint_as_float(r[c][4 * q + 2]), scale, v.z);
+      d[4 * q + 3] = fmaf(__uint_as_float(r[c][4 * q + 3]), scale, v.w);
+    }
+    if (MASKED) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e)
+        if (!((vis[c] >> e) & 1u)) d[e] = -INFINITY;
+    }
+    float m = fmax3(d[0], d[1], d[2]);
+#pragma unroll
+    for (int e = 3; e < 15; e += 2) m = fmax3(m, d[e], d[e + 1]);
+    em = fmax3(em, m, d[15]);
+#pragma unroll
+    for (int e = 0; e < 16; e += 2) {
+      const float p0 = ex2(d[e]);
+      const float p1 = (!MASKED && (e & 2)) ? ex2_poly(d[e + 1]) : ex2(d[e + 1]);
+      pk[c][e >> 1] = pack_bf16(p0, p1);
+    }
+  }
+  return em;
+}
+
+template <int NCH>
+__global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
+  constexpr int NP = NCH * 16;
+  constexpr int C0 = (NCH + 1) / 2, C1 = NCH / 2;  // row chunks of softmax half 0 / half 1
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t fullK[KT_KS], emptyK[KT_KS], fullV[KT_VS], emptyV[KT_VS], s_full[2], s_free[2],
+      p_full[2], o_done[2], q_ready;
+  __shared__ uint32_t tmem_sh;
+  __shared__ __align__(16) float nmref[NP];  // -(reference max), log2 domain; +inf: row has seen no key yet
+  __shared__ float alpha_sh[128];
+  __shared__ float wmax[4][NP];
+  __shared__ uint32_t colm[KT_KEYS][4];  // tree tile: bit r of colm[k][r / 32] = row r sees key k
+  __shared__ float2 ml_sh[128];          // cluster merge: (reference max, row sum) of this CTA's rows
+  sm100::grid_dep_launch();
+  if (threadIdx.x == 0) TRACE(31, 1);
+  if (threadIdx.x == 0) TRACE_MIN(0);
+  if (threadIdx.x == 0) TRACE_MAX(5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
+  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
+  constexpr int PB = kt_pbufs(NCH);  // P^T buffers: tile i uses buffer i % PB, barriers p_full / o_done[i % PB]
+  const uint32_t sQ = base, sP = sQ + NP * 256, sOnes = sP + PB * KT_P_BYTES, sK = sOnes + KT_ONES_BYTES;
+  const uint32_t sV = sK + KT_KS * KT_TILE_BYTES;
+  uint8_t* gQ = smem;
+  uint8_t* gP = smem + NP * 256;
+  uint8_t* gOnes = gP + PB * KT_P_BYTES;
+  uint8_t* gK = gOnes + KT_ONES_BYTES;  // K ring, then V ring; reused as the merge staging buffer
+  uint8_t* gV = gK + KT_KS * KT_TILE_BYTES;
+
+  const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
+  const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
+  const int n_keys = c_ctx + a.keys_after_c;
+  const int R = a.group * a.s;
+  const int row0 = rb * a.rows_per_block;
+  const int Rb = min(a.rows_per_block, R - row0);
+  int page0, n_pages;
+  split_pages(a, n_keys, split, page0, n_pages);
+  const int n_tiles = (n_pages + 1) >> 1;
+
+  if (threadIdx.x == 0) {
+    sm100::prefetch_tmap(&tmKV);
+    for (int i = 0; i < KT_KS; ++i) { sm100::mbar_init(&fullK[i], 1); sm100::mbar_init(&emptyK[i], 1); }
+    for (int i = 0; i < KT_VS; ++i) { sm100::mbar_init(&fullV[i], 1); sm100::mbar_init(&emptyV[i], 1); }
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&s_free[i], KT_SM_WARPS); }
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&p_full[i], KT_SM_WARPS); sm100::mbar_init(&o_done[i], 1); }
+    sm100::mbar_init(&q_ready, KT_SM_WARPS);
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 512);
+  sm100::tc_fence_before();
+  __syncthreads();
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_sh;
+
+  if (warp == 0 || warp == KT_VTMA_WARP) {
+    if (lane == 0) {
+      const bool isK = warp == 0;
+      if (isK)
+        issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
+                       gridDim.x * gridDim.y * gridDim.z);
+      uint64_t* fb = isK ? fullK : fullV;
+      uint64_t* eb = isK ? emptyK : emptyV;
+      uint8_t* ring = isK ? gK : gV;
+      // PDL: pages entirely below c hold committed K/V the previous kernel does not touch
+      const int safe_pages = max(min(pdl_safe_slots(a, c_ctx) / A_PAGE - page0, n_pages), 0);
+      const int64_t pt = (int64_t)req * a.req_pages + page0;
+      bool waited = false;
+      for (int i = 0; i < n_tiles; ++i) {
+        const int st = i & 1;
+        if (i >= 2) sm100::mbar_wait(&eb[st], ((i >> 1) & 1) ^ 1);
+        // the second page of an odd split's last tile re-loads the first (finite data; its keys are masked)
+        const int pA = 2 * i, pB = min(2 * i + 1, n_pages - 1);
+        if (!waited && (pB >= safe_pages || i >= 2)) {
+          sm100::grid_dep_wait();
+          waited = true;
+        }
+        const int kv = isK ? 0 : 1;
+        const int64_t rowA = ((((int64_t)a.layer * a.n_pages_total + a.page_table[pt + pA]) * 2 + kv) * a.n_kv + head) * A_PAGE;
+        const int64_t rowB = ((((int64_t)a.layer * a.n_pages_total + a.page_table[pt + pB]) * 2 + kv) * a.n_kv + head) * A_PAGE;
+        uint8_t* dst = ring + st * KT_TILE_BYTES;
+        sm100::mbar_expect_tx(&fb[st], KT_TILE_BYTES);
+        sm100::tma_load_2d(dst, &tmKV, &fb[st], 0, (int)rowA);
+        sm100::tma_load_2d(dst + 8192, &tmKV, &fb[st], 0, (int)rowB);
+        sm100::tma_load_2d(dst + 16384, &tmKV, &fb[st], 64, (int)rowA);
+        sm100::tma_load_2d(dst + 24576, &tmKV, &fb[st], 64, (int)rowB);
+        if (isK) TRACE(i, 0);
+      }
+    }
+  } else if (warp == 1) {
+    const uint32_t idS = sm100::idesc_bf16(128, NP);
+    sm100::mbar_wait(&q_ready, 0);
+    for (int i = 0; i < n_tiles; ++i) {
+      const int st = i & 1, b = i & 1;
+      sm100::mbar_wait(&fullK[st], (i >> 1) & 1);
+      if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
+      if (lane == 0) TRACE(i, 1);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t kb = sK + st * KT_TILE_BYTES;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint64_t ad = sm100::desc_k_sw128(kb + (j >> 2) * 16384 + (j & 3) * 32);
+          const uint64_t bd = sm100::desc_k_sw128(sQ + (j >> 2) * (NP * 128) + (j & 3) * 32);
+          sm100::umma_f16(tmem + b * 128, ad, bd, idS, j > 0 ? 1u : 0u);
+        }
+        sm100::umma_commit(&s_full[b]);
+        sm100::umma_commit(&emptyK[st]);
+      }
+      __syncwarp();
+    }
+  } else if (warp == KT_PV_WARP) {
+    const uint32_t idO = sm100::idesc_bf16_abmn(128, A_D);
+    const uint32_t idL = sm100::idesc_bf16_amn(128, 16);
+    for (int j = 0; j < n_tiles; ++j) {
+      const int st = j & 1;
+      sm100::mbar_wait(&p_full[j % PB], (j / PB) & 1);
+      sm100::mbar_wait(&fullV[st], (j >> 1) & 1);
+      if (lane == 0) TRACE(j, 2);
+      sm100::tc_fence_after();
+      if (sm100::elect_one()) {
+        const uint32_t vb = sV + st * KT_TILE_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = sm100::desc_mn_sw128(sP + (j % PB) * KT_P_BYTES + kk * 2048, 16384);
+          const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, 16384);
+          sm100::umma_f16(tmem + KT_O_COL, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t ad = sm100::desc_mn_sw128(sP + (j % PB) * KT_P_BYTES + kk * 2048, 16384);
+          const uint64_t bd = sm100::desc_k_sw128(sOnes + (kk & 3) * 32);
+          sm100::umma_f16(tmem + KT_L_COL, ad, bd, idL, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        sm100::umma_commit(&o_done[j % PB]);
+        sm100::umma_commit(&emptyV[st]);
+      }
+      __syncwarp();
+    }
+  } else {
+    // ---------------- softmax: warps 2 .. 9.  Warp w owns TMEM lanes 32 (w % 4) .. (key kk of
+    // each S^T tile, query row kk of O); half h = (w - 2) / 4 takes row chunks
+    // [h C0, h C0 + (h ? C1 : C0)) of the tile and O columns / dims [64 h, 64 h + 64).
+    const int t = threadIdx.x - 64;  // 0 .. 255
+    const int quad = warp & 3, h = (warp - 2) >> 2;
+    const int kk = quad * 32 + lane;
+    const int c0 = h ? C0 : 0;
+    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+    const float scale = a.scale_log2;
+    if (t < NP) nmref[t] = t < Rb ? INFINITY : 0.f;  // padding rows (zero Q): p = 1, never overflow
+    sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
+    if (t == 0) TRACE(31, 2);
+    {  // stage query rows (K-major, 128B swizzle): thread t stages dim half t / 128 of row t % 128
+      const int row = t & 127, hq = t >> 7;
+      if (row < NP) {
+        const bool valid = row < Rb;
+        const int rg = row0 + (valid ? row : 0);
+        const int tok = rg / a.group, qh = head * a.group + rg % a.group;
+        const int4* src =
+            reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * hq;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
+          *reinterpret_cast<int4*>(gQ + hq * (NP * 128) + row * 128 + ((q ^ (row & 7)) << 4)) = v;
+        }
+      }
+    }
+    if (t < KT_ONES_BYTES / 16)
+      *reinterpret_cast<uint4*>(gOnes + t * 16) = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+    sm100::fence_async_shared();
+    __syncwarp();
+    if (lane == 0) sm100::mbar_arrive(&q_ready);
+    named_bar_sync(2, 256);  // nmref initialised
+    if (t == 0) TRACE(31, 3);
+
+    const uint32_t* anc = a.mode == 0 ? a.anc + (int64_t)req * a.s * a.mask_words : nullptr;
+    const int my_tok = (row0 + min(t & 127, Rb - 1)) / a.group;
+    const int abl = g_kt_ablate;
+    for (int i = 0; i < n_tiles; ++i) {
+      const int b = i & 1;
+      const int tslot0 = (page0 + 2 * i) * A_PAGE;
+      const int slot = tslot0 + kk;
+      // key class: 0 visible to no row, 1 to every row, 2 per row (tree / causal part)
+      int cls;
+      if (2 * i + (kk >> 6) >= n_pages || slot >= n_keys) cls = 0;
+      else if (a.mode == 2 || slot < c_ctx) cls = 1;
+      else cls = 2;
+      if (a.mode == 0 && tslot0 + KT_KEYS > c_ctx && tslot0 < n_keys) {
+        // tree keys in this tile: column masks by ballots; thread t evaluates row t % 128
+        // for the keys of parity t / 128
+        const int k_lo = max(c_ctx - tslot0, 0), k_hi = min(n_keys - tslot0, KT_KEYS);
+        const int rr = t & 127;
+        int wi = -1;
+        uint32_t wv = 0;
+        for (int k2 = k_lo + h; k2 < k_hi; k2 += 2) {
+          const int j = tslot0 + k2 - c_ctx;
+          bool bit = false;
+          if (rr < Rb) {
+            if ((j >> 5) != wi) {
+              wi = j >> 5;
+              wv = anc[(int64_t)my_tok * a.mask_words + wi];
+            }
+            bit = (wv >> (j & 31)) & 1u;
+          }
+          const uint32_t bal = __ballot_sync(0xffffffffu, bit);
+          if (lane == 0) colm[k2][rr >> 5] = bal;
+        }
+        named_bar_sync(2, 256);
+      }
+      uint32_t vis[C0];
+#pragma unroll
+      for (int u = 0; u < C0; ++u) {
+        const int c = c0 + u;
+        uint32_t v;
+        if (cls == 2) {
+          if (a.mode == 1) {  // causal: rows whose token is >= the key's tree index
+            const int rmin = max((slot - c_ctx) * a.group - row0, 0), lo = 16 * c;
+            v = rmin <= lo ? 0xFFFFu : (rmin >= lo + 16 ? 0u : ((0xFFFFu << (rmin - lo)) & 0xFFFFu));
+          } else {
+            v = (colm[kk][c >> 1] >> (16 * (c & 1))) & 0xFFFFu;
+          }
+        } else {
+          v = cls == 1 ? 0xFFFFu : 0u;
+        }
+        vis[u] = v;
+      }
+      const bool masked = !__all_sync(0xffffffffu, cls == 1);
+      sm100::mbar_wait(&s_full[b], (i >> 1) & 1);
+      if (t == 0) TRACE(i, 3);
+      sm100::tc_fence_after();
+      const uint32_t sb = lane_base + b * 128 + 16 * c0;
+      const float* nmr = nmref + 16 * c0;
+      uint32_t pk[C0][8];
+      float emax = -INFINITY;
+      bool need;
+      if (i == 0) {
+        // first tile: references = the scores of key 0 when every row sees it (any visible
+        // score is <= the row max, so only the overflow side needs checking)
+        const bool cheap = n_pages > 0 && (a.mode == 2 ? tslot0 < n_keys : tslot0 < c_ctx);
+        if (cheap) {
+          if (quad == 0) {
+            uint32_t r0[C0][16];
+            if (h == 0) {
+#pragma unroll
+              for (int u = 0; u < C0; ++u) sm100::tmem_ld16_nw(sb + 16 * u, r0[u]);
+            } else {
+#pragma unroll
+              for (int u = 0; u < C1; ++u) sm100::tmem_ld16_nw(sb + 16 * u, r0[u]);
+            }
+            sm100::tmem_ld_wait();
+            if (lane == 0) {
+              const int nu = h ? C1 : C0;
+#pragma unroll
+              for (int u = 0; u < C0; ++u)
+#pragma unroll
+                for (int e = 0; e < 16; ++e)
+                  if (u < nu && 16 * (c0 + u) + e < Rb) nmref[16 * (c0 + u) + e] = -(__uint_as_float(r0[u][e]) * scale);
+            }
+          }
+          named_bar_sync(2, 256);
+        }
+        if (cheap) {
+          if (h == 0) emax = masked ? kt_tile<C0, true>(sb, nmr, scale, vis, pk) : kt_tile<C0, false>(sb, nmr, scale, vis, pk);
+          else if (C1 > 0) emax = masked ? kt_tile<C1, true>(sb, nmr, scale, vis, pk) : kt_tile<C1, false>(sb, nmr, scale, vis, pk);
+        }
+        need = !cheap || emax > KT_OVF;
+      } else if (abl & 1) {
+#pragma unroll
+        for (int u = 0; u < C0; ++u)
+#pragma unroll
+          for (int e = 0; e < 8; ++e) pk[u][e] = 0u;
+        need = false;
+      } else {
+        if (h == 0) emax = masked ? kt_tile<C0, true>(sb, nmr, scale, vis, pk) : kt_tile<C0, false>(sb, nmr, scale, vis, pk);
+        else if (C1 > 0) emax = masked ? kt_tile<C1, true>(sb, nmr, scale, vis, pk) : kt_tile<C1, false>(sb, nmr, scale, vis, pk);
+        need = emax > KT_OVF;
+      }
+      if (t == 0) TRACE(i, 4);
+      if ((abl & 4) ? need : bar_or(3, 256, need)) {
+        // slow path: per-row maxima of this tile -> raise the references -> rescale O, l
+        const int nu = h ? C1 : C0;
+#pragma unroll
+        for (int u = 0; u < C0; ++u) {
+          if (u < nu) {
+            uint32_t r[16];
+            sm100::tmem_ld16_nw(sb + 16 * u, r);
+            sm100::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const float x = ((vis[u] >> e) & 1u) ? __uint_as_float(r[e]) * scale : -INFINITY;
+              const float wm = redux_max(x);
+              if (lane == e + (u & 1) * 16) wmax[quad][16 * (c0 + u) + e] = wm;
+            }
+          }
+        }
+        named_bar_sync(2, 256);
+        if (t < 128) {
+          if (t < Rb) {
+            const float tm = fmaxf(fmaxf(wmax[0][t], wmax[1][t]), fmaxf(wmax[2][t], wmax[3][t]));
+            const float old = -nmref[t];
+            float al = 1.f;
+            if (tm > old) {
+              al = old == -INFINITY ? 0.f : ex2(old - tm);
+              nmref[t] = -tm;
+            }
+            alpha_sh[t] = al;
+          } else {
+            alpha_sh[t] = 1.f;
+          }
+        }
+        named_bar_sync(2, 256);
+        if (i >= 1) {
+          sm100::mbar_wait(&o_done[(i - 1) % PB], ((i - 1) / PB) & 1);  // O, l hold PV(0 .. i-1)
+          sm100::tc_fence_after();
+          const float f = alpha_sh[kk];
+          if (__any_sync(0xffffffffu, f != 1.f)) {  // O columns 0-79 (half 0), 80-143 (half 1, incl. l)
+#pragma unroll 1
+            for (int cc = 5 * h; cc < (h ? 9 : 5); ++cc) {
+              float ov[16];
+              sm100::tmem_ld16(lane_base + KT_O_COL + 16 * cc, ov);
+#pragma unroll
+              for (int e = 0; e < 16; ++e) ov[e] *= f;
+              sm100::tmem_st16(lane_base + KT_O_COL + 16 * cc, ov);
+            }
+            sm100::tmem_st_wait();
+          }
+        }
+        if (h == 0) kt_tile<C0, true>(sb, nmr, scale, vis, pk);
+        else if (C1 > 0) kt_tile<C1, true>(sb, nmr, scale, vis, pk);
+        if (t == 0) TRACE(i, 7);
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&s_free[b]);
+      if (i >= PB) sm100::mbar_wait(&o_done[i % PB], ((i - PB) / PB) & 1);  // PV(i-PB) has read this P buffer
+      if (t == 0) TRACE(i, 5);
+      // my key's column of P^T: rows 16c .. 16c+15 are 16-byte chunks 2c, 2c+1
+      if (!(abl & 2)) {
+        const int nu = h ? C1 : C0;
+#pragma unroll
+        for (int u = 0; u < C0; ++u) {
+          if (u < nu) {
+#pragma unroll
+            for (int hh = 0; hh < 2; ++hh) {
+              const int q = 2 * (c0 + u) + hh;
+              *reinterpret_cast<uint4*>(gP + (i % PB) * KT_P_BYTES + (q >> 3) * 16384 + kk * 128 + (((q & 7) ^ (kk & 7)) << 4)) =
+                  make_uint4(pk[u][4 * hh], pk[u][4 * hh + 1], pk[u][4 * hh + 2], pk[u][4 * hh + 3]);
+            }
+          }
+        }
+      }
+      sm100::fence_async_shared();
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive(&p_full[i % PB]);
+      if (t == 0) TRACE(i, 6);
+    }
+    // ---------------- epilogue: thread (h, kk) owns dims [64 h, 64 h + 64) of query row kk
+    float o[64];
+    float L = 0.f;
+    if (n_tiles > 0) {
+      sm100::mbar_wait(&o_done[(n_tiles - 1) % PB], ((n_tiles - 1) / PB) & 1);
+      if (t == 0) TRACE(31, 4);
+      sm100::tc_fence_after();
+#pragma unroll
+      for (int cc = 0; cc < 4; ++cc) {
+        float t16[16];
+        sm100::tmem_ld16(lane_base + KT_O_COL + 64 * h + 16 * cc, t16);
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[16 * cc + e] = t16[e];
+      }
+      float lv[16];
+      sm100::tmem_ld16(lane_base + KT_L_COL, lv);
+      L = lv[0];
+    } else {
+#pragma unroll
+      for (int e = 0; e < 64; ++e) o[e] = 0.f;
+    }
+    const bool valid = kk < Rb;
+    const float m = valid ? -nmref[kk] : -INFINITY;
+    const int rg = row0 + (valid ? kk : 0);
+    const int tok = rg / a.group, qh = head * a.group + rg % a.group;
+    if (a.n_splits > 1 && a.merge == 2) {
+      // cluster merge: stage the partial rows in this CTA's shared memory (the idle K ring)
+      float* stg = reinterpret_cast<float*>(gK);
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        *reinterpret_cast<float4*>(stg + kk * A_D + (((16 * h + q) ^ (kk & 7)) << 2)) =
+            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      if (h == 0) ml_sh[kk] = make_float2(m, L);
+    } else if (a.n_splits > 1 && a.merge) {
+      if (valid) {  // unnormalised partial straight to the (L2-resident) workspace, coalesced over rows
+        const int Rt = a.group * a.s, rr = row0 + kk;
+        const int64_t bse = kt_ws_base(a, req, split, head);
+        float4* op = reinterpret_cast<float4*>(a.ws_o) + (bse * 32 + 16 * h) * Rt + rr;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) __stcg(op + (int64_t)q * Rt, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+        if (h == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + bse * Rt + rr, make_float2(m, L));
+      }
+      if (t == 0) TRACE(31, 5);
+      if (t == 0) TRACE_MAX(1);
+      kt_global_merge(a, head, split, req, rb, row0, Rb, t);
+    } else if (valid) {
+      if (a.n_splits == 1) {
+        const float inv = L > 0.f ? 1.f / L : 0.f;
+        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * h);
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                             pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
+      } else {
+        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
+        float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D + 64 * h);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+        if (h == 0) {
+          a.ws_ml[r * 2 + 0] = m;
+          a.ws_ml[r * 2 + 1] = L;
+        }
+      }
+    }
+  }
+  if (a.n_splits > 1 && a.merge == 2) {
+    // the splits of this (head, row block) form one cluster (rank = split): every CTA
+    // merges rows [rank * per, rank * per + per) from all ranks' staged partials over
+    // DSMEM, in rank order (deterministic); a second cluster barrier keeps the staging
+    // alive until every remote read is done
+    if (threadIdx.x == 64) TRACE_MAX(1);
+    cluster_sync_all();
+    if (threadIdx.x == 64) TRACE_MAX(3);
+    if (warp >= 2 && warp < 2 + KT_SM_WARPS) {
+      const int t = threadIdx.x - 64, ns = a.n_splits;
+      const int per = (Rb + ns - 1) / ns, r0 = split * per, r1 = min(r0 + per, Rb);
+      const uint32_t stg_u = sK, ml_u = sm100::smem_u32(ml_sh);
+      for (int it = t; it < (r1 - r0) * 32; it += 256) {
+        const int r = r0 + (it >> 5), cq = it & 31;
+        const uint32_t off = (uint32_t)(r * A_D + ((cq ^ (r & 7)) << 2)) * 4u;
+        float2 ml[8];
+        float4 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {  // every rank's loads in flight at once
+          if (q < ns) {
+            ml[q] = ld_dsmem_f2(mapa_shared(ml_u + r * 8, q));
+            v[q] = ld_dsmem_f4(mapa_shared(stg_u + off, q));
+          }
+        }
+        float M = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < ns) M = fmaxf(M, ml[q].x);
+        float Lsum = 0.f;
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          if (q < ns && ml[q].x != -INFINITY) {
+            const float w = ex2(ml[q].x - M);
+            Lsum += w * ml[q].y;
+            acc.x += w * v[q].x; acc.y += w * v[q].y; acc.z += w * v[q].z; acc.w += w * v[q].w;
+          }
+        }
+        const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+        const int rg = row0 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+        __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * cq;
+        *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+      }
+    }
+    if (threadIdx.x == 64) TRACE_MAX(4);
+    cluster_sync_all();
+  }
+  if (threadIdx.x == 64) TRACE_MAX(2);
+  if (threadIdx.x == 64) TRACE(31, 6);
+  sm100::tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) TRACE(31, 0);
+  if (threadIdx.x == 0) TRACE_MAX(6);
+  if (threadIdx.x == 0) TRACE_MIN(1);
   if (warp == 1) {
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, 512);
@@ -1491,6 +2182,40 @@ __global__ void attn_combine_kernel(AttnArgs a) {
 }  // namespace bst
 
 namespace bst {
+// resident clusters of `cs` key-major CTAs (cudaOccupancyMaxActiveClusters)
+static int kt_cluster_occupancy(int nch, int cs) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(8, cs, 1);
+  cfg.blockDim = dim3(KT_THREADS);
+  cfg.dynamicSmemBytes = kt_smem(nch);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = cs;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  cudaError_t e = cudaSuccess;
+  switch (nch) {
+    case 1: cudaFuncSetAttribute(attn_kt_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(1)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<1>, &cfg); break;
+    case 2: cudaFuncSetAttribute(attn_kt_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(2)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<2>, &cfg); break;
+    case 3: cudaFuncSetAttribute(attn_kt_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(3)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<3>, &cfg); break;
+    case 4: cudaFuncSetAttribute(attn_kt_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(4)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<4>, &cfg); break;
+    case 5: cudaFuncSetAttribute(attn_kt_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(5)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<5>, &cfg); break;
+    case 6: cudaFuncSetAttribute(attn_kt_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(6)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<6>, &cfg); break;
+    case 7: cudaFuncSetAttribute(attn_kt_kernel<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(7)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<7>, &cfg); break;
+    default: cudaFuncSetAttribute(attn_kt_kernel<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(8)); e = cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<8>, &cfg); break;
+  }
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+static int g_attn_variant = -1;  // -1: from BST_ATTN on first use; bst_attention_set_variant overrides
+
 static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
                           int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
                           int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
@@ -1510,6 +2235,7 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   const int pages = (max_keys + A_PAGE - 1) / A_PAGE;
   BST_REQUIRE(pages <= n_pages_total, "context exceeds the page table");
   if (n_req > 1) BST_REQUIRE(req_pages >= pages, "request page slice (%d) smaller than the context (%d pages)", req_pages, pages);
+  const int n_splits_arg = n_splits;
   if (n_splits <= 0) {
     // one wave of CTAs: per-tile work (GQA group x tokens rows against 64 keys)
     // dominates a CTA's fixed cost, so spread the pages over every SM
@@ -1558,20 +2284,144 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   a.n_req = n_req;
   a.req_pages = req_pages;
   a.req_state = req_state;
+  a.rows_per_block = 128;
   a.pf = take_prefetch();
-  cudaStream_t st = as_stream(stream);
-  static int variant = -1;
+  int& variant = g_attn_variant;
   if (variant < 0) {
     const char* e = getenv("BST_ATTN");
-    // default: tcgen05 64-key kernel (attn_tc_kernel).  BST_ATTN=mma selects the
-    // mma.sync kernel, BST_ATTN=fa the 128-key two-warpgroup kernel (experimental:
-    // fails the engine's greedy-preservation test, under investigation).
-    variant = (e && e[0] == 'm') ? 1 : ((e && e[0] == 'f') ? 0 : ((e && e[0] == 't' && e[2] == '1') ? 2 : 3));
+    // default: row-major tcgen05 kernels (tc1 for short page runs, tc2 for long; fastest
+    // in the verify graph, scripts/attn_graph.py).  BST_ATTN=kt: key-major kernel,
+    // BST_ATTN=mma: mma.sync kernel, BST_ATTN=fa: 128-key two-warpgroup kernel
+    // (experimental), BST_ATTN=tc1: tc1 only.
+    if (e && e[0] == 'k') variant = 4;
+    else if (e && e[0] == 'm') variant = 1;
+    else if (e && e[0] == 'f') variant = 0;
+    else if (e && e[0] == 't' && e[1] == 'c' && e[2] == '1') variant = 2;
+    else variant = 3;
   }
   static int tc2_min = -1;
   if (tc2_min < 0) {
     const char* e = getenv("BST_TC2_MIN");
     tc2_min = e ? atoi(e) : 8;
+  }
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    BST_CUDA(cudaGetDevice(&dev));
+    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  static int no_merge = -1;
+  if (no_merge < 0) no_merge = getenv("BST_ATTN_COMBINE") ? 1 : 0;
+  cudaStream_t st = as_stream(stream);
+  if (variant == 4) {
+    // key-major kernel: row blocks of <= 128 rows balanced over R, one CTA per SM
+    const int rbk = (R + 127) / 128;
+    const int rpb = (R + rbk - 1) / rbk;
+    const int nch = (rpb + 15) / 16;
+    a.row_blocks = rbk;
+    a.rows_per_block = rpb;
+    // split plan.  Global merge (one wave of CTAs over every SM, partials through L2 and
+    // a gpu-scope counter barrier) vs cluster merge (the splits of a (head, row block)
+    // form one thread-block cluster and merge over DSMEM): per-CTA tile time ~1.2 us,
+    // or the HBM share when the grid saturates HBM; the L2 merge chain costs ~6 us,
+    // the DSMEM merge ~1 us.  The live context is known on the host only as a bound.
+    const int G = n_kv * rbk * n_req;
+    const int hint_keys = state ? max_keys : c + keys_after_c;
+    const int tiles = ((hint_keys + A_PAGE - 1) / A_PAGE + 1) / 2;
+    const double t_tile = 1.2, bw_us = 6.5e6 / 65536.0;  // tiles per us the whole GPU can stream
+    auto tile_time = [&](int ctas) { return fmax(t_tile, ctas / bw_us); };
+    int splits = 0, merge_mode = 0, cs_best = 0;
+    if (n_splits_arg > 0) {
+      splits = n_splits_arg;
+    } else {
+      const int sg = max(1, min(pages, n_sm / G));
+      double best = ((tiles + sg - 1) / sg) * tile_time(G * sg) + (sg > 1 ? 6.0 : 0.0);
+      splits = sg;
+      static int occ[9][4];  // [nch][cs 2, 4, 8] resident clusters (-1: unknown)
+      static bool occ_init = false;
+      if (!occ_init) {
+        for (int i = 0; i < 9; ++i) for (int j = 0; j < 4; ++j) occ[i][j] = -1;
+        occ_init = true;
+      }
+      const int nc8 = nch > 8 ? 8 : nch;
+      static int force = -1;  // BST_KT_MERGE=global|cluster (measurement only)
+      if (force < 0) {
+        const char* e = getenv("BST_KT_MERGE");
+        force = (e && e[0] == 'g') ? 1 : ((e && e[0] == 'c') ? 2 : 0);
+      }
+      if (force == 2) best = 1e30;
+      for (int j = 0; j < 3 && force != 1; ++j) {
+        const int cs = 2 << j;
+        if (cs > pages) break;
+        if (occ[nc8][j] < 0) occ[nc8][j] = kt_cluster_occupancy(nc8, cs);
+        if (occ[nc8][j] < G) continue;
+        const double tc = ((tiles + cs - 1) / cs) * tile_time(G * cs) + 1.0 - (force == 2 ? cs : 0);
+        if (tc < best) { best = tc; splits = cs; cs_best = cs; }
+      }
+      if (cs_best) merge_mode = 2;
+    }
+    if (splits > pages) splits = pages;
+    if (merge_mode == 2) {
+      a.n_splits = cs_best;  // exactly one cluster per (head, row block, request)
+      a.pages_per_split = (pages + cs_best - 1) / cs_best;
+    } else {
+      int pk = (pages + splits - 1) / splits;
+      pk += pk & 1;  // 128-key tiles
+      a.n_splits = (pages + pk - 1) / pk;
+      a.pages_per_split = pk;
+    }
+    // two workspace banks (counters + partials) alternating with the layer, so back-to-back
+    // launches whose CTAs overlap under PDL never share a counter or a partial buffer
+    const size_t bank_floats = (size_t)n_req * a.n_splits * s * n_q * (A_D + 2);
+    if (a.n_splits > 1 && merge_mode != 2) {
+      const size_t need = A_WS_CNT_BYTES + 2 * bank_floats * sizeof(float);
+      BST_REQUIRE(ws && ws_bytes >= need, "attention workspace too small: %zu < %zu", ws_bytes, need);
+    }
+    const int bank = layer & 1;
+    if (ws) {
+      a.cnt = reinterpret_cast<unsigned long long*>(ws) + bank * (A_WS_CNT_BYTES / 16);
+      a.ws_o = ws + A_WS_CNT_BYTES / sizeof(float) + bank * bank_floats;
+      a.ws_ml = a.ws_o + (size_t)n_req * a.n_splits * s * n_q * A_D;
+    }
+    if (merge_mode == 2)
+      a.merge = 2;
+    else
+      a.merge = (a.n_splits > 1 && !no_merge && n_kv * a.n_splits * rbk * n_req <= n_sm &&
+                 n_kv * rbk * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES / 2) ? 1 : 0;
+    static bool kt_attr = false;
+    if (!kt_attr) {
+#define KT_ATTR(n) BST_CUDA(cudaFuncSetAttribute(attn_kt_kernel<n>, cudaFuncAttributeMaxDynamicSharedMemorySize, kt_smem(n)))
+      KT_ATTR(1); KT_ATTR(2); KT_ATTR(3); KT_ATTR(4); KT_ATTR(5); KT_ATTR(6); KT_ATTR(7); KT_ATTR(8);
+#undef KT_ATTR
+      kt_attr = true;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(n_kv, a.n_splits, rbk * n_req);
+    cfg.blockDim = dim3(KT_THREADS);
+    cfg.dynamicSmemBytes = kt_smem(nch > 8 ? 8 : nch);
+    cfg.stream = st;
+    cudaLaunchAttribute lat[2];
+    lat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    lat[0].val.programmaticStreamSerializationAllowed = 1;
+    lat[1].id = cudaLaunchAttributeClusterDimension;
+    lat[1].val.clusterDim.x = 1;
+    lat[1].val.clusterDim.y = a.merge == 2 ? a.n_splits : 1;
+    lat[1].val.clusterDim.z = 1;
+    cfg.attrs = lat;
+    cfg.numAttrs = 2;
+    switch (nch) {
+      case 1: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<1>, tm, a)); break;
+      case 2: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<2>, tm, a)); break;
+      case 3: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<3>, tm, a)); break;
+      case 4: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<4>, tm, a)); break;
+      case 5: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<5>, tm, a)); break;
+      case 6: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<6>, tm, a)); break;
+      case 7: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<7>, tm, a)); break;
+      default: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<8>, tm, a)); break;
+    }
+    if (a.n_splits > 1 && !a.merge) attn_combine_kernel<<<dim3((s * n_q + 7) / 8, n_req), 256, 0, st>>>(a);
+    BST_LAUNCH_CHECK();
+    return BST_OK;
   }
   static bool attr = false;
   const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
@@ -1585,20 +2435,20 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc2));
     attr = true;
   }
-  // default: single-group kernel for short per-CTA page runs, two alternating
+  if (ws && n_splits > 1) {  // two workspace banks alternating with the layer (see the key-major path)
+    const size_t bank_floats = (size_t)n_req * n_splits * s * n_q * (A_D + 2);
+    const size_t need = A_WS_CNT_BYTES + 2 * bank_floats * sizeof(float);
+    BST_REQUIRE(ws_bytes >= need, "attention workspace too small: %zu < %zu", ws_bytes, need);
+    const int bank = layer & 1;
+    a.cnt = reinterpret_cast<unsigned long long*>(ws) + bank * (A_WS_CNT_BYTES / 16);
+    a.ws_o = ws + A_WS_CNT_BYTES / sizeof(float) + bank * bank_floats;
+    a.ws_ml = a.ws_o + (size_t)n_req * n_splits * s * n_q * A_D;
+  }
+  // row-major kernels: single-group kernel for short per-CTA page runs, two alternating
   // softmax groups once a CTA walks >= 8 tiles (long context)
   const int v = variant == 3 ? (pps >= tc2_min ? 3 : 2) : variant;
-  // splits merge in-kernel when the whole grid is one wave (one CTA per SM)
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    BST_CUDA(cudaGetDevice(&dev));
-    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
-  static int no_merge = -1;
-  if (no_merge < 0) no_merge = getenv("BST_ATTN_COMBINE") ? 1 : 0;
   a.merge = (n_splits > 1 && (v == 2 || v == 3) && !no_merge && n_kv * n_splits * row_blocks * n_req <= n_sm &&
-             n_kv * row_blocks * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES) ? 1 : 0;
+             n_kv * row_blocks * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES / 2) ? 1 : 0;
   BST_REQUIRE(n_req == 1 || v == 2 || v == 3, "batched attention runs on the tcgen05 kernels only");
   if (v == 1)
     attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
@@ -1652,8 +2502,8 @@ extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* ou
                              ws, ws_bytes, n_req, req_pages, req_state, stream);
 }
 
-extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {
-  return bst::A_WS_CNT_BYTES + (size_t)(n_splits < 1 ? 1 : n_splits) * s * n_q * (128 + 2) * sizeof(float);
+extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {  // two banks of partials
+  return bst::A_WS_CNT_BYTES + 2 * (size_t)(n_splits < 1 ? 1 : n_splits) * s * n_q * (128 + 2) * sizeof(float);
 }
 
 extern "C" int bst_debug_attn_trace_cta(int y) {
@@ -1685,4 +2535,38 @@ extern "C" int bst_debug_cluster_occupancy(int cluster, int smem) {
   int n = 0;
   BST_CUDA(cudaOccupancyMaxActiveClusters(&n, attn_tc_kernel, &cfg));
   return n;
+}
+
+// debug: clusters of `cluster` key-major attention CTAs (dynamic smem `smem`) resident at once
+extern "C" int bst_debug_cluster_occupancy_kt(int cluster, int smem) {
+  using namespace bst;
+  BST_CUDA(cudaFuncSetAttribute(attn_kt_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));  // probe only
+  BST_CUDA(cudaFuncSetAttribute(attn_kt_kernel<5>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(8, cluster, 1);
+  cfg.blockDim = dim3(KT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 1;
+  attr[0].val.clusterDim.y = cluster;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int n = 0;
+  BST_CUDA(cudaOccupancyMaxActiveClusters(&n, attn_kt_kernel<5>, &cfg));
+  return n;
+}
+
+extern "C" int bst_debug_kt_ablate(int v) {
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_kt_ablate, &v, sizeof(int)));
+  return BST_OK;
+}
+
+// Select the K3 kernel family: 3 row-major tcgen05 (default), 4 key-major, 2 tc1 only,
+// 1 mma.sync, 0 experimental FA-style; -1 re-reads BST_ATTN.
+extern "C" int bst_attention_set_variant(int v) {
+  BST_REQUIRE(v >= -1 && v <= 4, "variant must be in -1..4");
+  bst::g_attn_variant = v;
+  return BST_OK;
 }

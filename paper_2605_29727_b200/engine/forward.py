@@ -68,7 +68,8 @@ def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
         splits = math.ceil(pages / pps)
         if splits > 1:
             best = max(best, splits * s * cfg.n_q * 130)
-    return best + 1024  # + the 4 KiB split-counter head (zero-initialised, kept zero by K3)
+    # two alternating banks of partials + the 4 KiB split-counter head (zero-initialised, kept zero by K3)
+    return 2 * best + 1024
 
 
 def _max_partial(shapes, max_rows: int) -> int:

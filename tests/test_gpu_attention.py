@@ -48,10 +48,21 @@ def _ref(q, kv, layer, n_q, n_kv, c, s, visible):
     return torch.einsum("hqk,khd->qhd", torch.softmax(sc, -1), V).reshape(s, n_q * 128)
 
 
+VARIANTS = {"tc": 3, "kt": 4}
+
+
+@pytest.fixture(params=sorted(VARIANTS))
+def variant(request):
+    from paper_2605_29727_b200 import _lib
+    _lib.call("bst_attention_set_variant", VARIANTS[request.param])
+    yield request.param
+    _lib.call("bst_attention_set_variant", -1)
+
+
 @pytest.mark.parametrize("n_q,n_kv", [(32, 8), (4, 2)])
 @pytest.mark.parametrize("c,s", [(0, 1), (5, 17), (2048, 17), (300, 65), (1000, 256), (4096, 33), (20000, 17), (9000, 100)])
 @pytest.mark.parametrize("splits", [0, 1])
-def test_tree_attention(n_q, n_kv, c, s, splits):
+def test_tree_attention(n_q, n_kv, c, s, splits, variant):
     from oracle import specplan_port as O
     from paper_2605_29727_b200 import ops
     kv, q = _setup(n_q, n_kv, c, s, seed=c + s)
@@ -77,7 +88,7 @@ def test_tree_attention(n_q, n_kv, c, s, splits):
 
 @pytest.mark.parametrize("mode", [1, 2])
 @pytest.mark.parametrize("c,s", [(0, 64), (130, 40), (1900, 17)])
-def test_causal_and_full_attention_with_device_c(mode, c, s):
+def test_causal_and_full_attention_with_device_c(mode, c, s, variant):
     from paper_2605_29727_b200 import ops
     n_q, n_kv = 32, 8
     kv, q = _setup(n_q, n_kv, c, s, seed=7 + c)
