@@ -315,6 +315,77 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
   }
 }
 
+// Global split merge of the key-major kernel.  Partials live in a head-major, dim-chunk
+// major layout so both the writers (one query row per thread) and the readers are
+// coalesced: ws_o float4 index ((req, split, head) * 32 + d4) * R + row, ws_ml float2
+// index (req, split, head) * R + row (row = the GQA row index inside the head).  The
+// arrival protocol is split_merge's generation counter.
+__device__ __forceinline__ int64_t kt_ws_base(const AttnArgs& a, int req, int split, int head) {
+  return ((int64_t)req * a.n_splits + split) * a.n_kv + head;
+}
+__device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req, int rb, int row0, int Rb, int t) {
+  const int R = a.group * a.s;
+  named_bar_sync(1, 256);
+  unsigned long long* cnt = a.cnt + ((int64_t)req * a.row_blocks + rb) * a.n_kv + head;
+  if (t == 0) {
+    const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
+    TRACE_MAX(3);
+    if ((unsigned)(old & 0xffffffffu) == (unsigned)a.n_splits - 1u) {
+      red_add_release_gpu(cnt, (1ull << 32) - (unsigned long long)a.n_splits);
+    } else {
+      const unsigned gen = (unsigned)(old >> 32);
+      const long long t0 = gtimer_ns();
+      for (uint32_t it = 1; (unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen; ++it) {
+        if ((it & 1023u) == 0 && gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived
+      }
+    }
+  }
+  if (t == 0) TRACE_MAX(4);
+  named_bar_sync(1, 256);
+  const int ns = a.n_splits;
+  const int per = (Rb + ns - 1) / ns, r0 = split * per, nr = min(r0 + per, Rb) - r0;
+  const float2* ml_all = reinterpret_cast<const float2*>(a.ws_ml);
+  const float4* o_all = reinterpret_cast<const float4*>(a.ws_o);
+  for (int it = t; it < nr * 32; it += 256) {
+    const int rr = row0 + r0 + it % nr, d4 = it / nr;  // lanes walk rows: coalesced
+    float M = -INFINITY, L = 0.f;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int j0 = 0; j0 < ns; j0 += 16) {
+      float2 ml[16];
+      float4 v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        if (j0 + u < ns) {
+          const int64_t b = kt_ws_base(a, req, j0 + u, head);
+          ml[u] = __ldcg(ml_all + b * R + rr);
+          v[u] = __ldcg(o_all + (b * 32 + d4) * R + rr);
+        } else {
+          ml[u] = make_float2(-INFINITY, 0.f);
+          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      float Mn = M;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) Mn = fmaxf(Mn, ml[u].x);
+      if (Mn == -INFINITY) continue;
+      const float sc = M == -INFINITY ? 0.f : ex2(M - Mn);
+      L *= sc;
+      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        const float w = ml[u].x == -INFINITY ? 0.f : ex2(ml[u].x - Mn);
+        L += w * ml[u].y;
+        acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
+      }
+      M = Mn;
+    }
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const int tok = rr / a.group, qh = head * a.group + rr % a.group;
+    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
+    *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  }
+}
+
 // Slots the previous kernel cannot be writing, so their pages may be loaded before
 // griddepcontrol.wait: the committed prefix below c, except that in FULL mode (the
 // drafter block) the keys_after_c context slots just below c are written by the
@@ -1408,19 +1479,16 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
     }
     if (a.n_splits > 1 && a.merge) {
-      float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once both groups' last PV is done
+      if (valid) {  // unnormalised partial straight to the L2 workspace, coalesced over rows
+        const int64_t bse = kt_ws_base(a, req, split, head);
+        float4* op = reinterpret_cast<float4*>(a.ws_o) + (bse * 32 + 16 * g) * R + rg;
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
-            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-      if (valid && g == 0) {
-        const int64_t r = (((int64_t)req * a.n_splits + split) * a.s + tok) * a.n_q + qh;
-        *reinterpret_cast<float2*>(a.ws_ml + r * 2) = make_float2(M, L);
+        for (int q = 0; q < 16; ++q) __stcg(op + (int64_t)q * R, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+        if (g == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + bse * R + rg, make_float2(M, L));
       }
-      named_bar_sync(1, 256);
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
-      split_merge<256>(a, stg, head, split, req, rb, rb * 128, min(128, R - rb * 128), threadIdx.x - 64);
+      kt_global_merge(a, head, split, req, rb, rb * 128, min(128, R - rb * 128), threadIdx.x - 64);
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
@@ -1512,77 +1580,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float r;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
-}
-
-// Global split merge of the key-major kernel.  Partials live in a head-major, dim-chunk
-// major layout so both the writers (one query row per thread) and the readers are
-// coalesced: ws_o float4 index ((req, split, head) * 32 + d4) * R + row, ws_ml float2
-// index (req, split, head) * R + row (row = the GQA row index inside the head).  The
-// arrival protocol is split_merge's generation counter.
-__device__ __forceinline__ int64_t kt_ws_base(const AttnArgs& a, int req, int split, int head) {
-  return ((int64_t)req * a.n_splits + split) * a.n_kv + head;
-}
-__device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req, int rb, int row0, int Rb, int t) {
-  const int R = a.group * a.s;
-  named_bar_sync(1, 256);
-  unsigned long long* cnt = a.cnt + ((int64_t)req * a.row_blocks + rb) * a.n_kv + head;
-  if (t == 0) {
-    const unsigned long long old = atom_add_acq_rel_gpu(cnt, 1ull);
-    TRACE_MAX(3);
-    if ((unsigned)(old & 0xffffffffu) == (unsigned)a.n_splits - 1u) {
-      red_add_release_gpu(cnt, (1ull << 32) - (unsigned long long)a.n_splits);
-    } else {
-      const unsigned gen = (unsigned)(old >> 32);
-      const long long t0 = gtimer_ns();
-      for (uint32_t it = 1; (unsigned)(ld_acquire_gpu64(cnt) >> 32) == gen; ++it) {
-        if ((it & 1023u) == 0 && gtimer_ns() - t0 > 2000000000ll) __trap();  // a split never arrived
-      }
-    }
-  }
-  if (t == 0) TRACE_MAX(4);
-  named_bar_sync(1, 256);
-  const int ns = a.n_splits;
-  const int per = (Rb + ns - 1) / ns, r0 = split * per, nr = min(r0 + per, Rb) - r0;
-  const float2* ml_all = reinterpret_cast<const float2*>(a.ws_ml);
-  const float4* o_all = reinterpret_cast<const float4*>(a.ws_o);
-  for (int it = t; it < nr * 32; it += 256) {
-    const int rr = row0 + r0 + it % nr, d4 = it / nr;  // lanes walk rows: coalesced
-    float M = -INFINITY, L = 0.f;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < ns; j0 += 16) {
-      float2 ml[16];
-      float4 v[16];
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        if (j0 + u < ns) {
-          const int64_t b = kt_ws_base(a, req, j0 + u, head);
-          ml[u] = __ldcg(ml_all + b * R + rr);
-          v[u] = __ldcg(o_all + (b * 32 + d4) * R + rr);
-        } else {
-          ml[u] = make_float2(-INFINITY, 0.f);
-          v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-      float Mn = M;
-#pragma unroll
-      for (int u = 0; u < 16; ++u) Mn = fmaxf(Mn, ml[u].x);
-      if (Mn == -INFINITY) continue;
-      const float sc = M == -INFINITY ? 0.f : ex2(M - Mn);
-      L *= sc;
-      acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        const float w = ml[u].x == -INFINITY ? 0.f : ex2(ml[u].x - Mn);
-        L += w * ml[u].y;
-        acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
-      }
-      M = Mn;
-    }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    const int tok = rr / a.group, qh = head * a.group + rr % a.group;
-    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
-    *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
-  }
 }
 
 // ---- distributed shared memory (thread-block clusters)
