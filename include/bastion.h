@@ -173,6 +173,14 @@ int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* 
 /* Per-row argmax of Y with numpy tie-break (lowest index), verify_sim.py:107-109. */
 int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* argmax,
                     bst_stream_t stream);
+/* Vocab-parallel LM head (tensor-parallel target): per-row argmax keys of
+ * this shard, key = (order-preserving fp32 bits << 32 | 0xFFFFFFFF - global index),
+ * global index = vocab_offset + column, top bit flipped so a signed int64 MAX
+ * all-reduce across shards keeps np.argmax's lowest-index tie-break
+ * (verify_sim.py:107-109).  bst_argmax_from_keys decodes the reduced keys. */
+int bst_gemm_argmax_keys(const float* partial, const bst_gemm_sched_t* sched, int64_t* keys, int vocab_offset,
+                         bst_stream_t stream);
+int bst_argmax_from_keys(const int64_t* keys, int m, int32_t* argmax, bst_stream_t stream);
 
 /* L2 prefetch hint: DRAM-idle kernels (attention, epilogues) stream the next
  * GEMM's weights into L2 while they run (weights never depend on activations). */

@@ -311,14 +311,15 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_s
 }
 
 // Per-token argmax over the full output width, lowest index on ties (np.argmax).
+// vocab_offset: global index of output column 0 (vocab-parallel LM head shards).
 __global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_sched_t s,
-                                   unsigned long long* best) {
+                                   unsigned long long* best, int vocab_offset = 0) {
   const int t = blockIdx.y;
   unsigned long long key = 0;
   auto consider = [&](float v, int n) {
     unsigned int b = __float_as_uint(v);
     b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-    const unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)n);
+    const unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)(n + vocab_offset));
     key = k > key ? k : key;
   };
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g * 4 < s.n_out; g += gridDim.x * blockDim.x) {
@@ -344,6 +345,16 @@ __global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_s
 __global__ void argmax_finalize_kernel(const unsigned long long* best, int m, int32_t* out) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(best[t] & 0xFFFFFFFFull));
+}
+// packed keys <-> signed int64 (flip the top bit) so a signed MAX all-reduce (NCCL int64)
+// orders them exactly as the unsigned comparison above
+__global__ void argmax_key_flip_kernel(unsigned long long* keys, int m) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) keys[t] ^= 0x8000000000000000ull;
+}
+__global__ void argmax_from_signed_kernel(const unsigned long long* keys, int m, int32_t* out) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(keys[t] & 0xFFFFFFFFull));
 }
 
 }  // namespace bst
@@ -442,6 +453,35 @@ extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sch
   gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64));
   argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
                                                             argmax);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+// Vocab-parallel LM head: per-row packed argmax keys of this shard (global index =
+// vocab_offset + column), as signed int64 ready for a MAX all-reduce across shards.
+extern "C" int bst_gemm_argmax_keys(const float* partial, const bst_gemm_sched_t* sched, int64_t* keys,
+                                    int vocab_offset, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(partial && sched && keys, "null pointer argument");
+  BST_REQUIRE(vocab_offset >= 0, "vocab_offset must be >= 0");
+  const bst_gemm_sched_t s = *sched;
+  cudaStream_t st = as_stream(stream);
+  BST_CUDA(cudaMemsetAsync(keys, 0, sizeof(int64_t) * s.m, st));
+  dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
+  unsigned long long* k = reinterpret_cast<unsigned long long*>(keys);
+  gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, k, vocab_offset);
+  argmax_key_flip_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(k, s.m);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+// argmax indices from all-reduced signed keys (lowest global index on ties)
+extern "C" int bst_argmax_from_keys(const int64_t* keys, int m, int32_t* argmax, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(keys && argmax && m >= 0, "bad arguments");
+  if (m == 0) return BST_OK;
+  argmax_from_signed_kernel<<<(m + 127) / 128, 128, 0, as_stream(stream)>>>(
+      reinterpret_cast<const unsigned long long*>(keys), m, argmax);
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -1,0 +1,188 @@
+"""Tensor-parallel target verify — BASELINE config 5 (Qwen3-32B shape, TP=8, NCCL
+all-reduce over NVLink, tree verify + accept).  SURVEY §8e.
+
+Rank r of a tp-way group holds
+  * q/k/v (column-parallel): query heads [r n_q/tp, (r+1) n_q/tp) and KV heads
+    [r n_kv/tp, ...), so attention and the paged KV cache are head-local;
+  * o_proj, down_proj (row-parallel): the matching input columns; their outputs are
+    partial sums of the residual stream, all-reduced (SUM, fp32) before RMSNorm;
+  * gate/up (column-parallel): FFN columns [r h_ffn/tp, ...) of gate and of up;
+  * the LM head (vocab-parallel): vocabulary rows [r V/tp, ...); the per-row argmax
+    is reduced as one signed 64-bit key (order-preserving fp32 bits | ~global index,
+    bst_gemm_argmax_keys) with a MAX all-reduce, which keeps np.argmax's lowest-index
+    tie-break (verify_sim.py:107-109) bit-exactly across shards.
+Embedding, norms and the decode bookkeeping (tree, accept walk, KV compaction of the
+local heads, committed stream) are replicated: every rank computes the same tree from
+the same lattice, so no broadcast is needed.
+
+The collective points are exposed by ``forward_steps`` (a generator yielding
+``(op, tensor)``), so the same code runs under NCCL (``dist_collective``) and in a
+single-process lock-step simulation of tp shards (``run_lockstep``, the parity test).
+Residual protocol at each row-parallel output: rank 0 adds its partial into the
+residual (residual_rmsnorm with the partial), the other ranks overwrite their copy
+of the residual with their partial (gemm_reduce), then SUM all-reduce → every rank
+holds residual + sum of partials; RMSNorm of the reduced residual follows.
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+import torch
+
+from .. import ops
+from .config import ModelConfig
+from .forward import PAGE, TargetModel
+from .weights import LayerWeights, TargetWeights, _normal, _ones
+
+
+def local_config(cfg: ModelConfig, tp: int) -> ModelConfig:
+    """Per-rank shapes of a tp-way shard (heads, FFN columns and vocabulary split evenly)."""
+    if tp < 1 or cfg.n_q % tp or cfg.n_kv % tp or cfg.h_ffn % tp or cfg.V % tp:
+        raise ValueError(f"{cfg.name} does not split {tp} ways (n_q, n_kv, h_ffn and V must divide)")
+    return replace(cfg, name=f"{cfg.name}/tp{tp}", n_q=cfg.n_q // tp, n_kv=cfg.n_kv // tp, h_ffn=cfg.h_ffn // tp,
+                   V=cfg.V // tp)
+
+
+def shard_layer(lw: LayerWeights, cfg: ModelConfig, tp: int, rank: int) -> LayerWeights:
+    d, hq, hkv, f = cfg.d, cfg.h_q // tp, cfg.h_kv // tp, cfg.h_ffn // tp
+    q = lw.qkv[rank * hq:(rank + 1) * hq]
+    k = lw.qkv[cfg.h_q + rank * hkv:cfg.h_q + (rank + 1) * hkv]
+    v = lw.qkv[cfg.h_q + cfg.h_kv + rank * hkv:cfg.h_q + cfg.h_kv + (rank + 1) * hkv]
+    gate = lw.gate_up[rank * f:(rank + 1) * f]
+    up = lw.gate_up[cfg.h_ffn + rank * f:cfg.h_ffn + (rank + 1) * f]
+    del d
+    return LayerWeights(in_norm=lw.in_norm, qkv=torch.cat([q, k, v]).contiguous(), q_norm=lw.q_norm,
+                        k_norm=lw.k_norm, o=lw.o[:, rank * hq:(rank + 1) * hq].contiguous(), post_norm=lw.post_norm,
+                        gate_up=torch.cat([gate, up]).contiguous(),
+                        down=lw.down[:, rank * f:(rank + 1) * f].contiguous())
+
+
+def shard_weights(full: TargetWeights, cfg: ModelConfig, tp: int, rank: int) -> TargetWeights:
+    """Rank `rank`'s slice of full target weights (parity tests)."""
+    local_config(cfg, tp)
+    vl = cfg.V // tp
+    return TargetWeights(emb=full.emb, layers=[shard_layer(lw, cfg, tp, rank) for lw in full.layers],
+                         final_norm=full.final_norm, lm_head=full.lm_head[rank * vl:(rank + 1) * vl].contiguous())
+
+
+def random_shard(cfg: ModelConfig, tp: int, rank: int, seed: int, dev) -> TargetWeights:
+    """Random-init weights of one shard only (the 32B bench: no rank builds the full model)."""
+    lc = local_config(cfg, tp)
+    g = torch.Generator(device=dev).manual_seed(seed * 1009 + rank)
+    layers = [LayerWeights(in_norm=_ones(cfg.h, dev), qkv=_normal((lc.qkv_out, cfg.h), g, dev),
+                           q_norm=_ones(cfg.d, dev), k_norm=_ones(cfg.d, dev), o=_normal((cfg.h, lc.h_q), g, dev),
+                           post_norm=_ones(cfg.h, dev), gate_up=_normal((2 * lc.h_ffn, cfg.h), g, dev),
+                           down=_normal((cfg.h, lc.h_ffn), g, dev)) for _ in range(cfg.L)]
+    eg = torch.Generator(device=dev).manual_seed(seed * 1009 + 997)  # embedding replicated: same on every rank
+    return TargetWeights(emb=_normal((cfg.V, cfg.h), eg, dev), layers=layers, final_norm=_ones(cfg.h, dev),
+                         lm_head=_normal((lc.V, cfg.h), g, dev))
+
+
+class TPTargetModel(TargetModel):
+    """One rank of the tensor-parallel target (heads / FFN / vocabulary shards)."""
+
+    def __init__(self, cfg: ModelConfig, tp: int, rank: int, w: TargetWeights, max_slots: int, max_rows: int,
+                 dev) -> None:
+        if not 0 <= rank < tp:
+            raise ValueError("rank out of range")
+        self.full_cfg, self.tp, self.rank = cfg, tp, rank
+        super().__init__(local_config(cfg, tp), w, max_slots, max_rows, (), dev)
+        self.keys = torch.zeros(max_rows, dtype=torch.int64, device=dev)
+
+    def _row_parallel_out(self, p: ops.PartialOut, n: int):
+        """Residual protocol of a row-parallel GEMM output; yields the SUM all-reduce."""
+        cfg = self.cfg
+        resid = self.resid[:n]
+        if self.rank == 0:
+            ops.residual_rmsnorm(p, resid, n, cfg.h, self.w.final_norm, cfg.eps, x=self.x[:n])  # resid += Y_0
+        else:
+            ops.gemm_reduce_into(p, resid)  # resid = Y_r
+        yield "sum", resid
+
+    def forward_steps(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None,
+                      mask_words: int = 0, head: str | None = "argmax", c_host: int = 0):
+        """The verify forward of this shard; yields (op, tensor) at every collective."""
+        cfg, w, kv = self.cfg, self.w, self.kv
+        n, eps = rows, cfg.eps
+        pt = kv.page_table
+        x, resid = self.x[:n], self.resid[:n]
+        ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
+        for li, lw in enumerate(w.layers):
+            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
+            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
+                         None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state)
+            ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, cfg.n_q, cfg.n_kv, n,
+                          c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words, self.attn_ws,
+                          n_splits=self.attn_splits)
+            p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
+            yield from self._row_parallel_out(p, n)
+            ops.residual_rmsnorm(None, resid, n, cfg.h, lw.post_norm, eps, x=x)
+            p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
+            ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
+            p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
+            yield from self._row_parallel_out(p, n)
+            nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
+            ops.residual_rmsnorm(None, resid, n, cfg.h, nxt, eps, x=x)
+        if head == "argmax":
+            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
+            ops.gemm_argmax_keys(p, self.keys[:n], self.rank * cfg.V)
+            yield "max", self.keys[:n]
+            ops.argmax_from_keys(self.keys, n, self.argmax)
+
+    def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
+                head: str | None = "argmax", c_host: int = 0, pt=None, batch=None, collective=None) -> None:
+        if pt is not None or batch is not None:
+            raise ValueError("the tensor-parallel target serves one request per group")
+        coll = collective or dist_collective
+        for op, t in self.forward_steps(rows, state, mode, keys_after_c, anc, mask_words, head, c_host):
+            coll(op, t)
+
+
+def dist_collective(op: str, t: torch.Tensor) -> None:
+    """NCCL all-reduce over the tensor-parallel group (the default process group)."""
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    dist.all_reduce(t, op=dist.ReduceOp.SUM if op == "sum" else dist.ReduceOp.MAX)
+
+
+def run_lockstep(models: list[TPTargetModel], streams: list, *args, **kw) -> None:
+    """Single-process simulation of a tp group: run every shard's forward_steps in lock
+    step and reduce at each collective (SUM / MAX over the shard tensors), on one GPU."""
+    gens = [m.forward_steps(*args, **kw) for m in models]
+    while True:
+        items = []
+        for g, st in zip(gens, streams):
+            with torch.cuda.stream(st):
+                items.append(next(g, None))
+        if all(it is None for it in items):
+            return
+        if any(it is None for it in items):
+            raise RuntimeError("shards disagree on the collective sequence")
+        for st in streams:
+            st.synchronize()
+        op = items[0][0]
+        ts = [it[1] for it in items]
+        acc = ts[0].clone()
+        for t in ts[1:]:
+            acc = acc + t if op == "sum" else torch.maximum(acc, t)
+        for t in ts:
+            t.copy_(acc)
+        torch.cuda.synchronize()
+
+
+def pack_argmax_key(value: float, global_index: int) -> int:
+    """Host restatement of the shard key (bst_gemm_argmax_keys): order-preserving fp32
+    bits in the high word, 0xFFFFFFFF - index in the low word, top bit flipped into the
+    signed int64 order.  max() over shards' keys decodes to np.argmax of the full row."""
+    import struct
+    b = struct.unpack("<I", struct.pack("<f", value))[0]
+    b = (~b & 0xFFFFFFFF) if b & 0x80000000 else (b | 0x80000000)
+    u = (b << 32) | (0xFFFFFFFF - global_index)
+    f = u ^ (1 << 63)  # uint64 with the top bit flipped, read as int64
+    return f - (1 << 64) if f >> 63 else f
+
+
+def unpack_argmax_key(key: int) -> int:
+    return 0xFFFFFFFF - (key & 0xFFFFFFFF)

@@ -57,6 +57,28 @@ def linear(x: torch.Tensor, w: torch.Tensor, dtype=torch.float32) -> torch.Tenso
     return gemm_reduce(gemm_partial(x, w), dtype)
 
 
+def gemm_reduce_into(p: PartialOut, y: torch.Tensor) -> torch.Tensor:
+    """Dense fp32 Y[m, n_out] (row stride y.stride(0)) from the partial slots."""
+    s = p.sched
+    assert y.dtype == torch.float32 and y.stride(1) == 1 and y.shape[0] >= s.m and y.shape[1] >= s.n_out
+    _lib.call("bst_gemm_reduce", p.buf.data_ptr(), C.byref(s), y.data_ptr(), None, y.stride(0), stream_ptr())
+    return y
+
+
+def gemm_argmax_keys(p: PartialOut, keys: torch.Tensor, vocab_offset: int) -> torch.Tensor:
+    """Signed int64 packed (value, global index) argmax keys of a vocab-parallel LM-head shard."""
+    assert keys.dtype == torch.int64 and keys.numel() >= p.sched.m
+    _lib.call("bst_gemm_argmax_keys", p.buf.data_ptr(), C.byref(p.sched), keys.data_ptr(), int(vocab_offset),
+              stream_ptr())
+    return keys
+
+
+def argmax_from_keys(keys: torch.Tensor, m: int, out: torch.Tensor) -> torch.Tensor:
+    assert keys.dtype == torch.int64 and out.dtype == torch.int32
+    _lib.call("bst_argmax_from_keys", keys.data_ptr(), int(m), out.data_ptr(), stream_ptr())
+    return out
+
+
 def gemm_argmax(p: PartialOut, out: torch.Tensor | None = None, scratch: torch.Tensor | None = None) -> torch.Tensor:
     s = p.sched
     out = out if out is not None else torch.empty(s.m, dtype=torch.int32, device=p.buf.device)
