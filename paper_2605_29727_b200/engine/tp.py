@@ -186,3 +186,110 @@ def pack_argmax_key(value: float, global_index: int) -> int:
 
 def unpack_argmax_key(key: int) -> int:
     return 0xFFFFFFFF - (key & 0xFFFFFFFF)
+
+
+class TPVerifier:
+    """Config 5 engine: one request per tensor-parallel group, tree verify + accept.
+
+    Every rank runs the same replicated bookkeeping (K2 tree from the same lattice,
+    verify rows, the K6 accept walk, KV compaction of its local heads, the committed
+    stream); only the target forward is sharded.  The lattice is a fixed seeded one
+    (config 5 measures verify + accept at fixed budgets, BASELINE.json configs[4])."""
+
+    def __init__(self, cfg: ModelConfig, tp: int, rank: int, max_ctx: int, seed: int = 0,
+                 weights: TargetWeights | None = None, n_cap: int = 255, gamma: int = 16, top_k: int = 8,
+                 device=None) -> None:
+        from .decode import MAX_ROWS
+        from ..draft_tree import DeviceTree
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.dev, self.cfg, self.tp, self.rank = dev, cfg, tp, rank
+        self.gamma, self.top_k, self.n_cap = gamma, top_k, min(n_cap, MAX_ROWS - 1)
+        self.max_ctx = max_ctx
+        w = weights if weights is not None else random_shard(cfg, tp, rank, seed, dev)
+        self.target = TPTargetModel(cfg, tp, rank, w, max_ctx + MAX_ROWS + PAGE, MAX_ROWS, dev)
+        i32 = dict(dtype=torch.int32, device=dev)
+        self.state = torch.zeros(8, **i32)
+        self.tree = DeviceTree(self.n_cap, dev)
+        self.path = torch.zeros(gamma + 1, **i32)
+        self.committed = torch.zeros(gamma + 1, **i32)
+        self.acc_meta = torch.zeros(4, **i32)
+        self.out_tokens = torch.zeros(max_ctx + MAX_ROWS, **i32)
+        self.stream = torch.cuda.Stream(dev)
+        self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
+        self.n_nodes = 0
+
+    def reset(self, prompt) -> None:
+        """Prefill prompt[:-1] causally (chunks of MAX_ROWS); prompt[-1] is the pending root."""
+        from .decode import MAX_ROWS
+        from .forward import MODE_CAUSAL
+        prompt = [int(t) for t in prompt]
+        P = len(prompt)
+        if not 1 <= P <= self.max_ctx:
+            raise ValueError("prompt length must be in [1, max_ctx]")
+        t = self.target
+        with torch.cuda.stream(self.stream):
+            for start in range(0, P - 1, MAX_ROWS):
+                n = min(MAX_ROWS, P - 1 - start)
+                self.state.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+                t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
+                ar = torch.arange(n, dtype=torch.int32, device=self.dev)
+                t.pos[:n].copy_(ar)
+                t.slot[:n].copy_(ar)
+                t.forward(n, self.state, MODE_CAUSAL, keys_after_c=n, head=None, c_host=start)
+            self.state.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
+        self.stream.synchronize()
+
+    def set_tree(self, n_nodes: int, seed: int = 0) -> int:
+        """K2 (fixed budget, best-first) on a seeded lattice: the same tree on every rank."""
+        import numpy as np
+
+        from .. import _lib
+        from ..draft_tree import expand_device
+        rng = np.random.default_rng(seed)
+        tok = np.stack([rng.choice(self.cfg.V, self.top_k, replace=False) for _ in range(self.gamma)]).astype(np.int32)
+        raw = np.sort(rng.dirichlet(np.full(self.top_k, 0.6), self.gamma), axis=1)[:, ::-1] * 0.95
+        plan = _lib.Plan(policy=_lib.POLICY_FIXED, n_max=int(n_nodes))
+        with torch.cuda.stream(self.stream):
+            expand_device(torch.from_numpy(tok).to(self.dev), torch.from_numpy(raw.copy()).to(self.dev), plan,
+                          self.n_cap, out=self.tree)
+        self.stream.synchronize()
+        self.n_nodes = int(self.tree.meta[0].item())
+        return self.n_nodes
+
+    def _verify_body(self, rows: int) -> None:
+        from ..verify_sim import accept_device
+        from .forward import MODE_TREE
+        t, tr, cfg = self.target, self.tree, self.target.cfg
+        ops.verify_rows(self.state, tr.token, tr.depth, tr.meta, rows, t.tokens, t.pos, t.slot)
+        t.forward(rows, self.state, MODE_TREE, keys_after_c=rows, anc=tr.anc_mask, mask_words=tr.mask_words,
+                  head="argmax")
+        accept_device(tr.token, tr.child_start, tr.child_list, t.argmax, self.gamma + 1, self.path, self.committed,
+                      self.acc_meta)
+        kv = t.kv
+        ops.kv_compact(kv.buf, cfg.L, cfg.n_kv, PAGE, kv.layer_stride, kv.page_table, self.state, self.path,
+                       self.acc_meta, self.gamma + 1)
+        ops.commit_state(self.state, self.acc_meta, self.committed, self.gamma + 1, self.out_tokens)
+
+    def step(self, graph: bool = True) -> None:
+        """One verify + accept + compact + commit on the current tree (asynchronous)."""
+        from .decode import BUCKET, MAX_ROWS
+        rows = min(MAX_ROWS, ((self.n_nodes + 1 + BUCKET - 1) // BUCKET) * BUCKET)
+        if not graph:
+            with torch.cuda.stream(self.stream):
+                self._verify_body(rows)
+            return
+        g = self.graphs.get(rows)
+        if g is None:
+            saved = self.state.clone()
+            with torch.cuda.stream(self.stream):
+                self._verify_body(rows)  # warm-up (attributes, tensor maps, communicators)
+            self.stream.synchronize()
+            self.state.copy_(saved)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=self.stream):
+                self._verify_body(rows)
+            self.stream.synchronize()
+            self.state.copy_(saved)
+            self.graphs[rows] = g
+        with torch.cuda.stream(self.stream):
+            g.replay()
