@@ -173,6 +173,14 @@ int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sched, float* 
 /* Per-row argmax of Y with numpy tie-break (lowest index), verify_sim.py:107-109. */
 int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* argmax,
                     bst_stream_t stream);
+/* Temperature-T sample per row (exact-match sampled verification, verify_sim.py:111-126):
+ * argmax over n of logit_n / T + Gumbel noise, the noise a Philox4x32-10 function of
+ * (seed, absolute position c + pos[row], n) with c = state[c_idx] (state may be NULL:
+ * c = 0), so the tree row of a node and the AR step at the same position sample
+ * identically.  T must be > 0. */
+int bst_gemm_sample(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* out,
+                    const int32_t* pos, const int32_t* state, int c_idx, float temperature, uint64_t seed,
+                    bst_stream_t stream);
 /* Vocab-parallel LM head (tensor-parallel target): per-row argmax keys of
  * this shard, key = (order-preserving fp32 bits << 32 | 0xFFFFFFFF - global index),
  * global index = vocab_offset + column, top bit flipped so a signed int64 MAX

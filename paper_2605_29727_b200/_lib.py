@@ -73,6 +73,7 @@ SIGNATURES = {
     "bst_gemm_reduce": (_I, [_P, C.POINTER(GemmSched), _P, _P, _I64, _P]),
     "bst_gemm_argmax": (_I, [_P, C.POINTER(GemmSched), _P, _P, _P]),
     "bst_gemm_argmax_keys": (_I, [_P, C.POINTER(GemmSched), _P, _I, _P]),
+    "bst_gemm_sample": (_I, [_P, C.POINTER(GemmSched), _P, _P, _P, _P, _I, C.c_float, C.c_uint64, _P]),
     "bst_argmax_from_keys": (_I, [_P, _I, _P, _P]),
     "bst_expand_dev": (_I, [_P, _P, _I, _I, _P, _I, _I, _I, C.POINTER(Tree), _P, _SZ, _P]),
     "bst_attention": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P, _I, _I,
@@ -131,7 +132,7 @@ KERNELS_PER_CALL = {
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
     "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,
-    "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1, "bst_gemm_argmax_keys": 2, "bst_argmax_from_keys": 1,
+    "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1, "bst_gemm_argmax_keys": 2, "bst_argmax_from_keys": 1, "bst_gemm_sample": 2,
 }
 launch_count = 0
 

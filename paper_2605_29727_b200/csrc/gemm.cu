@@ -342,6 +342,61 @@ __global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_s
   if ((threadIdx.x & 31) == 0) atomicMax(best + t, key);
 }
 
+// ---- temperature sampling (T > 0): Gumbel-max over logits / T.  The noise of vocabulary
+// entry n at row t is Philox4x32-10 keyed by the request seed with counter (n / 4,
+// absolute position c + pos[t]), so a sample is a function of (seed, position, logits):
+// the tree row of a node at depth d and the autoregressive step at the same position draw
+// the same noise, and tree decode reproduces sampled AR decode exactly (the sampled
+// analogue of greedy output preservation, exact-match verification verify_sim.py:111-126).
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = c.x * 0xD2511F53u, hi0 = __umulhi(c.x, 0xD2511F53u);
+    const uint32_t lo1 = c.z * 0xCD9E8D57u, hi1 = __umulhi(c.z, 0xCD9E8D57u);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u;
+    k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+__device__ __forceinline__ float gumbel_of(uint32_t x) {
+  const float u = (float)(x >> 8) * 5.9604645e-8f + 2.9802322e-8f;  // (0, 1)
+  return -__logf(-__logf(u));
+}
+__global__ void gemm_sample_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, unsigned long long* best,
+                                   const int32_t* __restrict__ pos, const int32_t* __restrict__ state, int c_idx,
+                                   float inv_t, uint2 seed) {
+  const int t = blockIdx.y;
+  const uint32_t apos = (uint32_t)((state ? state[c_idx] : 0) + pos[t]);
+  unsigned long long key = 0;
+  auto consider = [&](float v, int n) {
+    unsigned int b = __float_as_uint(v);
+    b = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    const unsigned long long k = ((unsigned long long)b << 32) | (0xFFFFFFFFu - (unsigned)n);
+    key = k > key ? k : key;
+  };
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g * 4 < s.n_out; g += gridDim.x * blockDim.x) {
+    const int n0 = g * 4;
+    const uint4 r = philox4x32_10(make_uint4((uint32_t)g, apos, 0u, 0u), seed);
+    const uint32_t rr[4] = {r.x, r.y, r.z, r.w};
+    if (n0 + 4 <= s.n_out) {
+      const float4 v = gemm_load4(partial, s, t, n0);
+      consider(fmaf(v.x, inv_t, gumbel_of(rr[0])), n0);
+      consider(fmaf(v.y, inv_t, gumbel_of(rr[1])), n0 + 1);
+      consider(fmaf(v.z, inv_t, gumbel_of(rr[2])), n0 + 2);
+      consider(fmaf(v.w, inv_t, gumbel_of(rr[3])), n0 + 3);
+    } else {
+      for (int n = n0; n < s.n_out; ++n) consider(fmaf(gemm_load(partial, s, t, n), inv_t, gumbel_of(rr[n - n0])), n);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, o);
+    key = ok > key ? ok : key;
+  }
+  if ((threadIdx.x & 31) == 0) atomicMax(best + t, key);
+}
+
 __global__ void argmax_finalize_kernel(const unsigned long long* best, int m, int32_t* out) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(best[t] & 0xFFFFFFFFull));
@@ -453,6 +508,25 @@ extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sch
   gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64));
   argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
                                                             argmax);
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+// Temperature sample per row: argmax_n (logit_n / T + Gumbel(seed, c + pos[row], n)).
+extern "C" int bst_gemm_sample(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64,
+                               int32_t* out, const int32_t* pos, const int32_t* state, int c_idx, float temperature,
+                               uint64_t seed, bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(partial && sched && scratch_u64 && out && pos, "null pointer argument");
+  BST_REQUIRE(temperature > 0.f, "temperature must be > 0 (T = 0 is bst_gemm_argmax)");
+  const bst_gemm_sched_t s = *sched;
+  cudaStream_t st = as_stream(stream);
+  BST_CUDA(cudaMemsetAsync(scratch_u64, 0, sizeof(unsigned long long) * s.m, st));
+  dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
+  gemm_sample_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64), pos, state,
+                                           c_idx, 1.f / temperature,
+                                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
+  argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m, out);
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -138,6 +138,7 @@ class B200Engine:
             self.state.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
         self.stream.synchronize()
         self.exported = []
+        self._pending = None
 
     def set_policy(self, kind: str, n: int = 0, estimator: VerifyLatencyEstimator | None = None,
                    latencies: CycleLatencies | None = None, n_max: int | None = None) -> None:
@@ -180,14 +181,26 @@ class B200Engine:
         topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
         expand_device_plan(self.lat_tok, self.lat_prob, self.plan_dev, self.policy[0], self.policy[1], self.tree)
 
-    def _verify_body(self, rows: int) -> None:
-        t, d, tr = self.target, self.drafter, self.tree
+    def _head(self) -> str:
+        return "sample" if self.target.temperature > 0.0 else "argmax"
+
+    def _verify_forward(self, rows: int) -> None:
+        t, tr = self.target, self.tree
         ops.verify_rows(self.state, tr.token, tr.depth, tr.meta, rows, t.tokens, t.pos, t.slot)
         t.forward(rows, self.state, MODE_TREE, keys_after_c=rows, anc=tr.anc_mask, mask_words=tr.mask_words,
-                  head="argmax")
+                  head=self._head())
+
+    def _verify_body(self, rows: int) -> None:
+        self._verify_forward(rows)
         from ..verify_sim import accept_device
+        t, tr = self.target, self.tree
         accept_device(tr.token, tr.child_start, tr.child_list, t.argmax, self.gamma + 1, self.path, self.committed,
                       self.acc_meta)
+        self._commit_tail()
+
+    def _commit_tail(self) -> None:
+        """KV compaction of the accepted path, drafter feature gather, state update."""
+        t, d, tr = self.target, self.drafter, self.tree
         kv = t.kv
         ops.kv_compact(kv.buf, self.cfg.L, self.cfg.n_kv, PAGE, kv.layer_stride, kv.page_table, self.state, self.path,
                        self.acc_meta, self.gamma + 1)
@@ -327,8 +340,8 @@ class B200Engine:
         t.tokens[:1].copy_(self.state[ST_BONUS:ST_BONUS + 1])
         t.pos[:1].zero_()
         t.slot[:1].zero_()
-        t.forward(1, self.state, MODE_CAUSAL, keys_after_c=1, head="argmax")
-        # commit: c += 1, root <- argmax
+        t.forward(1, self.state, MODE_CAUSAL, keys_after_c=1, head=self._head())
+        # commit: c += 1, root <- argmax (or the T > 0 sample)
         self.state[ST_C:ST_C + 1].add_(1)
         self.state[ST_BONUS:ST_BONUS + 1].copy_(t.argmax[:1])
 
@@ -382,6 +395,8 @@ class B200Engine:
         if sim_cfg.top_k != self.top_k:
             raise ValueError(f"engine was built with top_k={self.top_k}")
         ema = estimator.variant in ("ema", "ema_calib")
+        self.set_temperature(sim_cfg.temperature, self.target.sample_seed)
+        self._sync(self.tokens())
         events: list = []
         pending = None  # (index, s, events) of the previous cycle, observed at this cycle's sync
         cyc0 = int(self.state[ST_CYCLE].item())
@@ -412,8 +427,9 @@ class B200Engine:
         return records, tuple(self.tokens())
 
     def drafter_marginals(self, prefix) -> MarginalBlock:
-        """fp64 drafter rows for the engine's current state (prefix must be its committed stream)."""
-        self._check_prefix(prefix)
+        """fp64 drafter rows for the engine's current state (prefix must be its committed stream,
+        possibly extended by the acceptance of the last verified tree / the last next_token)."""
+        self._sync(prefix)
         self.probs_full = torch.empty(self.gamma, self.cfg.V, dtype=torch.float64, device=self.dev)
         with torch.cuda.stream(self.stream):
             logits = self.drafter.forward(self.state)
@@ -424,6 +440,93 @@ class B200Engine:
     def _check_prefix(self, prefix) -> None:
         if tuple(prefix) != tuple(self.tokens()):
             raise ValueError("engine plugin: prefix does not match the engine's committed stream")
+
+    # ----------------------------- reference plugin protocol, general façade loop
+    def set_temperature(self, temperature: float, seed: int = 0) -> None:
+        """Verify / AR head: T = 0 greedy argmax (np.argmax tie-break), T > 0 Gumbel-max samples
+        keyed by (seed, absolute position) (bst_gemm_sample), so a tree decode reproduces the
+        sampled AR decode token for token (exact-match sampled verification,
+        verify_sim.py:111-126).  Changing it drops the captured verify / AR graphs."""
+        if temperature < 0.0:
+            raise ValueError("temperature must be >= 0")
+        t = self.target
+        if (float(temperature), int(seed)) != (t.temperature, t.sample_seed):
+            t.temperature, t.sample_seed = float(temperature), int(seed)
+            self.graphs_v.clear()
+            self.graph_ar = None
+
+    def _sync(self, prefix) -> None:
+        """Bring the device state to ``prefix``: the committed stream, or it extended by the
+        acceptance of the last tree verified through ``tree_argmax`` / ``tree_sample`` (the
+        same K6 walk on the same target tokens) or by the last ``next_token`` result."""
+        prefix = tuple(int(x) for x in prefix)
+        pend, self._pending = getattr(self, "_pending", None), None
+        if prefix == tuple(self.tokens()):
+            return
+        from ..verify_sim import accept_device
+        with torch.cuda.stream(self.stream):
+            if pend == "tree":
+                t, tr = self.target, self.tree
+                accept_device(tr.token, tr.child_start, tr.child_list, t.argmax, self.gamma + 1, self.path,
+                              self.committed, self.acc_meta)
+                self._commit_tail()
+            elif isinstance(pend, tuple) and pend[0] == "ar":
+                self.path[:1].zero_()
+                self.committed[:1].fill_(pend[1])
+                self.acc_meta[:2].copy_(torch.tensor([1, pend[1]], dtype=torch.int32))
+                self._commit_tail()
+        self.stream.synchronize()
+        if prefix != tuple(self.tokens()):
+            raise ValueError("engine plugin: prefix does not continue the engine's committed stream")
+
+    def _tree_verify(self, tree, prefix) -> torch.Tensor:
+        from ..verify_sim import _device_children
+        self._sync(prefix)
+        n = len(tree.nodes) - 1
+        if n > self.n_cap:
+            raise ValueError(f"tree of {n} nodes exceeds the engine's capacity {self.n_cap}")
+        tr, t = self.tree, self.target
+        parents = [-1] + [x.parent for x in tree.nodes[1:]]
+        with torch.cuda.stream(self.stream):
+            tok, start, kids = _device_children(tree)
+            tr.token[: n + 1].copy_(tok[: n + 1])
+            tr.child_start[: n + 2].copy_(start[: n + 2])
+            tr.child_list[: max(n, 1)].copy_(kids[: max(n, 1)])
+            tr.parent[: n + 1].copy_(torch.tensor(parents, dtype=torch.int32))
+            tr.depth[: n + 1].copy_(torch.tensor([x.depth for x in tree.nodes], dtype=torch.int32))
+            tr.meta.zero_()
+            tr.meta[0] = n
+            _lib.call("bst_ancestor_mask", tr.parent.data_ptr(), n + 1, tr.mask_words, tr.anc_mask.data_ptr(),
+                      self.stream.cuda_stream)
+            self._verify_forward(self._bucket(n))
+        self.stream.synchronize()
+        self._pending = "tree"
+        return t.argmax[: n + 1]
+
+    def tree_argmax(self, tree, prefix) -> torch.Tensor:
+        """Greedy target token after every tree node (int32 device tensor, one batched verify)."""
+        self.set_temperature(0.0, self.target.sample_seed)
+        return self._tree_verify(tree, prefix)
+
+    def tree_sample(self, tree, prefix, temperature: float) -> torch.Tensor:
+        """Temperature-T target sample after every tree node (exact-match sampled verification)."""
+        self.set_temperature(temperature, self.target.sample_seed)
+        return self._tree_verify(tree, prefix)
+
+    def next_token(self, prefix, temperature: float) -> int:
+        """One target step after ``prefix`` (greedy at T = 0, else the keyed sample)."""
+        self.set_temperature(temperature, self.target.sample_seed)
+        self._sync(prefix)
+        t = self.target
+        with torch.cuda.stream(self.stream):
+            t.tokens[:1].copy_(self.state[ST_BONUS:ST_BONUS + 1])
+            t.pos[:1].zero_()
+            t.slot[:1].zero_()
+            t.forward(1, self.state, MODE_CAUSAL, keys_after_c=1, head=self._head())
+        self.stream.synchronize()
+        tok = int(t.argmax[0].item())
+        self._pending = ("ar", tok)
+        return tok
 
     def __repr__(self) -> str:  # pragma: no cover
         return f"B200Engine({self.cfg.name}, gamma={self.gamma}, top_k={self.top_k}, n_cap={self.n_cap})"

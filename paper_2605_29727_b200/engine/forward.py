@@ -101,6 +101,7 @@ class TargetModel:
         self.attn_ws = torch.zeros(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
         self.attn_splits = 0  # K3 split count (0: automatic); parity tests pin it
         self.logits = None
+        self.temperature, self.sample_seed = 0.0, 0  # head "sample": Gumbel-max at T keyed by (seed, c + pos)
 
     def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
                 head: str | None = "argmax", c_host: int = 0, pt: torch.Tensor | None = None,
@@ -158,6 +159,10 @@ class TargetModel:
         if head == "argmax":
             p = ops.gemm_partial(x, w.lm_head, out=self.partial)
             ops.gemm_argmax(p, out=self.argmax[:n], scratch=self.amx_scratch)
+        elif head == "sample":
+            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
+            ops.gemm_sample(p, self.pos, state, self.temperature, self.sample_seed, out=self.argmax[:n],
+                            scratch=self.amx_scratch)
         elif head == "logits":
             p = ops.gemm_partial(x, w.lm_head, out=self.partial)
             self.logits = ops.gemm_reduce(p)

@@ -79,6 +79,16 @@ def argmax_from_keys(keys: torch.Tensor, m: int, out: torch.Tensor) -> torch.Ten
     return out
 
 
+def gemm_sample(p: PartialOut, pos: torch.Tensor, state: torch.Tensor | None, temperature: float, seed: int,
+                out: torch.Tensor, scratch: torch.Tensor) -> torch.Tensor:
+    """Per-row temperature sample (Gumbel-max keyed by (seed, c + pos[row], vocab index))."""
+    s = p.sched
+    _lib.call("bst_gemm_sample", p.buf.data_ptr(), C.byref(s), scratch.data_ptr(), out.data_ptr(), pos.data_ptr(),
+              None if state is None else state.data_ptr(), 0, float(temperature), int(seed) & ((1 << 64) - 1),
+              stream_ptr())
+    return out
+
+
 def gemm_argmax(p: PartialOut, out: torch.Tensor | None = None, scratch: torch.Tensor | None = None) -> torch.Tensor:
     s = p.sched
     out = out if out is not None else torch.empty(s.m, dtype=torch.int32, device=p.buf.device)

@@ -215,8 +215,11 @@ def verify_tree(lin: LinearizedTree, tree: DraftTree, target, temperature: float
         raise ValueError("temperature must be >= 0")
     if len(lin.tokens) != len(tree.nodes):
         raise ValueError("linearization does not match the tree")
-    if temperature == 0.0 and hasattr(target, "tree_argmax"):
-        argmax = target.tree_argmax(tree, tuple(prefix))  # one batched verify pass, int32[t] on device
+    batched = hasattr(target, "tree_argmax") if temperature == 0.0 else hasattr(target, "tree_sample")
+    if batched:
+        # one batched verify pass, int32[t] on device: the target's token after every node
+        argmax = (target.tree_argmax(tree, tuple(prefix)) if temperature == 0.0
+                  else target.tree_sample(tree, tuple(prefix), temperature))
         token, start, kids = _device_children(tree)
         max_path = tree.lattice.gamma + 1
         path, _, meta = accept_device(token, start, kids, argmax, max_path)

@@ -177,3 +177,71 @@ def test_graph_and_eager_cycles_agree(eng):
         out.append(eng.run(20)[1])
     eng.use_graphs = True
     assert out[0] == out[1]
+
+
+def test_sampled_tree_decode_preserves_ar_samples(eng):
+    """T > 0 exact-match verification (verify_sim.py:111-126): with Gumbel noise keyed by
+    (seed, absolute position), tree decode with compaction == the sampled AR decode."""
+    prompt = _prompt(70, eng.cfg.V, seed=5)
+    eng.set_temperature(0.8, 11)
+    try:
+        eng.reset(prompt)
+        ar = eng.ar_decode(60)
+        eng.reset(prompt)
+        eng.set_policy("fixed", n=48)
+        eng.draft_override = _decoy_drafter(ar, GAMMA, eng.cfg.V, 1)
+        stats, toks = eng.run(45)
+    finally:
+        eng.draft_override = None
+        eng.set_temperature(0.0, 0)
+    assert toks[:45] == ar[:45]
+    assert max(s.accepted_len for s in stats) > 3
+    eng.reset(prompt)
+    assert eng.ar_decode(60) != ar  # the sampling path really ran
+
+
+class _Plugin:
+    """The reference plugin protocol only (no engine_decode): forces the façade's general loop."""
+
+    def __init__(self, e):
+        self.e = e
+
+    def drafter_marginals(self, prefix):
+        return self.e.drafter_marginals(prefix)
+
+    def tree_argmax(self, tree, prefix):
+        return self.e.tree_argmax(tree, prefix)
+
+    def tree_sample(self, tree, prefix, temperature):
+        return self.e.tree_sample(tree, prefix, temperature)
+
+    def next_token(self, prefix, temperature):
+        return self.e.next_token(prefix, temperature)
+
+
+@pytest.mark.parametrize("temperature", [0.0, 0.9])
+def test_general_facade_loop_matches_engine_fast_path(eng, temperature):
+    import paper_2605_29727_b200 as P
+    prompt = _prompt(50, eng.cfg.V, seed=6)
+    est = P.VerifyLatencyEstimator(eng.cfg.cost_params(1.6e15, 6.5e12))
+    lat = P.CycleLatencies(t_draft=3e-4, t_aux=0.0, l_ar=1e-3)
+    sim = P.SimConfig(controller=P.ControllerConfig(n_max=32, latencies=lat, variant="static",
+                                                    context_len=len(prompt) - 1), run_length=40, top_k=eng.top_k,
+                      temperature=temperature)
+    eng.set_temperature(0.0, 3)
+    try:
+        eng.reset(prompt)
+        rec_fast, tok_fast = P.decode_full(eng, sim, P.Policy.fixed(24), est)
+        eng.reset(prompt)
+        rec_gen, tok_gen = P.decode_full(_Plugin(eng), sim, P.Policy.fixed(24), est)
+        assert tuple(tok_gen) == tuple(tok_fast)
+        assert [r.accepted_len for r in rec_gen] == [r.accepted_len for r in rec_fast]
+        assert [r.tree_size for r in rec_gen] == [r.tree_size for r in rec_fast]
+        # the reference's AR baseline through next_token (lazy commit of each token)
+        eng.reset(prompt)
+        ar = P.ar_decode(_Plugin(eng), 12, temperature)
+        eng.set_temperature(temperature, 3)
+        eng.reset(prompt)
+        assert list(ar) == eng.ar_decode(12)
+    finally:
+        eng.set_temperature(0.0, 0)
