@@ -19,6 +19,8 @@
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
+#include <stdlib.h>
+
 #include <mutex>
 #include <unordered_map>
 
@@ -142,13 +144,14 @@ __device__ __forceinline__ bool next_seg(const bst_gemm_sched_t& s, int64_t& u, 
 
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
-                     bst_gemm_sched_t s, float* __restrict__ partial, int stages) {
+                     bst_gemm_sched_t s, float* __restrict__ partial, int stages, int trigger) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[G_MAX_STAGES], empty[G_MAX_STAGES], tfull[2], tempty[2];
   __shared__ uint32_t tmem_base_sh;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) gtrace(0);
+  if (trigger) sm100::grid_dep_launch();
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
   const int bn = s.bn;
@@ -446,7 +449,12 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   while (tc < 2 * s.bn) tc <<= 1;
   s.tmem_cols = tc;
   const int stage_bytes = G_TILE_W + s.bn * G_BK * 2;
-  int stages = (G_SMEM_BUDGET - 1024) / stage_bytes;
+  static int budget = 0;
+  if (!budget) {
+    const char* e = getenv("BST_GEMM_SMEM_KB");  // measurement knob
+    budget = e ? atoi(e) * 1024 : G_SMEM_BUDGET;
+  }
+  int stages = (budget - 1024) / stage_bytes;
   s.stages = stages > G_MAX_STAGES ? G_MAX_STAGES : stages;
   s.partial_floats = (int64_t)s.n_mt * s.s_max * s.bn * G_BM;
   *out = s;
@@ -481,7 +489,13 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  BST_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel, tw, tx, s, partial, (int)s.stages));
+  // PDL trigger at CTA entry: a PDL-launched successor (the next GEMM, which waits on
+  // griddepcontrol.wait before loading X) is scheduled as soon as SMs free up instead of
+  // after this grid retires; plain-launched epilogues still wait for completion.
+  // BST_GEMM_TRIGGER=0 disables it (measurement).
+  static int trigger = -1;
+  if (trigger < 0) trigger = getenv("BST_GEMM_TRIGGER") ? atoi(getenv("BST_GEMM_TRIGGER")) : 1;
+  BST_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel, tw, tx, s, partial, (int)s.stages, trigger));
   return BST_OK;
 }
 
