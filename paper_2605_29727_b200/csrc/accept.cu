@@ -18,6 +18,7 @@ namespace bst {
 __global__ void accept_kernel(const int32_t* __restrict__ token, const int32_t* __restrict__ child_start,
                               const int32_t* __restrict__ child_list, const int32_t* __restrict__ argmax,
                               int max_path, int32_t* path, int32_t* committed, int32_t* meta) {
+  pdl_enter();
   const int lane = threadIdx.x;
   int cur = 0, len = 1, bonus = -1;
   if (lane == 0) path[0] = 0;
@@ -55,6 +56,7 @@ __global__ void accept_kernel(const int32_t* __restrict__ token, const int32_t* 
 __global__ void kv_compact_kernel(__nv_bfloat16* kv, int n_kv, int head_dim, int page_size, int64_t layer_stride,
                                   const int32_t* __restrict__ page_table, const int32_t* __restrict__ c_dev,
                                   const int32_t* __restrict__ path, const int32_t* __restrict__ meta, int max_path) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char stage_raw[];
   const int len = meta[0];
   if (len <= 1) return;
@@ -87,6 +89,7 @@ __global__ void kv_compact_kernel(__nv_bfloat16* kv, int n_kv, int head_dim, int
 
 __global__ void linearize_mask_kernel(const uint32_t* __restrict__ anc, int mask_words, int t, int prefix_len,
                                       uint8_t* mask) {
+  pdl_enter();
   const int64_t n = (int64_t)prefix_len + t;
   const int64_t row = blockIdx.x;
   uint8_t* out = mask + row * n;
@@ -112,8 +115,8 @@ extern "C" int bst_accept(const int32_t* token, const int32_t* child_start, cons
                           bst_stream_t stream) {
   BST_REQUIRE(token && child_start && child_list && argmax && path && committed && meta, "null pointer argument");
   BST_REQUIRE(max_path >= 1, "max_path must be >= 1");
-  bst::accept_kernel<<<1, 32, 0, bst::as_stream(stream)>>>(token, child_start, child_list, argmax, max_path, path,
-                                                            committed, meta);
+  BST_CUDA(bst::launch_pdl(bst::accept_kernel, dim3(1), dim3(32), 0, bst::as_stream(stream), token, child_start, child_list, argmax, max_path, path,
+                                                            committed, meta));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -126,9 +129,9 @@ extern "C" int bst_kv_compact(void* kv, int n_layers, int n_kv, int head_dim, in
   BST_REQUIRE(n_layers >= 1 && n_kv >= 1 && page_size >= 1 && max_path >= 1, "bad shape");
   const size_t smem = (size_t)max_path * head_dim * 2;
   BST_REQUIRE(smem <= 48 * 1024, "max_path*head_dim too large");
-  bst::kv_compact_kernel<<<n_layers * 2 * n_kv, 128, smem, bst::as_stream(stream)>>>(
+  BST_CUDA(bst::launch_pdl(bst::kv_compact_kernel, dim3(n_layers * 2 * n_kv), dim3(128), smem, bst::as_stream(stream), 
       static_cast<__nv_bfloat16*>(kv), n_kv, head_dim, page_size, layer_stride_elems, page_table, c_dev, path, meta,
-      max_path);
+      max_path));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -140,13 +143,14 @@ extern "C" int bst_linearize_mask(const uint32_t* anc_mask, int mask_words, int 
   BST_REQUIRE((int64_t)mask_words * 32 >= t, "mask_words too small");
   const int64_t n = (int64_t)prefix_len + t;
   BST_REQUIRE(n < (1ll << 31), "mask too large");
-  bst::linearize_mask_kernel<<<(unsigned)n, 256, 0, bst::as_stream(stream)>>>(anc_mask, mask_words, t, prefix_len, mask);
+  BST_CUDA(bst::launch_pdl(bst::linearize_mask_kernel, dim3((unsigned)n), dim3(256), 0, bst::as_stream(stream), anc_mask, mask_words, t, prefix_len, mask));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
 
 namespace bst {
 __global__ void ancestor_mask_kernel(const int32_t* __restrict__ parent, int t, int mask_words, uint32_t* mask) {
+  pdl_enter();
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < t; i += gridDim.x * blockDim.x) {
     uint32_t* row = mask + (size_t)i * mask_words;
     for (int w = 0; w < mask_words; ++w) row[w] = 0u;
@@ -159,7 +163,7 @@ __global__ void ancestor_mask_kernel(const int32_t* __restrict__ parent, int t, 
 extern "C" int bst_ancestor_mask(const int32_t* parent, int t, int mask_words, uint32_t* mask, bst_stream_t stream) {
   BST_REQUIRE(parent && mask, "null pointer argument");
   BST_REQUIRE(t >= 1 && (int64_t)mask_words * 32 >= t, "bad shape");
-  bst::ancestor_mask_kernel<<<(t + 255) / 256, 256, 0, bst::as_stream(stream)>>>(parent, t, mask_words, mask);
+  BST_CUDA(bst::launch_pdl(bst::ancestor_mask_kernel, dim3((t + 255) / 256), dim3(256), 0, bst::as_stream(stream), parent, t, mask_words, mask));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

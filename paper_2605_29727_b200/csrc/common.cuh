@@ -70,4 +70,28 @@ __host__ __device__ inline double curve_latency(const bst_curve_t& c, long long 
 // Pending L2-prefetch hint (bst_set_prefetch) consumed by the next K3/K5 launch.
 bst_prefetch_t take_prefetch();
 
+// Programmatic dependent launch (PDL) of the small kernels: every such kernel starts
+// with pdl_enter() (griddepcontrol.launch_dependents, then griddepcontrol.wait before
+// any global access), so its CTAs may become resident while the predecessor drains and
+// the next PDL kernel may be scheduled early.  BST_PDL=0 disables it (measurement).
+int pdl_enabled();
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+template <typename... K, typename... A>
+inline cudaError_t launch_pdl(void (*kern)(K...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, static_cast<K>(args)...);
+}
+
 }  // namespace bst

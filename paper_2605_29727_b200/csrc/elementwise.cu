@@ -11,6 +11,8 @@
 //   swiglu            act = silu(gate) * up  (gate/up = one fused GEMM)
 //   gather_rows       rows[path[i]] -> dst[i]  (accepted-path hidden features)
 #include <climits>
+#include <cstdlib>
+#include <utility>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -20,6 +22,7 @@
 namespace bst {
 
 constexpr int E_THREADS = 256;
+
 
 __device__ __forceinline__ float block_sum(float v, float* sh) {
   v = warp_sum(v);
@@ -42,7 +45,7 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ emb, int h,
                                      const __nv_bfloat16* __restrict__ w, float eps, float* __restrict__ resid,
                                      __nv_bfloat16* __restrict__ x, int64_t ldx) {
-  sm100::grid_dep_launch();
+  pdl_enter();
   __shared__ float sh[32];
   const int t = blockIdx.x;
   const int64_t tok = tokens[t];
@@ -66,6 +69,7 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
     float eps, __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf, int rows, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
+  sm100::grid_dep_wait();  // PDL launch: the producer GEMM's partials are complete past this point
   __shared__ float sh[32];
   __shared__ float4 vals[2048];
   const int t = blockIdx.x;
@@ -111,6 +115,7 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
                                 int req_rows, int req_span, int req_state, int req_slots) {
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
+  sm100::grid_dep_wait();
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -176,6 +181,7 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
   const int t = blockIdx.y;
   sm100::grid_dep_launch();
+  sm100::grid_dep_wait();
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (ffn >> 2); g += gridDim.x * blockDim.x) {
     const float4 gt = gemm_load4(partial, s, t, g * 4);
     const float4 up = gemm_load4(partial, s, t, ffn + g * 4);
@@ -190,6 +196,7 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx,
                                    const int32_t* __restrict__ count, int max_rows, int cols,
                                    __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+  pdl_enter();
   const int r = blockIdx.x;
   const int n = count ? *count : max_rows;
   const int4* sp = reinterpret_cast<const int4*>(src + (int64_t)(r < n ? idx[r] : 0) * lds);
@@ -205,9 +212,9 @@ using namespace bst;
 extern "C" int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* emb, int h, const void* w, float eps,
                                  float* resid, void* x, int64_t ldx, bst_stream_t stream) {
   BST_REQUIRE(tokens && emb && w && resid && x, "null pointer argument");
-  embed_rmsnorm_kernel<<<rows, E_THREADS, 0, as_stream(stream)>>>(
+  BST_CUDA(launch_pdl(embed_rmsnorm_kernel, dim3(rows), dim3(E_THREADS), 0, as_stream(stream), 
       tokens, static_cast<const __nv_bfloat16*>(emb), h, static_cast<const __nv_bfloat16*>(w), eps, resid,
-      static_cast<__nv_bfloat16*>(x), ldx);
+      static_cast<__nv_bfloat16*>(x), ldx));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -219,9 +226,9 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   BST_REQUIRE(!partial || sched, "partial without schedule");
   bst_gemm_sched_t s{};
   if (sched) s = *sched;
-  residual_rmsnorm_kernel<<<rows, R_THREADS, 0, as_stream(stream)>>>(
-      partial, s, resid, h, static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
-      static_cast<__nv_bfloat16*>(feat), ldf, rows, take_prefetch());
+  BST_CUDA(launch_pdl(residual_rmsnorm_kernel, dim3(rows), dim3(R_THREADS), 0, as_stream(stream), partial, s, resid, h,
+                      static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
+                      static_cast<__nv_bfloat16*>(feat), ldf, rows, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -235,10 +242,11 @@ extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* 
   BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
               "null pointer argument");
   BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
-  qkv_rope_kernel<<<rows, 512, 0, as_stream(stream)>>>(
-      partial, *sched, n_q, n_kv, static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm),
-      eps, inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride, static_cast<__nv_bfloat16*>(kv),
-      layer_off_elems, page_table, page_size, state, state_c_idx, take_prefetch(), req_rows, req_span > 0 ? req_span : 1, req_state, req_slots);
+  BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows), dim3(512), 0, as_stream(stream), partial, *sched, n_q, n_kv,
+                      static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm), eps,
+                      inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride,
+                      static_cast<__nv_bfloat16*>(kv), layer_off_elems, page_table, page_size, state, state_c_idx,
+                      take_prefetch(), req_rows, req_span > 0 ? req_span : 1, req_state, req_slots));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -258,8 +266,8 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
   BST_REQUIRE(partial && sched && act, "null pointer argument");
   BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
   dim3 grid((ffn / 4 + 255) / 256, rows);
-  swiglu_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, *sched, ffn, static_cast<__nv_bfloat16*>(act), lda,
-                                                     take_prefetch());
+  BST_CUDA(launch_pdl(swiglu_kernel, grid, dim3(256), 0, as_stream(stream), partial, *sched, ffn,
+                      static_cast<__nv_bfloat16*>(act), lda, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -268,8 +276,8 @@ extern "C" int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx,
                                int cols, void* dst, int64_t ldd, bst_stream_t stream) {
   BST_REQUIRE(src && idx && dst, "null pointer argument");
   BST_REQUIRE(cols % 8 == 0 && lds % 8 == 0 && ldd % 8 == 0, "rows must be 16-byte multiples");
-  gather_rows_kernel<<<max_rows, 256, 0, as_stream(stream)>>>(static_cast<const __nv_bfloat16*>(src), lds, idx, count,
-                                                              max_rows, cols, static_cast<__nv_bfloat16*>(dst), ldd);
+  BST_CUDA(launch_pdl(gather_rows_kernel, dim3(max_rows), dim3(256), 0, as_stream(stream), static_cast<const __nv_bfloat16*>(src), lds, idx, count,
+                                                              max_rows, cols, static_cast<__nv_bfloat16*>(dst), ldd));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -278,6 +286,7 @@ extern "C" int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx,
 namespace bst {
 __global__ void verify_rows_kernel(const int32_t* state, const int32_t* tree_token, const int32_t* tree_depth,
                                    const int32_t* meta, int rows, int32_t* tokens, int32_t* pos, int32_t* slot) {
+  pdl_enter();
   const int n = meta[0];
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < rows; i += gridDim.x * blockDim.x) {
     const bool real = i <= n;
@@ -288,6 +297,7 @@ __global__ void verify_rows_kernel(const int32_t* state, const int32_t* tree_tok
 }
 __global__ void drafter_rows_kernel(const int32_t* state, int gamma, int mask_token, int ctx_rows, int32_t* tokens,
                                     int32_t* pos, int32_t* slot, int32_t* qrow) {
+  pdl_enter();
   const int n_new = state[BST_ST_NNEW];
   const int i = threadIdx.x;
   if (i <= gamma) {
@@ -307,6 +317,7 @@ __global__ void drafter_rows_kernel(const int32_t* state, int gamma, int mask_to
 // ctx_rows context rows at [n_req*(gamma+1) + r*ctx_rows, ...); qrow = the q-buffer row
 __global__ void drafter_rows_batch_kernel(const int32_t* state, int req_state, int n_req, int gamma, int mask_token,
                                           int ctx_rows, int32_t* tokens, int32_t* pos, int32_t* slot, int32_t* qrow) {
+  pdl_enter();
   const int r = blockIdx.x;
   const int n_new = state[r * req_state + BST_ST_NNEW];
   const int i = threadIdx.x;
@@ -328,6 +339,7 @@ __global__ void drafter_rows_batch_kernel(const int32_t* state, int req_state, i
 __global__ void commit_state_kernel(int32_t* state, const int32_t* meta, const int32_t* committed, int max_path,
                                     int32_t* out_tokens, int out_cap, const int32_t* tree_meta,
                                     const double* surrogate, int32_t* log_i32, double* log_f64, int log_cap) {
+  pdl_enter();
   const int len = meta[0];
   const int base = state[BST_ST_COMMITTED];
   for (int i = threadIdx.x; i < len && i < max_path; i += blockDim.x)
@@ -357,8 +369,8 @@ extern "C" int bst_verify_rows(const int32_t* state, const int32_t* tree_token, 
                                const int32_t* meta, int rows, int32_t* tokens, int32_t* pos, int32_t* slot,
                                bst_stream_t stream) {
   BST_REQUIRE(state && tree_token && tree_depth && meta && tokens && pos && slot, "null pointer argument");
-  verify_rows_kernel<<<(rows + 255) / 256, 256, 0, as_stream(stream)>>>(state, tree_token, tree_depth, meta, rows,
-                                                                        tokens, pos, slot);
+  BST_CUDA(launch_pdl(verify_rows_kernel, dim3((rows + 255) / 256), dim3(256), 0, as_stream(stream), state, tree_token, tree_depth, meta, rows,
+                                                                        tokens, pos, slot));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -367,7 +379,7 @@ extern "C" int bst_drafter_rows(const int32_t* state, int gamma, int mask_token,
                                 int32_t* pos, int32_t* slot, int32_t* qrow, bst_stream_t stream) {
   BST_REQUIRE(state && tokens && pos && slot && qrow, "null pointer argument");
   BST_REQUIRE(gamma + 1 + ctx_rows <= 1024, "too many drafter rows");
-  drafter_rows_kernel<<<1, 1024, 0, as_stream(stream)>>>(state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow);
+  BST_CUDA(launch_pdl(drafter_rows_kernel, dim3(1), dim3(1024), 0, as_stream(stream), state, gamma, mask_token, ctx_rows, tokens, pos, slot, qrow));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -377,8 +389,8 @@ extern "C" int bst_drafter_rows_batch(const int32_t* state, int req_state, int n
                                       bst_stream_t stream) {
   BST_REQUIRE(state && tokens && pos && slot && qrow && n_req >= 1, "null pointer argument");
   BST_REQUIRE(gamma + 1 + ctx_rows <= 1024, "too many drafter rows");
-  drafter_rows_batch_kernel<<<n_req, 1024, 0, as_stream(stream)>>>(state, req_state, n_req, gamma, mask_token, ctx_rows,
-                                                                   tokens, pos, slot, qrow);
+  BST_CUDA(launch_pdl(drafter_rows_batch_kernel, dim3(n_req), dim3(1024), 0, as_stream(stream), state, req_state, n_req, gamma, mask_token, ctx_rows,
+                                                                   tokens, pos, slot, qrow));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -387,8 +399,8 @@ extern "C" int bst_commit_state(int32_t* state, const int32_t* accept_meta, cons
                                 int32_t* out_tokens, int out_cap, const int32_t* tree_meta, const double* surrogate,
                                 int32_t* log_i32, double* log_f64, int log_cap, bst_stream_t stream) {
   BST_REQUIRE(state && accept_meta && committed && out_tokens, "null pointer argument");
-  commit_state_kernel<<<1, 128, 0, as_stream(stream)>>>(state, accept_meta, committed, max_path, out_tokens, out_cap,
-                                                        tree_meta, surrogate, log_i32, log_f64, log_cap);
+  BST_CUDA(launch_pdl(commit_state_kernel, dim3(1), dim3(128), 0, as_stream(stream), state, accept_meta, committed, max_path, out_tokens, out_cap,
+                                                        tree_meta, surrogate, log_i32, log_f64, log_cap));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

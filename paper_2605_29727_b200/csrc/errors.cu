@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Error reporting + ABI version for the bastion C ABI.
 #include <stdarg.h>
 
@@ -30,3 +31,14 @@ extern "C" int bst_set_prefetch(const bst_prefetch_t* pf) {
   bst::g_pf = pf ? *pf : bst_prefetch_t{};
   return BST_OK;
 }
+
+namespace bst {
+int pdl_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BST_PDL");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
+}  // namespace bst

@@ -638,6 +638,7 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
     expand_best_first_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
                              bst_plan_t plan_in, const bst_plan_t* plan_dev, int n_cap, bst_tree_t out, ExWs ws,
                              int heap_in_smem) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
   const bst_plan_t plan = resolve_plan(plan_in, plan_dev);
@@ -704,6 +705,7 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
 __global__ void __launch_bounds__(EX_THREADS, 1)
     expand_beam_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
                        bst_plan_t plan, int n_cap, bst_tree_t out, ExWs ws) {
+  pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
   __shared__ int s_next_id, s_surv_lo, s_surv_hi;
@@ -819,11 +821,11 @@ extern "C" int bst_expand(const int32_t* tok, const double* prob, int gamma, int
   }
   cudaStream_t st = as_stream(stream);
   if (p.policy == BST_POLICY_BEAM) {
-    expand_beam_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, n_cap, *out, w);
+    BST_CUDA(launch_pdl(expand_beam_kernel, dim3(1), dim3(EX_THREADS), smem, st, tok, prob, gamma, k, p, n_cap, *out, w));
   } else {
     const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
-    expand_best_first_kernel<<<1, EX_THREADS, smem, st>>>(tok, prob, gamma, k, p, nullptr, n_cap, *out, w,
-                                                          heap_in_smem);
+    BST_CUDA(launch_pdl(expand_best_first_kernel, dim3(1), dim3(EX_THREADS), smem, st, tok, prob, gamma, k, p, nullptr, n_cap, *out, w,
+                                                          heap_in_smem));
   }
   BST_LAUNCH_CHECK();
   return BST_OK;
@@ -852,8 +854,8 @@ extern "C" int bst_expand_dev(const int32_t* tok, const double* prob, int gamma,
   p.policy = policy;
   p.n_max = n_max;
   const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
-  expand_best_first_kernel<<<1, EX_THREADS, smem, as_stream(stream)>>>(tok, prob, gamma, k, p, plan_dev, n_cap, *out,
-                                                                        w, heap_in_smem);
+  BST_CUDA(launch_pdl(expand_best_first_kernel, dim3(1), dim3(EX_THREADS), smem, as_stream(stream), tok, prob, gamma, k, p, plan_dev, n_cap, *out,
+                                                                        w, heap_in_smem));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

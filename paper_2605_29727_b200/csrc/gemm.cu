@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 // ------------------------------------------------------ reduction kernels
 __global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* y_f32,
                                    __nv_bfloat16* y_bf16, int64_t ldy) {
+  pdl_enter();
   const int t = blockIdx.y;
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g * 4 < s.n_out; g += gridDim.x * blockDim.x) {
     const int n0 = g * 4;
@@ -317,6 +318,7 @@ __global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_s
 // vocab_offset: global index of output column 0 (vocab-parallel LM head shards).
 __global__ void gemm_argmax_kernel(const float* __restrict__ partial, bst_gemm_sched_t s,
                                    unsigned long long* best, int vocab_offset = 0) {
+  pdl_enter();
   const int t = blockIdx.y;
   unsigned long long key = 0;
   auto consider = [&](float v, int n) {
@@ -369,6 +371,7 @@ __device__ __forceinline__ float gumbel_of(uint32_t x) {
 __global__ void gemm_sample_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, unsigned long long* best,
                                    const int32_t* __restrict__ pos, const int32_t* __restrict__ state, int c_idx,
                                    float inv_t, uint2 seed) {
+  pdl_enter();
   const int t = blockIdx.y;
   const uint32_t apos = (uint32_t)((state ? state[c_idx] : 0) + pos[t]);
   unsigned long long key = 0;
@@ -401,16 +404,19 @@ __global__ void gemm_sample_kernel(const float* __restrict__ partial, bst_gemm_s
 }
 
 __global__ void argmax_finalize_kernel(const unsigned long long* best, int m, int32_t* out) {
+  pdl_enter();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(best[t] & 0xFFFFFFFFull));
 }
 // packed keys <-> signed int64 (flip the top bit) so a signed MAX all-reduce (NCCL int64)
 // orders them exactly as the unsigned comparison above
 __global__ void argmax_key_flip_kernel(unsigned long long* keys, int m) {
+  pdl_enter();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) keys[t] ^= 0x8000000000000000ull;
 }
 __global__ void argmax_from_signed_kernel(const unsigned long long* keys, int m, int32_t* out) {
+  pdl_enter();
   int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t < m) out[t] = (int32_t)(0xFFFFFFFFu - (unsigned)(keys[t] & 0xFFFFFFFFull));
 }
@@ -505,8 +511,8 @@ extern "C" int bst_gemm_reduce(const float* partial, const bst_gemm_sched_t* sch
   BST_REQUIRE(partial && sched && (y_f32 || y_bf16), "null pointer argument");
   const bst_gemm_sched_t s = *sched;
   dim3 grid((s.n_out / 4 + 255) / 256 < 148 ? (s.n_out / 4 + 255) / 256 + 1 : 148, s.m);
-  gemm_reduce_kernel<<<grid, 256, 0, as_stream(stream)>>>(partial, s, y_f32,
-                                                          static_cast<__nv_bfloat16*>(y_bf16), ldy);
+  BST_CUDA(launch_pdl(gemm_reduce_kernel, dim3(grid), dim3(256), 0, as_stream(stream), partial, s, y_f32,
+                                                          static_cast<__nv_bfloat16*>(y_bf16), ldy));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -519,9 +525,9 @@ extern "C" int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sch
   cudaStream_t st = as_stream(stream);
   BST_CUDA(cudaMemsetAsync(scratch_u64, 0, sizeof(unsigned long long) * s.m, st));
   dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
-  gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64));
-  argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m,
-                                                            argmax);
+  BST_CUDA(launch_pdl(gemm_argmax_kernel, dim3(grid), dim3(256), 0, st, partial, s, static_cast<unsigned long long*>(scratch_u64), 0));
+  BST_CUDA(launch_pdl(argmax_finalize_kernel, dim3((s.m + 127) / 128), dim3(128), 0, st, static_cast<unsigned long long*>(scratch_u64), s.m,
+                                                            argmax));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -537,10 +543,10 @@ extern "C" int bst_gemm_sample(const float* partial, const bst_gemm_sched_t* sch
   cudaStream_t st = as_stream(stream);
   BST_CUDA(cudaMemsetAsync(scratch_u64, 0, sizeof(unsigned long long) * s.m, st));
   dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
-  gemm_sample_kernel<<<grid, 256, 0, st>>>(partial, s, static_cast<unsigned long long*>(scratch_u64), pos, state,
+  BST_CUDA(launch_pdl(gemm_sample_kernel, dim3(grid), dim3(256), 0, st, partial, s, static_cast<unsigned long long*>(scratch_u64), pos, state,
                                            c_idx, 1.f / temperature,
-                                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)));
-  argmax_finalize_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(static_cast<unsigned long long*>(scratch_u64), s.m, out);
+                                           make_uint2((uint32_t)seed, (uint32_t)(seed >> 32))));
+  BST_CUDA(launch_pdl(argmax_finalize_kernel, dim3((s.m + 127) / 128), dim3(128), 0, st, static_cast<unsigned long long*>(scratch_u64), s.m, out));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -557,8 +563,8 @@ extern "C" int bst_gemm_argmax_keys(const float* partial, const bst_gemm_sched_t
   BST_CUDA(cudaMemsetAsync(keys, 0, sizeof(int64_t) * s.m, st));
   dim3 grid(s.n_out / 4 / 256 < 74 ? s.n_out / 4 / 256 + 1 : 74, s.m);
   unsigned long long* k = reinterpret_cast<unsigned long long*>(keys);
-  gemm_argmax_kernel<<<grid, 256, 0, st>>>(partial, s, k, vocab_offset);
-  argmax_key_flip_kernel<<<(s.m + 127) / 128, 128, 0, st>>>(k, s.m);
+  BST_CUDA(launch_pdl(gemm_argmax_kernel, dim3(grid), dim3(256), 0, st, partial, s, k, vocab_offset));
+  BST_CUDA(launch_pdl(argmax_key_flip_kernel, dim3((s.m + 127) / 128), dim3(128), 0, st, k, s.m));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -568,8 +574,8 @@ extern "C" int bst_argmax_from_keys(const int64_t* keys, int m, int32_t* argmax,
   using namespace bst;
   BST_REQUIRE(keys && argmax && m >= 0, "bad arguments");
   if (m == 0) return BST_OK;
-  argmax_from_signed_kernel<<<(m + 127) / 128, 128, 0, as_stream(stream)>>>(
-      reinterpret_cast<const unsigned long long*>(keys), m, argmax);
+  BST_CUDA(launch_pdl(argmax_from_signed_kernel, dim3((m + 127) / 128), dim3(128), 0, as_stream(stream), 
+      reinterpret_cast<const unsigned long long*>(keys), m, argmax));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -72,6 +72,7 @@ __device__ __forceinline__ bool better(double pa, int ta, double pb, int tb) {
 // --- A: chunk max ----------------------------------------------------------
 __global__ void __launch_bounds__(TK_THREADS) k1_chunk_max(const void* logits, int dtype, int vocab,
                                                            int64_t stride, float* pmax) {
+  pdl_enter();
   const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
   const int64_t base = (int64_t)row * stride;
   float m = -INFINITY;
@@ -102,6 +103,7 @@ __device__ __forceinline__ float row_max(const float* pmax, int row, int chunks)
 __global__ void __launch_bounds__(TK_THREADS) k1_chunk_sum(const void* logits, int dtype, int vocab,
                                                            int64_t stride, const float* pmax,
                                                            double* psum) {
+  pdl_enter();
   const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
   __shared__ float sm_m;
   if (threadIdx.x == 0) sm_m = row_max(pmax, row, chunks);
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_chunk_select(const void* logits
                                                               const double* psum, int k,
                                                               double* probs_full, double* cprob,
                                                               int32_t* ctok) {
+  pdl_enter();
   const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
   __shared__ double sm_z;
   __shared__ float sm_m;
@@ -222,6 +225,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_chunk_select(const void* logits
 // --- D: merge chunk candidates of one row ----------------------------------
 __global__ void __launch_bounds__(TK_THREADS) k1_merge(const double* cprob, const int32_t* ctok, int chunks,
                                                        int k, int32_t* tok_out, double* prob_out) {
+  pdl_enter();
   const int row = blockIdx.x;
   const int n = chunks * k;
   double p[TK_PER_THREAD];
@@ -296,6 +300,7 @@ __device__ void block_top_keys(unsigned long long (&c)[TK_PER_THREAD], int n, un
 __global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(const void* logits, int dtype, int vocab, int64_t stride,
                                                             int kp, float* pmax, double* psum,
                                                             unsigned long long* ckeys) {
+  pdl_enter();
   const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
   const int64_t base = (int64_t)row * stride;
   float l[TK_PER_THREAD];
@@ -348,6 +353,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax
                                                                const unsigned long long* ckeys, int chunks, int kp,
                                                                int k, int32_t* tok_out, double* prob_out,
                                                                double* stats, int* fallback) {
+  pdl_enter();
   const int row = blockIdx.x;
   const int n = chunks * kp;
   unsigned long long c[TK_PER_THREAD];
@@ -403,6 +409,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax
 // Full fp64 rows (MarginalBlock export) with the same m and Z.
 __global__ void __launch_bounds__(TK_THREADS) k1_full_rows(const void* logits, int dtype, int vocab, int64_t stride,
                                                            const double* stats, double* probs_full) {
+  pdl_enter();
   const int row = blockIdx.y;
   const double m = stats[row * 2], z = stats[row * 2 + 1];
   for (int v = blockIdx.x * TK_THREADS + threadIdx.x; v < vocab; v += gridDim.x * TK_THREADS)
@@ -415,6 +422,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_full_rows(const void* logits, i
 __global__ void __launch_bounds__(TK_THREADS) k1_fast_fallback(const void* logits, int dtype, int vocab,
                                                                int64_t stride, const double* stats, const int* fallback,
                                                                int k, int32_t* tok_out, double* prob_out) {
+  pdl_enter();
   const int row = blockIdx.x;
   if (!fallback[row]) return;
   const double m = stats[row * 2], z = stats[row * 2 + 1];
@@ -476,22 +484,22 @@ static int run_topk(const void* logits, int dtype, const double* probs_in, int g
   dim3 grid(chunks, gamma);
   const int kp = k + 1 <= vocab ? k + 1 : k;
   if (probs_in == nullptr && kp < TK_KP_MAX && (int64_t)chunks * kp <= TK_CHUNK) {
-    k1_fast_chunk<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, kp, w.pmax, w.psum, w.ckeys);
-    k1_fast_finalize<<<gamma, TK_THREADS, 0, st>>>(w.pmax, w.psum, w.ckeys, chunks, kp, k, tok, prob, w.stats,
-                                                   w.fallback);
-    k1_fast_fallback<<<gamma, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.stats, w.fallback, k, tok, prob);
-    if (probs_full) k1_full_rows<<<dim3(chunks, gamma), TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.stats,
-                                                                            probs_full);
+    BST_CUDA(launch_pdl(k1_fast_chunk, dim3(grid), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, kp, w.pmax, w.psum, w.ckeys));
+    BST_CUDA(launch_pdl(k1_fast_finalize, dim3(gamma), dim3(TK_THREADS), 0, st, w.pmax, w.psum, w.ckeys, chunks, kp, k, tok, prob, w.stats,
+                                                   w.fallback));
+    BST_CUDA(launch_pdl(k1_fast_fallback, dim3(gamma), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.stats, w.fallback, k, tok, prob));
+    if (probs_full) BST_CUDA(launch_pdl(k1_full_rows, dim3(dim3(chunks, gamma)), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.stats,
+                                                                            probs_full));
     BST_LAUNCH_CHECK();
     return BST_OK;
   }
   if (probs_in == nullptr) {
-    k1_chunk_max<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax);
-    k1_chunk_sum<<<grid, TK_THREADS, 0, st>>>(logits, dtype, vocab, stride, w.pmax, w.psum);
+    BST_CUDA(launch_pdl(k1_chunk_max, dim3(grid), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.pmax));
+    BST_CUDA(launch_pdl(k1_chunk_sum, dim3(grid), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.pmax, w.psum));
   }
-  k1_chunk_select<<<grid, TK_THREADS, 0, st>>>(logits, dtype, probs_in, vocab, stride, w.pmax, w.psum, k,
-                                               probs_full, w.cprob, w.ctok);
-  k1_merge<<<gamma, TK_THREADS, 0, st>>>(w.cprob, w.ctok, chunks, k, tok, prob);
+  BST_CUDA(launch_pdl(k1_chunk_select, dim3(grid), dim3(TK_THREADS), 0, st, logits, dtype, probs_in, vocab, stride, w.pmax, w.psum, k,
+                                               probs_full, w.cprob, w.ctok));
+  BST_CUDA(launch_pdl(k1_merge, dim3(gamma), dim3(TK_THREADS), 0, st, w.cprob, w.ctok, chunks, k, tok, prob));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
