@@ -114,11 +114,12 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
                                 int page_size, const int32_t* __restrict__ state, int state_c_idx, bst_prefetch_t pf,
                                 int req_rows, int req_span, int req_state, int req_slots) {
   sm100::grid_dep_launch();
-  if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
+  if (threadIdx.x == 0 && blockIdx.y == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   sm100::grid_dep_wait();
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
+  const int h_end = min(n_q + 2 * n_kv, (int)(blockIdx.y + 1) * nw);  // blockIdx.y: group of nw heads
   // batched requests: row t belongs to request (t % req_span) / req_rows, whose
   // context length is state[r * req_state + c_idx] and whose slots start at r * req_slots
   const int r = req_rows > 0 ? (t % req_span) / req_rows : 0;
@@ -134,7 +135,7 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
     const float ang = (float)p * inv_freq[i];
     sincosf(ang, &sn[e], &cs[e]);
   }
-  for (int hd = warp; hd < n_q + 2 * n_kv; hd += nw) {
+  for (int hd = blockIdx.y * nw + warp; hd < h_end; hd += nw) {
     const bool is_q = hd < n_q, is_k = !is_q && hd < n_q + n_kv;
     if (is_q && qr < 0) continue;
     if (!is_q && sl < 0) continue;
@@ -242,7 +243,7 @@ extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* 
   BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
               "null pointer argument");
   BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
-  BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows), dim3(512), 0, as_stream(stream), partial, *sched, n_q, n_kv,
+  BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows, (n_q + 2 * n_kv + 15) / 16), dim3(512), 0, as_stream(stream), partial, *sched, n_q, n_kv,
                       static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm), eps,
                       inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride,
                       static_cast<__nv_bfloat16*>(kv), layer_off_elems, page_table, page_size, state, state_c_idx,
