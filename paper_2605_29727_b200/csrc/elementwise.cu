@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "rope.cuh"
 #include "sm100.cuh"
 
 namespace bst {
@@ -105,74 +106,19 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
 }
 
 // ------------------------------------------------------------- q/k/v + rope
-// One CTA per token row; one warp per head (d = 128, 4 values per lane).
-__global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int n_q, int n_kv,
-                                const __nv_bfloat16* __restrict__ qn, const __nv_bfloat16* __restrict__ kn, float eps,
-                                const float* __restrict__ inv_freq, const int32_t* __restrict__ pos, const int32_t* __restrict__ slot,
-                                const int32_t* __restrict__ qrow, __nv_bfloat16* q_out, int64_t q_tok_stride,
-                                __nv_bfloat16* kv, int64_t layer_off, const int32_t* __restrict__ page_table,
-                                int page_size, const int32_t* __restrict__ state, int state_c_idx, bst_prefetch_t pf,
-                                int req_rows, int req_span, int req_state, int req_slots) {
+// One CTA per (token row, group of 16 heads); one warp per head (d = 128, 4 values per lane).
+__global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, RopeArgs ra, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
   if (threadIdx.x == 0 && blockIdx.y == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   sm100::grid_dep_wait();
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
-  const int h_end = min(n_q + 2 * n_kv, (int)(blockIdx.y + 1) * nw);  // blockIdx.y: group of nw heads
-  // batched requests: row t belongs to request (t % req_span) / req_rows, whose
-  // context length is state[r * req_state + c_idx] and whose slots start at r * req_slots
-  const int r = req_rows > 0 ? (t % req_span) / req_rows : 0;
-  const int c0 = state ? state[r * req_state + state_c_idx] : 0;
-  const int p = pos[t] + c0;
-  const int sl = slot[t] == INT_MIN ? -1 : slot[t] + c0 + r * req_slots;
-  const int qr = qrow ? qrow[t] : t;
-  // rotary angles for this lane's 4 dims (i in [0,64) pairs with i+64)
-  float cs[4], sn[4];
-#pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int i = (lane * 4 + e) & 63;
-    const float ang = (float)p * inv_freq[i];
-    sincosf(ang, &sn[e], &cs[e]);
-  }
+  const int h_end = min(ra.n_q + 2 * ra.n_kv, (int)(blockIdx.y + 1) * nw);
   for (int hd = blockIdx.y * nw + warp; hd < h_end; hd += nw) {
-    const bool is_q = hd < n_q, is_k = !is_q && hd < n_q + n_kv;
-    if (is_q && qr < 0) continue;
-    if (!is_q && sl < 0) continue;
-    const int col0 = hd * 128 + lane * 4;
-    const float4 y4 = gemm_load4(partial, s, t, col0);
+    const float4 y4 = gemm_load4(partial, s, t, hd * 128 + lane * 4);
     float v[4] = {y4.x, y4.y, y4.z, y4.w};
-    if (is_q || is_k) {
-      const __nv_bfloat16* nw_ = is_q ? qn : kn;
-      float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
-      ss = warp_sum(ss);
-      const float inv = rsqrtf(ss / 128.f + eps);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = v[e] * inv * __bfloat162float(nw_[lane * 4 + e]);
-      // rotate_half: lanes 0-15 hold dims 0-63, lanes 16-31 hold 64-127
-      float o[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float partner = __shfl_xor_sync(0xffffffffu, v[e], 16);
-        o[e] = lane < 16 ? v[e] * cs[e] - partner * sn[e] : v[e] * cs[e] + partner * sn[e];
-      }
-#pragma unroll
-      for (int e = 0; e < 4; ++e) v[e] = o[e];
-    }
-    __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]), hi = __floats2bfloat162_rn(v[2], v[3]);
-    if (is_q) {
-      __nv_bfloat16* dst = q_out + (int64_t)qr * q_tok_stride + hd * 128 + lane * 4;
-      *reinterpret_cast<__nv_bfloat162*>(dst) = lo;
-      *reinterpret_cast<__nv_bfloat162*>(dst + 2) = hi;
-    } else {
-      const int head = is_k ? hd - n_q : hd - n_q - n_kv;
-      const int which = is_k ? 0 : 1;
-      const int64_t page = page_table[sl / page_size];
-      const int64_t off = ((page * 2 + which) * n_kv + head) * page_size + (sl % page_size);
-      __nv_bfloat16* dst = kv + layer_off + off * 128 + lane * 4;
-      *reinterpret_cast<__nv_bfloat162*>(dst) = lo;
-      *reinterpret_cast<__nv_bfloat162*>(dst + 2) = hi;
-    }
+    rope_store_head(ra, t, hd, v, lane);
   }
 }
 
@@ -234,6 +180,38 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   return BST_OK;
 }
 
+namespace bst {
+RopeArgs make_rope_args(int n_q, int n_kv, const void* q_norm, const void* k_norm, float eps, const float* inv_freq,
+                        const int32_t* pos, const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride,
+                        void* kv, int64_t layer_off_elems, const int32_t* page_table, int page_size,
+                        const int32_t* state, int state_c_idx, int req_rows, int req_span, int req_state,
+                        int req_slots) {
+  RopeArgs r;
+  r.n_q = n_q;
+  r.n_kv = n_kv;
+  r.qn = static_cast<const __nv_bfloat16*>(q_norm);
+  r.kn = static_cast<const __nv_bfloat16*>(k_norm);
+  r.eps = eps;
+  r.inv_freq = inv_freq;
+  r.pos = pos;
+  r.slot = slot;
+  r.qrow = qrow;
+  r.q_out = static_cast<__nv_bfloat16*>(q_out);
+  r.q_tok_stride = q_tok_stride;
+  r.kv = static_cast<__nv_bfloat16*>(kv);
+  r.layer_off = layer_off_elems;
+  r.page_table = page_table;
+  r.page_size = page_size;
+  r.state = state;
+  r.c_idx = state_c_idx;
+  r.req_rows = req_rows;
+  r.req_span = req_span > 0 ? req_span : 1;
+  r.req_state = req_state;
+  r.req_slots = req_slots;
+  return r;
+}
+}  // namespace bst
+
 extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* sched, int rows, int n_q, int n_kv,
                                   const void* q_norm, const void* k_norm, float eps, const float* inv_freq,
                                   const int32_t* pos, const int32_t* slot, const int32_t* qrow, void* q_out,
@@ -243,11 +221,11 @@ extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* 
   BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
               "null pointer argument");
   BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
-  BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows, (n_q + 2 * n_kv + 15) / 16), dim3(512), 0, as_stream(stream), partial, *sched, n_q, n_kv,
-                      static_cast<const __nv_bfloat16*>(q_norm), static_cast<const __nv_bfloat16*>(k_norm), eps,
-                      inv_freq, pos, slot, qrow, static_cast<__nv_bfloat16*>(q_out), q_tok_stride,
-                      static_cast<__nv_bfloat16*>(kv), layer_off_elems, page_table, page_size, state, state_c_idx,
-                      take_prefetch(), req_rows, req_span > 0 ? req_span : 1, req_state, req_slots));
+  const RopeArgs ra = make_rope_args(n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, q_tok_stride,
+                                     kv, layer_off_elems, page_table, page_size, state, state_c_idx, req_rows,
+                                     req_span, req_state, req_slots);
+  BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows, (n_q + 2 * n_kv + 15) / 16), dim3(512), 0, as_stream(stream),
+                      partial, *sched, ra, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -118,16 +118,14 @@ class TargetModel:
         ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
         for li, lw in enumerate(w.layers):
             nxt_l = w.layers[li + 1] if li + 1 < cfg.L else None
-            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
-            if "rope" not in _ABLATE:
-                if batch is None:
-                    ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
-                                 self.slot, None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state)
-                else:
-                    nr, S, rp = batch
-                    ops.qkv_rope_batch(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
-                                       self.slot, None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state, S,
-                                       nr * S, state.stride(0), rp * PAGE)
+            if "rope" in _ABLATE:
+                ops.gemm_partial(x, lw.qkv, out=self.partial)
+            else:
+                req = (0, 1, 0, 0) if batch is None else (batch[1], batch[0] * batch[1], state.stride(0),
+                                                          batch[2] * PAGE)
+                ops.gemm_qkv_rope(x, lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm,
+                                  eps, self.inv_freq, self.pos, self.slot, None, self.q, kv.buf, li * kv.layer_stride,
+                                  pt, PAGE, state, req)
             if "attn" not in _ABLATE:
                 _pf((lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB))
                 if batch is None:
@@ -216,9 +214,9 @@ class DrafterModel:
         self._ctx_rows(n, x, state)
         self.qrow[:n].fill_(-1)
         for li, lw in enumerate(self.w.layers):
-            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
-            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, cfg.eps, self.inv_freq, self.pos,
-                         self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, pt, PAGE, state)
+            ops.gemm_qkv_rope(x, lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm,
+                              cfg.eps, self.inv_freq, self.pos, self.slot, self.qrow, self.q, self.kv.buf,
+                              li * self.kv.layer_stride, pt, PAGE, state)
 
     def forward(self, state: torch.Tensor) -> torch.Tensor:
         """Draft one block: returns logits [gamma, V] fp32 for future positions c+1..c+gamma."""
@@ -229,9 +227,9 @@ class DrafterModel:
         xb, resid = self.X[:B], self.resid[:B]
         ops.embed_rmsnorm(self.tokens, B, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
         for li, lw in enumerate(w.layers):
-            p = ops.gemm_partial(self.X[:M], lw.qkv, out=self.partial)
-            ops.qkv_rope(p, M, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
-                         self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, self.kv.page_table, PAGE, state)
+            ops.gemm_qkv_rope(self.X[:M], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm,
+                              lw.k_norm, eps, self.inv_freq, self.pos, self.slot, self.qrow, self.q, self.kv.buf,
+                              li * self.kv.layer_stride, self.kv.page_table, PAGE, state)
             ops.attention(self.q[:B], self.attn[:B], self.kv.buf, self.dcfg.layers, self.kv.n_pages, li,
                           self.kv.page_table, cfg.n_q, cfg.n_kv, B, 0, B, self.kv.max_slots, state, MODE_FULL, None, 0,
                           self.attn_ws, n_splits=self.attn_splits)
@@ -263,10 +261,9 @@ class DrafterModel:
         xb, resid = self.X[:QB], self.resid[:QB]
         ops.embed_rmsnorm(self.tokens, QB, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
         for li, lw in enumerate(w.layers):
-            p = ops.gemm_partial(self.X[:M], lw.qkv, out=self.partial)
-            ops.qkv_rope_batch(p, M, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos,
-                               self.slot, self.qrow, self.q, self.kv.buf, li * self.kv.layer_stride, pt, PAGE, state,
-                               B, QB, rs, req_pages * PAGE)
+            ops.gemm_qkv_rope(self.X[:M], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm,
+                              lw.k_norm, eps, self.inv_freq, self.pos, self.slot, self.qrow, self.q, self.kv.buf,
+                              li * self.kv.layer_stride, pt, PAGE, state, (B, QB, rs, req_pages * PAGE))
             ops.attention_batch(self.q[:QB], self.attn[:QB], self.kv.buf, self.dcfg.layers, self.kv.n_pages, li, pt,
                                 req_pages, cfg.n_q, cfg.n_kv, n, B, B, req_pages * PAGE, state, rs, MODE_FULL, None,
                                 0, self.attn_ws, n_splits=self.attn_splits)

@@ -109,9 +109,9 @@ class TPTargetModel(TargetModel):
         x, resid = self.x[:n], self.resid[:n]
         ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
         for li, lw in enumerate(w.layers):
-            p = ops.gemm_partial(x, lw.qkv, out=self.partial)
-            ops.qkv_rope(p, n, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps, self.inv_freq, self.pos, self.slot,
-                         None, self.q, kv.buf, li * kv.layer_stride, pt, PAGE, state)
+            ops.gemm_qkv_rope(x, lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm, eps,
+                              self.inv_freq, self.pos, self.slot, None, self.q, kv.buf, li * kv.layer_stride, pt,
+                              PAGE, state)
             ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, cfg.n_q, cfg.n_kv, n,
                           c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words, self.attn_ws,
                           n_splits=self.attn_splits)

@@ -7,6 +7,7 @@ is no eager/torch fallback — a missing library or device raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from functools import lru_cache
 
 import torch
@@ -129,6 +130,17 @@ def residual_rmsnorm(p: PartialOut | None, resid, rows, h, w, eps, x=None, feat=
     _lib.call("bst_residual_rmsnorm", None if p is None else p.buf.data_ptr(), sched, _p(resid), rows, h,
               w.data_ptr(), C.c_float(eps), _p(x), 0 if x is None else x.stride(0), _p(feat),
               0 if feat is None else feat.stride(0), stream_ptr())
+
+
+def gemm_qkv_rope(x, w, out, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv,
+                  layer_off, page_table, page_size, state, req=(0, 1, 0, 0)) -> None:
+    """q/k/v projection (K4) then q/k RMSNorm + RoPE + q and paged-KV stores (K5 qkv_rope)
+    of the m = x.shape[0] rows.  (A variant fusing the epilogue into the GEMM's stream-K
+    tile fixup was measured slower: it raised the GEMM to 168 registers, which blocks the
+    PDL co-residency of the epilogue kernels, and serialised one head x all rows per CTA.)"""
+    p = gemm_partial(x, w, out=out)
+    qkv_rope_batch(p, x.shape[0], n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv, layer_off,
+                   page_table, page_size, state, *req)
 
 
 def qkv_rope(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv, layer_off,
