@@ -137,6 +137,12 @@ int bst_ancestor_mask(const int32_t* parent, int t, int mask_words, uint32_t* ma
 int bst_expand_dev(const int32_t* tok, const double* prob, int gamma, int k, const bst_plan_t* plan_dev,
                    int policy, int n_max, int n_cap, const bst_tree_t* out, void* ws, size_t ws_bytes,
                    bst_stream_t stream);
+/* K2 over n_req independent requests in one launch (batched engine, config 3): request r
+ * reads lattice rows tok/prob + r * lat_stride, plan_dev[r], writes trees_dev[r] (device
+ * array of n_req bst_tree_t); ws: n_req x bst_expand_workspace(gamma, k, n_cap) bytes. */
+int bst_expand_dev_batch(const int32_t* tok, const double* prob, int64_t lat_stride, int gamma, int k,
+                         const bst_plan_t* plan_dev, int policy, int n_max, int n_cap, const bst_tree_t* trees_dev,
+                         int n_req, void* ws, size_t ws_bytes, bst_stream_t stream);
 
 int bst_accept(const int32_t* token, const int32_t* child_start, const int32_t* child_list,
                const int32_t* argmax, int max_path, int32_t* path, int32_t* committed, int32_t* meta,

@@ -634,13 +634,29 @@ __device__ __forceinline__ bst_plan_t resolve_plan(bst_plan_t plan, const bst_pl
   return plan;
 }
 
+// Batched form (trees != nullptr): CTA r expands request r's lattice (tok/prob + r *
+// lat_stride) with plan_dev[r] into trees[r], workspace shifted by r * ws_stride bytes.
 __global__ void __launch_bounds__(EX_THREADS, 1)
-    expand_best_first_kernel(const int32_t* __restrict__ tok, const double* __restrict__ prob, int gamma, int k,
-                             bst_plan_t plan_in, const bst_plan_t* plan_dev, int n_cap, bst_tree_t out, ExWs ws,
-                             int heap_in_smem) {
+    expand_best_first_kernel(const int32_t* __restrict__ tok_in, const double* __restrict__ prob_in, int gamma, int k,
+                             bst_plan_t plan_in, const bst_plan_t* plan_dev_in, int n_cap, bst_tree_t out_in,
+                             ExWs ws_in, int heap_in_smem, const bst_tree_t* trees, int64_t lat_stride,
+                             int64_t ws_stride) {
   pdl_enter();
   extern __shared__ __align__(16) unsigned char smem_raw[];
   ExSmem& sm = *reinterpret_cast<ExSmem*>(smem_raw);
+  const int req = trees ? (int)blockIdx.x : 0;
+  const int32_t* tok = tok_in + req * lat_stride;
+  const double* prob = prob_in + req * lat_stride;
+  const bst_plan_t* plan_dev = plan_dev_in ? plan_dev_in + req : nullptr;
+  const bst_tree_t out = trees ? trees[req] : out_in;
+  ExWs ws = ws_in;
+  if (trees) {
+    const int64_t o = req * ws_stride;
+    ws.ahat = reinterpret_cast<double*>(reinterpret_cast<char*>(ws.ahat) + o);
+    ws.shat = reinterpret_cast<double*>(reinterpret_cast<char*>(ws.shat) + o);
+    ws.counts = reinterpret_cast<int*>(reinterpret_cast<char*>(ws.counts) + o);
+    ws.heap = reinterpret_cast<HeapEntry*>(reinterpret_cast<char*>(ws.heap) + o);
+  }
   const bst_plan_t plan = resolve_plan(plan_in, plan_dev);
   const bool adaptive = plan.policy == BST_POLICY_ADAPTIVE;
   const int n_max = plan.n_max;
@@ -825,7 +841,7 @@ extern "C" int bst_expand(const int32_t* tok, const double* prob, int gamma, int
   } else {
     const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
     BST_CUDA(launch_pdl(expand_best_first_kernel, dim3(1), dim3(EX_THREADS), smem, st, tok, prob, gamma, k, p, nullptr, n_cap, *out, w,
-                                                          heap_in_smem));
+                                                          heap_in_smem, static_cast<const bst_tree_t*>(nullptr), (int64_t)0, (int64_t)0));
   }
   BST_LAUNCH_CHECK();
   return BST_OK;
@@ -855,12 +871,41 @@ extern "C" int bst_expand_dev(const int32_t* tok, const double* prob, int gamma,
   p.n_max = n_max;
   const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
   BST_CUDA(launch_pdl(expand_best_first_kernel, dim3(1), dim3(EX_THREADS), smem, as_stream(stream), tok, prob, gamma, k, p, plan_dev, n_cap, *out,
-                                                                        w, heap_in_smem));
+                                                                        w, heap_in_smem, static_cast<const bst_tree_t*>(nullptr), (int64_t)0, (int64_t)0));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
 
 extern "C" int bst_debug_expand_trace(void* buf) {
   BST_CUDA(cudaMemcpyToSymbol(bst::g_ex_trace, &buf, sizeof(void*)));
+  return BST_OK;
+}
+
+// K2 for n_req requests in one launch (config 3's batched engine): request r's lattice
+// rows at tok/prob + r * lat_stride, plan plan_dev[r], tree trees[r] (a device array of
+// n_req bst_tree_t); ws holds n_req x bst_expand_workspace(gamma, k, n_cap) bytes.
+extern "C" int bst_expand_dev_batch(const int32_t* tok, const double* prob, int64_t lat_stride, int gamma, int k,
+                                    const bst_plan_t* plan_dev, int policy, int n_max, int n_cap,
+                                    const bst_tree_t* trees_dev, int n_req, void* ws, size_t ws_bytes,
+                                    bst_stream_t stream) {
+  using namespace bst;
+  BST_REQUIRE(tok && prob && plan_dev && trees_dev && n_req >= 1, "bad arguments");
+  BST_REQUIRE(policy == BST_POLICY_ADAPTIVE || policy == BST_POLICY_FIXED, "device plans support adaptive/fixed");
+  BST_REQUIRE(gamma >= 1 && gamma <= EX_MAXG && k >= 1 && k <= EX_MAXK, "bad lattice shape");
+  BST_REQUIRE(n_max >= 1 && n_max <= n_cap && n_cap < (1 << 20), "bad n_max/n_cap");
+  size_t per = 0;
+  ExWs w = ex_carve(ws, n_cap, &per);
+  BST_REQUIRE(ws != nullptr && ws_bytes >= per * (size_t)n_req, "workspace too small: %zu < %zu", ws_bytes,
+              per * (size_t)n_req);
+  const size_t smem = sizeof(ExSmem);
+  BST_CUDA(cudaFuncSetAttribute(expand_best_first_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  bst_plan_t p{};
+  p.policy = policy;
+  p.n_max = n_max;
+  const int heap_in_smem = (2 * (size_t)n_cap + 4) * sizeof(HeapEntry) <= sizeof(unsigned long long) * EX_CAP * 2;
+  BST_CUDA(launch_pdl(expand_best_first_kernel, dim3(n_req), dim3(EX_THREADS), smem, as_stream(stream), tok, prob,
+                      gamma, k, p, plan_dev, n_cap, bst_tree_t{}, w, heap_in_smem, trees_dev, lat_stride,
+                      (int64_t)per));
+  BST_LAUNCH_CHECK();
   return BST_OK;
 }

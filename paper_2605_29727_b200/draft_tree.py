@@ -193,3 +193,24 @@ def expand_device_plan(tok: torch.Tensor, prob: torch.Tensor, plan_dev: torch.Te
     _lib.call("bst_expand_dev", tok.data_ptr(), prob.data_ptr(), gamma, k, plan_dev.data_ptr(), policy, n_max,
               out.n_cap, st, ws.data_ptr(), ws.numel(), stream_ptr())
     return out
+
+
+def expand_device_plan_batch(tok: torch.Tensor, prob: torch.Tensor, lat_stride: int, gamma: int,
+                             plan_dev: torch.Tensor, policy: int, n_max: int, trees: list[DeviceTree],
+                             trees_dev: torch.Tensor) -> None:
+    """K2 for every request in one launch: request r's lattice at row offset r * lat_stride / k,
+    plan plan_dev[r], output trees[r] (trees_dev: their bst_tree_t structs on the device)."""
+    k = tok.shape[-1]
+    n_cap = trees[0].n_cap
+    need = _lib.lib().bst_expand_workspace(gamma, k, n_cap) * len(trees)
+    ws = workspace("expand_batch", need)
+    _lib.call("bst_expand_dev_batch", tok.data_ptr(), prob.data_ptr(), int(lat_stride), gamma, k, plan_dev.data_ptr(),
+              policy, n_max, n_cap, trees_dev.data_ptr(), len(trees), ws.data_ptr(), ws.numel(), stream_ptr())
+
+
+def tree_structs_device(trees: list[DeviceTree], device) -> torch.Tensor:
+    """Device array of the trees' bst_tree_t structs (for expand_device_plan_batch)."""
+    import ctypes as _C
+    structs = [t.struct() for t in trees]  # keep the ctypes objects alive while their bytes are read
+    raw = b"".join(_C.string_at(_C.addressof(st), _C.sizeof(_lib.Tree)) for st in structs)
+    return torch.frombuffer(bytearray(raw), dtype=torch.uint8).to(device)

@@ -31,7 +31,7 @@ import torch
 
 from .. import _lib, ops
 from ..device import graph_kernel_nodes
-from ..draft_tree import DeviceTree, expand_device_plan
+from ..draft_tree import DeviceTree, expand_device_plan_batch, tree_structs_device
 from ..lattice import topk_logits_into
 from ..verify_sim import accept_device
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
@@ -82,6 +82,7 @@ class BatchEngine:
         self.anc = torch.zeros(n_req, self.S * self.mask_words, **i32)  # contiguous ancestor masks (batched K3)
         for r, tr in enumerate(self.trees):
             tr.anc_mask = self.anc[r]
+        self.trees_dev = tree_structs_device(self.trees, dev)  # K2 writes every request's tree in one launch
         n_feat = len(feat) * cfg.h
         self.feat = torch.zeros(n_req * G1, n_feat, dtype=torch.bfloat16, device=dev)  # drafter context features
         self.path = torch.zeros(n_req, G1, **i32)
@@ -171,9 +172,9 @@ class BatchEngine:
                                      feat=self.feat[r0 * G1:(r0 + n) * G1])
             topk_logits_into(logits, self.top_k, self.lat_tok[r0 * G1:(r0 + n) * G1],
                              self.lat_prob[r0 * G1:(r0 + n) * G1], None)
-        for r, tr in enumerate(self.trees):
-            rows = slice(r * G1 + 1, (r + 1) * G1)  # block row 0 is the bonus position
-            expand_device_plan(self.lat_tok[rows], self.lat_prob[rows], self.plan_dev[r], self.policy, self.N, tr)
+        # block row 0 of each request is the bonus position: request r's lattice is rows r*G1+1 ..
+        expand_device_plan_batch(self.lat_tok[1:], self.lat_prob[1:], G1 * self.top_k, self.gamma, self.plan_dev,
+                                 self.policy, self.N, self.trees, self.trees_dev)
         # phase 2: verify every request (chunks of chunk_v), then accept / compact / gather / commit
         for r0 in range(0, n_req, self.chunk_v):
             n = min(self.chunk_v, n_req - r0)

@@ -36,7 +36,7 @@ from ..device import graph_kernel_nodes
 from ..draft_tree import DeviceTree, expand_device_plan
 from ..lattice import MarginalBlock, topk_logits_into
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
-from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
+from .forward import _ABLATE, MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
 from .weights import DrafterWeights, TargetWeights
 
 ST_C, ST_NNEW, ST_BONUS, ST_COMMITTED, ST_CYCLE = 0, 1, 2, 3, 4
@@ -178,8 +178,10 @@ class B200Engine:
             logits = self.draft_override(self)
         else:
             logits = self.drafter.forward(self.state)
-        topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
-        expand_device_plan(self.lat_tok, self.lat_prob, self.plan_dev, self.policy[0], self.policy[1], self.tree)
+        if "k1" not in _ABLATE:
+            topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
+        if "k2" not in _ABLATE:
+            expand_device_plan(self.lat_tok, self.lat_prob, self.plan_dev, self.policy[0], self.policy[1], self.tree)
 
     def _head(self) -> str:
         return "sample" if self.target.temperature > 0.0 else "argmax"
