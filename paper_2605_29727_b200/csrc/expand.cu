@@ -211,41 +211,43 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
       }
       __syncthreads();
     };
-    crossing(max_range);
+    // level-by-level convolution of the path-cost histogram over every bin < max_range
+    // (one bin per thread for pass 0, ping-pong buffers: one barrier per level); the
+    // crossing is located once at the end — tot only grows with the levels, so the first
+    // crossing bin is the same as tracking it level by level
+    unsigned int* hp = hprev;
+    unsigned int* hc = hcur;
     for (int d = 2; d <= gamma; ++d) {
-      // the crossing bin B* only moves down as levels are added, so bins above
-      // the current crossing never matter for the remaining levels
-      const int range = s_range;
       int cr[8];
       int nk = 0;
       for (int r = 0; r < k && r < 8; ++r) {
         cr[r] = cost[(d - 1) * k + r];
         if (cr[r] >= 0) nk = r + 1;
       }
-      for (int b = threadIdx.x; b < range; b += EX_THREADS) {
+      for (int b = threadIdx.x; b < max_range; b += EX_THREADS) {
         unsigned long long acc = 0;
         if (k <= 8) {
 #pragma unroll
           for (int r = 0; r < 8; ++r)
-            if (r < nk && cr[r] <= b) acc += hprev[b - cr[r]];
+            if (r < nk && cr[r] <= b) acc += hp[b - cr[r]];
         } else {
           for (int r = 0; r < k; ++r) {
             const int ci = cost[(d - 1) * k + r];
             if (ci < 0) break;
-            if (ci <= b) acc += hprev[b - ci];
+            if (ci <= b) acc += hp[b - ci];
           }
         }
-        hcur[b] = acc > SAT ? SAT : (unsigned int)acc;
-      }
-      __syncthreads();
-      for (int b = threadIdx.x; b < range; b += EX_THREADS) {
-        hprev[b] = hcur[b];
-        unsigned long long t = (unsigned long long)tot[b] + hcur[b];
+        const unsigned int a32 = acc > SAT ? SAT : (unsigned int)acc;
+        hc[b] = a32;
+        const unsigned long long t = (unsigned long long)tot[b] + a32;
         tot[b] = t > SAT ? SAT : (unsigned int)t;
       }
       __syncthreads();
-      crossing(range);
+      unsigned int* tmp = hp;
+      hp = hc;
+      hc = tmp;
     }
+    crossing(max_range);
     if (threadIdx.x == 0) s_bstar = s_cross ? s_range - 1 : -1;
     __syncthreads();
     int bstar = s_bstar;
