@@ -147,6 +147,57 @@ def run_reference(args) -> None:
 
 
 # -------------------------------------------------------------------- ours
+def attention_roofline(peaks: dict, c: int, s: int, layers: int = 36) -> dict:
+    """K3 per-layer time in a CUDA graph of `layers` launches (distinct layers, PDL) at context c,
+    s tree rows; roofline = SURVEY §8d K3 bytes bp*(2(c+s)h_kv + 2 s h_q) + mask vs measured HBM."""
+    import torch
+
+    from paper_2605_29727_b200 import ops
+    from paper_2605_29727_b200.engine.forward import PagedKV
+    n_q, n_kv = 32, 8
+    kv = PagedKV(layers, n_kv, c + 320, "cuda")
+    kv.buf.normal_(0, 1)
+    q = torch.randn(s, n_q * 128, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(q)
+    words = (s + 31) // 32
+    anc = torch.zeros(s, words, dtype=torch.int32, device="cuda")
+    for i in range(s):  # chain of siblings: every row sees the root and itself
+        anc[i, 0] |= 1
+        anc[i, i // 32] |= (1 << (i % 32)) if (i % 32) != 31 else -(1 << 31)
+    ws = torch.zeros(64 << 20, dtype=torch.float32, device="cuda")
+    st = torch.cuda.Stream()
+
+    def run():
+        for li in range(layers):
+            ops.attention(q, out, kv.buf, layers, kv.n_pages, li, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0,
+                          anc.view(-1), words, ws)
+    with torch.cuda.stream(st):
+        run()
+    st.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=st):
+        run()
+    ts = []
+    for it in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        with torch.cuda.stream(st):
+            g.replay()
+        b.record(st)
+        b.synchronize()
+        if it >= 1:
+            ts.append(a.elapsed_time(b) * 1e-3 / layers)
+    t = statistics.median(ts)
+    byts = 2 * (2 * (c + s) * n_kv * 128 + 2 * s * n_q * 128) + s * words * 4
+    achieved = byts / t / 1e9
+    del kv, g
+    torch.cuda.empty_cache()
+    return {"bound": "hbm", "kernel": "attn_tc2_kernel (K3)", "context": c, "tree_rows": s, "layer_us": t * 1e6,
+            "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
+            "algorithmic_bytes_per_launch": byts, "traffic": "DRAM read = algorithmic (profiles/attn_tc2_ncu_summary.txt)",
+            "timing": "CUDA events around a graph of 36 launches over distinct layers (config-4 verify context)"}
+
+
 def run_ours(args) -> None:
     import numpy as np
     import torch
@@ -306,6 +357,12 @@ def run_ours(args) -> None:
     if prof.exists():
         traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
 
+    # ---- K3 tree-verify attention in its verify-graph context (config 4 shape: c=32K, s=17):
+    # a graph of 36 back-to-back launches over 36 distinct layers (36 x 134 MB >> L2)
+    attn = None
+    if not args.no_attn:
+        attn = attention_roofline(peaks, 32768, 17)
+
     # ---- CPU baseline (rank 0, N=1 only): bounded sample of the reference planning path
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
@@ -344,6 +401,8 @@ def run_ours(args) -> None:
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
     }
+    if attn:
+        line["verify_attention_roofline"] = attn
     if cpu:
         line["cpu_baseline"] = cpu
     print(json.dumps(line), flush=True)
@@ -364,6 +423,7 @@ def main() -> None:
     ap.add_argument("--e2e-cycles", type=int, default=30)
     ap.add_argument("--cpu-cycles", type=int, default=30)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-attn", action="store_true", help="skip the K3 roofline probe (c=32K, s=17)")
     ap.add_argument("--profile", action="store_true", help="only the cycle loop (for ncu --profile-from-start off)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
