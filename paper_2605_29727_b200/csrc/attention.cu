@@ -2129,7 +2129,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_con
 // merge flash-decoding splits: one warp per (token, q-head) row, single pass
 // with online rescaling, 4 splits in flight per iteration
 __global__ void attn_combine_kernel(AttnArgs a) {
-  sm100::grid_dep_launch();
+  pdl_enter();
   if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 0);
   const int row = blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5), req = blockIdx.y;
   const int lane = threadIdx.x & 31;
@@ -2416,7 +2416,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
       case 7: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<7>, tm, a)); break;
       default: BST_CUDA(cudaLaunchKernelEx(&cfg, attn_kt_kernel<8>, tm, a)); break;
     }
-    if (a.n_splits > 1 && !a.merge) attn_combine_kernel<<<dim3((s * n_q + 7) / 8, n_req), 256, 0, st>>>(a);
+    if (a.n_splits > 1 && !a.merge)
+      BST_CUDA(launch_pdl(attn_combine_kernel, dim3((s * n_q + 7) / 8, n_req), dim3(256), 0, st, a));
     BST_LAUNCH_CHECK();
     return BST_OK;
   }
@@ -2470,7 +2471,7 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   if (n_splits > 1 && !a.merge) {
     const int rows_total = s * n_q;
     // plain launch: a PDL launch of the combine measured slower in the verify graph
-    attn_combine_kernel<<<dim3((rows_total + 7) / 8, n_req), 256, 0, st>>>(a);
+    BST_CUDA(launch_pdl(attn_combine_kernel, dim3((rows_total + 7) / 8, n_req), dim3(256), 0, st, a));
   }
   BST_LAUNCH_CHECK();
   return BST_OK;

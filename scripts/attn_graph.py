@@ -2,6 +2,7 @@
 the verify forward; every layer's KV is distinct, 36 x 134 MB at c=32K >> L2, no flush).
 Prints per-launch time and the fraction of the per-layer HBM roofline."""
 import json
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -33,7 +34,7 @@ for s in [int(x) for x in sys.argv[2:]] or [17, 33, 65, 129, 257]:
     def run():
         for li in range(L):
             ops.attention(q, out, kv.buf, L, kv.n_pages, li, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0,
-                          anc.view(-1), words, ws)
+                          anc.view(-1), words, ws, n_splits=int(os.environ.get("SPLITS", "0")))
     with torch.cuda.stream(st):
         run()
     st.synchronize()
