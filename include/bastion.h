@@ -230,7 +230,7 @@ int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t 
 size_t bst_attention_workspace(int n_q, int s, int n_splits);
 /* K3 kernel family: 3 = row-major tcgen05 (tc1 / tc2, default), 4 = key-major tcgen05
  * (S^T = K Q^T, reference-max softmax, cluster or L2 split merge), 2 = tc1 only,
- * 1 = mma.sync, 0 = experimental FA-style; -1 = from the BST_ATTN environment variable.
+ * 1 = mma.sync; -1 = from the BST_ATTN environment variable.
  * Split partials alternate between two workspace banks with the layer index, so the
  * workspace holds 2 x n_splits x s x n_q x 130 floats after the counter head. */
 int bst_attention_set_variant(int variant);

@@ -920,300 +920,12 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 }
 
 
-// ===========================================================================
-// tcgen05 FA4-style variant (default): 128-key tiles (two 64-slot pages), two
-// softmax warpgroups that split the keys of every query row (one max exchange
-// per tile through shared memory; partial row sums are merged once at the end),
-// S double buffered in TMEM (2 x 128 columns) + O (128 columns).
-// warp 0: TMA (2-stage ring of 64 KiB K+V), warp 1: TMEM owner + UMMA issuer,
-// warps 2-5 (WG0: keys 0-63 of a tile, O dims 0-63) and 6-9 (WG1: keys 64-127,
-// O dims 64-127); thread (wg, row) of both groups share TMEM lane `row`.
-// ===========================================================================
-constexpr int F_THREADS = 320;
-constexpr int F_STAGES = 2;
-constexpr int F_KT = 128;                       // keys per tile
-constexpr int F_KV_BYTES = F_KT * A_D * 2;      // 32 KiB (K or V)
-constexpr int F_STAGE_BYTES = 2 * F_KV_BYTES;   // 64 KiB
-constexpr int F_P_BYTES = 128 * F_KT * 2;       // 32 KiB
-
-
-__global__ void __launch_bounds__(F_THREADS, 1) attn_fa_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[F_STAGES], empty[F_STAGES], s_full[2], s_free[2], p_full, o_done, q_ready;
-  __shared__ uint32_t tmem_sh;
-  __shared__ float xmax[2][2][128];
-  __shared__ float xsum[2][128];
-  sm100::grid_dep_launch();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
-  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-  const uint32_t sQ = base, sP = base + T_Q_BYTES, sKV = sP + F_P_BYTES;
-  uint8_t* gQ = smem;
-  uint8_t* gP = smem + T_Q_BYTES;
-  uint8_t* gKV = gP + F_P_BYTES;
-
-  const int head = blockIdx.x, split = blockIdx.y, rb = blockIdx.z;
-  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
-  const int n_keys = c_ctx + a.keys_after_c;
-  const int R = a.group * a.s;
-  const int page0 = split * a.pages_per_split;  // pages_per_split is even
-  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
-  const int page_end = min(page0 + a.pages_per_split, n_pages_keys);
-  const int n_tiles = max((page_end - page0 + 1) >> 1, 0);
-
-  if (threadIdx.x == 0) {
-    sm100::prefetch_tmap(&tmKV);
-    for (int i = 0; i < F_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
-    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&s_full[i], 1); sm100::mbar_init(&s_free[i], 8); }
-    sm100::mbar_init(&p_full, 8);
-    sm100::mbar_init(&o_done, 1);
-    sm100::mbar_init(&q_ready, 8);
-    sm100::fence_mbar_init();
-  }
-  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 512);
-  sm100::tc_fence_before();
-  __syncthreads();
-  sm100::tc_fence_after();
-  const uint32_t tmem = tmem_sh;
-
-  if (warp == 0) {
-    if (lane == 0) {
-      issue_prefetch(a.pf, (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x,
-                     gridDim.x * gridDim.y * gridDim.z);
-      const int safe_tiles = max(min((pdl_safe_slots(a, c_ctx) / A_PAGE - page0) >> 1, n_tiles), 0);
-      bool waited = false;
-      for (int i = 0; i < n_tiles; ++i) {
-        const int st = i % F_STAGES;
-        if (i >= F_STAGES) sm100::mbar_wait(&empty[st], ((i / F_STAGES) & 1) ^ 1);
-        if (!waited && (i >= safe_tiles || i >= F_STAGES)) {
-          sm100::grid_dep_wait();
-          waited = true;
-        }
-        uint8_t* dst = gKV + st * F_STAGE_BYTES;
-        sm100::mbar_expect_tx(&full[st], F_STAGE_BYTES);
-#pragma unroll
-        for (int pg = 0; pg < 2; ++pg) {
-          int lp = page0 + 2 * i + pg;
-          if (lp >= page_end) lp = page0 + 2 * i;  // odd tail: reload page A (keys masked by n_keys)
-          const int phys = a.page_table[lp];
-          const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
-          const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
-          uint8_t* k0 = dst + pg * (A_PAGE * 128);
-          sm100::tma_load_2d(k0, &tmKV, &full[st], 0, (int)rowK);
-          sm100::tma_load_2d(k0 + F_KT * 128, &tmKV, &full[st], 64, (int)rowK);
-          sm100::tma_load_2d(k0 + F_KV_BYTES, &tmKV, &full[st], 0, (int)rowV);
-          sm100::tma_load_2d(k0 + F_KV_BYTES + F_KT * 128, &tmKV, &full[st], 64, (int)rowV);
-        }
-        TRACE(i, 0);
-      }
-    }
-  } else if (warp == 1) {
-    const uint32_t idS = sm100::idesc_bf16(128, F_KT);
-    const uint32_t idO = sm100::idesc_bf16_bmn(128, A_D);
-    sm100::mbar_wait(&q_ready, 0);
-    for (int i = 0; i <= n_tiles; ++i) {
-      if (i < n_tiles) {
-        const int st = i % F_STAGES, b = i & 1;
-        sm100::mbar_wait(&full[st], (i / F_STAGES) & 1);
-        if (lane == 0) TRACE(i, 1);
-        if (i >= 2) sm100::mbar_wait(&s_free[b], ((i - 2) >> 1) & 1);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          const uint32_t kb = sKV + st * F_STAGE_BYTES;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint64_t ad = sm100::desc_k_sw128(sQ + (j >> 2) * (128 * 128) + (j & 3) * 32);
-            const uint64_t bd = sm100::desc_k_sw128(kb + (j >> 2) * (F_KT * 128) + (j & 3) * 32);
-            sm100::umma_f16(tmem + b * F_KT, ad, bd, idS, j > 0 ? 1u : 0u);
-          }
-          sm100::umma_commit(&s_full[b]);
-        }
-        __syncwarp();
-      }
-      if (i >= 1) {
-        const int j = i - 1, stj = j % F_STAGES;
-        sm100::mbar_wait(&p_full, j & 1);
-        if (lane == 0) TRACE(j, 2);
-        sm100::tc_fence_after();
-        if (sm100::elect_one()) {
-          const uint32_t vb = sKV + stj * F_STAGE_BYTES + F_KV_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint64_t ad = sm100::desc_k_sw128(sP + (kk >> 2) * (128 * 128) + (kk & 3) * 32);
-            const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, F_KT * 128);
-            sm100::umma_f16(tmem + 256, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
-          }
-          sm100::umma_commit(&o_done);
-          sm100::umma_commit(&empty[stj]);
-        }
-        __syncwarp();
-      }
-    }
-  } else {
-    const int wg = (warp - 2) >> 2;  // 0: keys 0-63 / O dims 0-63, 1: keys 64-127 / dims 64-127
-    const int quad = warp & 3;
-    const int row = quad * 32 + lane;
-    const int rg = rb * 128 + row;
-    const bool valid = rg < R;
-    const int rr = valid ? rg : 0;
-    const int tok = rr / a.group;
-    const int qh = head * a.group + rr % a.group;
-    const uint32_t* mrow = a.mode == 0 ? a.anc + (int64_t)tok * a.mask_words : nullptr;
-    const int mode = a.mode, mwords = a.mask_words;
-    const float scale = a.scale_log2;
-    sm100::grid_dep_wait();  // q comes from the previous kernel (PDL)
-    {
-      const int4* src = reinterpret_cast<const int4*>(a.q + (int64_t)tok * a.q_tok_stride + (int64_t)qh * A_D) + 8 * wg;
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
-        *reinterpret_cast<int4*>(gQ + wg * (128 * 128) + row * 128 + ((q ^ (row & 7)) << 4)) = v;
-      }
-    }
-    sm100::fence_async_shared();
-    __syncwarp();
-    if (lane == 0) sm100::mbar_arrive(&q_ready);
-    const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-    float m_run = -INFINITY, l_own = 0.f;
-    for (int i = 0; i < n_tiles; ++i) {
-      const int b = i & 1;
-      sm100::mbar_wait(&s_full[b], (i >> 1) & 1);
-      if (threadIdx.x == 64) TRACE(i, 3);
-      sm100::tc_fence_after();
-      float sv[64];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float t16[16];
-        sm100::tmem_ld16(lane_base + b * F_KT + 64 * wg + 16 * k, t16);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) sv[16 * k + e] = t16[e];
-      }
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&s_free[b]);
-      const int slot0 = (page0 + 2 * i) * A_PAGE + 64 * wg;
-      const uint64_t vis = valid ? row_vis64(mode, c_ctx, n_keys, tok, slot0, mrow, mwords) : 0ull;
-      float mx8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
-      if (__all_sync(0xffffffffu, vis == ~0ull)) {
-#pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          sv[k] *= scale;
-          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          const float v = ((vis >> k) & 1ull) ? sv[k] * scale : -INFINITY;
-          sv[k] = v;
-          mx8[k & 7] = fmaxf(mx8[k & 7], v);
-        }
-      }
-      const float mloc = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                               fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
-      xmax[i & 1][wg][row] = mloc;
-      if (threadIdx.x == 64) TRACE(i, 7);
-      named_bar_sync(1, 256);
-      const float mt = fmaxf(mloc, xmax[i & 1][wg ^ 1][row]);
-      const float m_new = fmaxf(m_run, mt);
-      const bool rescale = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + T_RESCALE);
-      const float m_ref = rescale ? m_new : m_run;
-      const float alpha = (rescale && m_run != -INFINITY) ? ex2(m_run - m_ref) : (rescale ? 0.f : 1.f);
-      const float msub = m_ref == -INFINITY ? 0.f : m_ref;
-      float rs8[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) rs8[k] = 0.f;
-      uint32_t pk[32];
-#pragma unroll
-      for (int k = 0; k < 64; k += 2) {
-        const float p0 = ex2(sv[k] - msub);
-        const float p1 = ex2(sv[k + 1] - msub);
-        rs8[(k >> 1) & 7] += p0 + p1;
-        pk[k >> 1] = pack_bf16(p0, p1);
-      }
-      const float rs = ((rs8[0] + rs8[1]) + (rs8[2] + rs8[3])) + ((rs8[4] + rs8[5]) + (rs8[6] + rs8[7]));
-      if (threadIdx.x == 64) TRACE(i, 4);
-      if (i >= 1) sm100::mbar_wait(&o_done, (i - 1) & 1);  // PV(i-1) done: O stable, P free
-      if (threadIdx.x == 64) TRACE(i, 5);
-      sm100::tc_fence_after();
-      if (__any_sync(0xffffffffu, rescale && i >= 1)) {
-        const float f = (rescale && i >= 1) ? alpha : 1.f;
-#pragma unroll 1
-        for (int cc = 0; cc < 4; ++cc) {
-          float ov[16];
-          sm100::tmem_ld16(lane_base + 256 + 64 * wg + 16 * cc, ov);
-#pragma unroll
-          for (int e = 0; e < 16; ++e) ov[e] *= f;
-          sm100::tmem_st16(lane_base + 256 + 64 * wg + 16 * cc, ov);
-        }
-        sm100::tmem_st_wait();
-      }
-      l_own = rescale ? l_own * alpha + rs : l_own + rs;
-      m_run = m_ref;
-#pragma unroll
-      for (int cq = 0; cq < 8; ++cq)
-        *reinterpret_cast<uint4*>(gP + wg * (128 * 128) + row * 128 + ((cq ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
-      sm100::fence_async_shared();
-      sm100::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) sm100::mbar_arrive(&p_full);
-      if (threadIdx.x == 64) TRACE(i, 6);
-    }
-    // ---------------- epilogue: this thread owns O dims [64 wg, 64 wg + 64)
-    xsum[wg][row] = l_own;
-    named_bar_sync(1, 256);
-    const float l_run = l_own + xsum[wg ^ 1][row];
-    float o[64];
-    if (n_tiles > 0) {
-      sm100::mbar_wait(&o_done, (n_tiles - 1) & 1);
-      sm100::tc_fence_after();
-#pragma unroll
-      for (int cc = 0; cc < 4; ++cc) {
-        float t16[16];
-        sm100::tmem_ld16(lane_base + 256 + 64 * wg + 16 * cc, t16);
-#pragma unroll
-        for (int e = 0; e < 16; ++e) o[16 * cc + e] = t16[e];
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < 64; ++e) o[e] = 0.f;
-    }
-    if (valid) {
-      if (a.n_splits == 1) {
-        const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + (int64_t)tok * a.o_tok_stride + (int64_t)qh * A_D + 64 * wg);
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
-                             pack_bf16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_bf16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
-      } else {
-        const int64_t r = (int64_t)split * a.s * a.n_q + (int64_t)tok * a.n_q + qh;
-        float4* op = reinterpret_cast<float4*>(a.ws_o + r * A_D + 64 * wg);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) op[q] = make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-        if (wg == 0) {
-          a.ws_ml[r * 2 + 0] = m_run;
-          a.ws_ml[r * 2 + 1] = l_run;
-        }
-      }
-    }
-  }
-  sm100::tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    sm100::tc_fence_after();
-    sm100::tmem_dealloc(tmem, 512);
-  }
-}
-
 // K and V pages stream through separate rings: a K stage is released when its S
 // MMA completes, a V stage when its PV MMA completes, so K runs further ahead of
 // the softmax than a joint K+V ring of the same size allows.
 constexpr int T2_KS = 5, T2_VS = 4;
 constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
-constexpr int T2_THREADS = F_THREADS + 64;  // + warp 10: V producer, warp 11: PV issuer
+constexpr int T2_THREADS = 384;  // warps 0-1 K TMA / S issuer, 2-9 softmax groups, 10 V TMA, 11 PV issuer
 
 __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -2288,11 +2000,9 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     const char* e = getenv("BST_ATTN");
     // default: row-major tcgen05 kernels (tc1 for short page runs, tc2 for long; fastest
     // in the verify graph, scripts/attn_graph.py).  BST_ATTN=kt: key-major kernel,
-    // BST_ATTN=mma: mma.sync kernel, BST_ATTN=fa: 128-key two-warpgroup kernel
-    // (experimental), BST_ATTN=tc1: tc1 only.
+    // BST_ATTN=mma: mma.sync kernel (the pre-tcgen05 baseline), BST_ATTN=tc1: tc1 only.
     if (e && e[0] == 'k') variant = 4;
     else if (e && e[0] == 'm') variant = 1;
-    else if (e && e[0] == 'f') variant = 0;
     else if (e && e[0] == 't' && e[1] == 'c' && e[2] == '1') variant = 2;
     else variant = 3;
   }
@@ -2424,12 +2134,10 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   static bool attr = false;
   const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
   const int smem_tc = T_Q_BYTES + T_P_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
-  const int smem_fa = T_Q_BYTES + F_P_BYTES + F_STAGES * F_STAGE_BYTES + 1024;
   const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
   if (!attr) {
     BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mma));
     BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
-    BST_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_fa));
     BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc2));
     attr = true;
   }
@@ -2453,17 +2161,15 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   else {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_kv, n_splits, row_blocks * n_req);
-    cfg.blockDim = dim3(v == 2 ? T_THREADS : (v == 3 ? T2_THREADS : F_THREADS));
-    cfg.dynamicSmemBytes = v == 0 ? smem_fa : (v == 3 ? smem_tc2 : smem_tc);
+    cfg.blockDim = dim3(v == 2 ? T_THREADS : T2_THREADS);
+    cfg.dynamicSmemBytes = v == 3 ? smem_tc2 : smem_tc;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (v == 0)
-      BST_CUDA(cudaLaunchKernelEx(&cfg, attn_fa_kernel, tm, a));
-    else if (v == 2)
+    if (v == 2)
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, a));
     else
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc2_kernel, tm, a));
@@ -2562,9 +2268,9 @@ extern "C" int bst_debug_kt_ablate(int v) {
 }
 
 // Select the K3 kernel family: 3 row-major tcgen05 (default), 4 key-major, 2 tc1 only,
-// 1 mma.sync, 0 experimental FA-style; -1 re-reads BST_ATTN.
+// 1 mma.sync; -1 re-reads BST_ATTN.
 extern "C" int bst_attention_set_variant(int v) {
-  BST_REQUIRE(v >= -1 && v <= 4, "variant must be in -1..4");
+  BST_REQUIRE(v == -1 || (v >= 1 && v <= 4), "variant must be -1 or 1..4");
   bst::g_attn_variant = v;
   return BST_OK;
 }
