@@ -12,8 +12,9 @@ from paper_2605_29727_b200.engine.config import QWEN3_8B, DrafterConfig  # noqa:
 from paper_2605_29727_b200.engine.decode import B200Engine  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 31
-eng = B200Engine(QWEN3_8B, DrafterConfig(layers=5, gamma=16, logit_scale=6.0), max_ctx=4096, n_cap=255)
-eng.reset(np.random.default_rng(0).integers(0, QWEN3_8B.V - 1, 2049).tolist())
+ctx = int(os.environ.get("CTX", "2048"))  # prompt context (32768: config 4)
+eng = B200Engine(QWEN3_8B, DrafterConfig(layers=5, gamma=16, logit_scale=6.0), max_ctx=ctx + 2048, n_cap=255)
+eng.reset(np.random.default_rng(0).integers(0, QWEN3_8B.V - 1, ctx + 1).tolist())
 eng.set_policy("fixed", n=n)
 nn, _ = eng.draft()
 rows = eng._bucket(nn)
