@@ -271,8 +271,10 @@ def plan_tree(lattice: CandidateLattice, policy: Policy, cfg: ControllerConfig,
 def decode_full(pair, cfg: SimConfig, policy: Policy, estimator: VerifyLatencyEstimator):
     """Decode until run_length tokens are committed; returns (records, tokens) (verify_sim.py:426-461)."""
     rule = pair[1] if isinstance(pair, tuple) else pair
-    if hasattr(rule, "engine_decode"):
-        return rule.engine_decode(cfg, policy, estimator)
+    if hasattr(rule, "engine_decode") and policy.kind in ("adaptive", "fixed"):
+        return rule.engine_decode(cfg, policy, estimator)  # the whole loop on the device
+    # any other policy (greedy chain, beam) runs the reference loop below; a GPU engine
+    # still serves it through the plugin protocol (drafter_marginals / tree_argmax)
     lat = cfg.controller.latencies
     cache = SimCache()
     records: list[CycleRecord] = []

@@ -245,3 +245,20 @@ def test_general_facade_loop_matches_engine_fast_path(eng, temperature):
         assert list(ar) == eng.ar_decode(12)
     finally:
         eng.set_temperature(0.0, 0)
+
+
+def test_beam_policy_runs_through_the_plugin_protocol(eng):
+    """Policies the on-device loop does not implement (beam, greedy chain) run the façade's
+    reference loop with the engine as plugin; the committed stream is the engine's own."""
+    import paper_2605_29727_b200 as P
+    prompt = _prompt(40, eng.cfg.V, seed=8)
+    est = P.VerifyLatencyEstimator(eng.cfg.cost_params(1.6e15, 6.5e12))
+    lat = P.CycleLatencies(t_draft=3e-4, t_aux=0.0, l_ar=1e-3)
+    sim = P.SimConfig(controller=P.ControllerConfig(n_max=32, latencies=lat, variant="static",
+                                                    context_len=len(prompt) - 1), run_length=20, top_k=eng.top_k)
+    eng.set_temperature(0.0, 0)
+    for pol in (P.Policy.beam(2, 4), P.Policy.greedy_chain()):
+        eng.reset(prompt)
+        recs, toks = P.decode_full(eng, sim, pol, est)
+        assert len(toks) >= 20 and all(r.tree_size >= 1 for r in recs)
+        assert tuple(eng.tokens())[: len(toks) - recs[-1].accepted_len] == tuple(toks)[: len(toks) - recs[-1].accepted_len]
