@@ -106,3 +106,45 @@ def test_causal_and_full_attention_with_device_c(mode, c, s, variant):
     ref = _ref(q, kv, 1, n_q, n_kv, c, s, vis)
     torch.cuda.synchronize()
     assert (out.float() - ref).abs().max().item() < 2e-2
+
+
+@pytest.mark.parametrize("c", [2048, 20000])
+def test_back_to_back_launches_in_a_graph(c, variant):
+    """PDL lets the CTAs of the next K3 launch start while the previous one merges its
+    splits; the alternating workspace banks keep them apart (layer parity).  A graph of
+    back-to-back launches over distinct layers must reproduce the eager results bitwise."""
+    from paper_2605_29727_b200 import ops
+    from paper_2605_29727_b200.engine.forward import PagedKV
+    n_q, n_kv, s, L = 32, 8, 17, 6
+    g = torch.Generator(device="cuda").manual_seed(c)
+    kv = PagedKV(L, n_kv, c + s + 64, "cuda")
+    kv.buf.normal_(0, 1, generator=g)
+    q = torch.randn(s, n_q * 128, device="cuda", generator=g).to(torch.bfloat16)
+    words = 1
+    anc = torch.full((s, words), -1, dtype=torch.int32, device="cuda")
+    ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
+    outs = [torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16) for _ in range(L)]
+
+    def run():
+        for li in range(L):
+            ops.attention(q, outs[li], kv.buf, L, kv.n_pages, li, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0,
+                          anc.view(-1), words, ws)
+    run()
+    torch.cuda.synchronize()
+    want = [o.clone() for o in outs]
+    st = torch.cuda.Stream()
+    with torch.cuda.stream(st):
+        run()
+    st.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=st):
+        run()
+    for _ in range(3):
+        for o in outs:
+            o.zero_()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(st):
+            graph.replay()
+        st.synchronize()
+        for o, w in zip(outs, want):
+            assert torch.equal(o, w)
