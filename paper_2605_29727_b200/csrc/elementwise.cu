@@ -46,19 +46,50 @@ __device__ __forceinline__ float block_sum(float v, float* sh) {
 __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const __nv_bfloat16* __restrict__ emb, int h,
                                      const __nv_bfloat16* __restrict__ w, float eps, float* __restrict__ resid,
                                      __nv_bfloat16* __restrict__ x, int64_t ldx) {
+  // one row per CTA; 16-byte chunks of 8 columns held in registers (h <= 8192, h % 8 == 0)
   pdl_enter();
   __shared__ float sh[32];
+  constexpr int CPT = 4;  // chunks per thread (E_THREADS x 8 x CPT columns)
   const int t = blockIdx.x;
   const int64_t tok = tokens[t];
+  const int nc = h >> 3;
+  float v[CPT][8];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < h; i += blockDim.x) {
-    float v = __bfloat162float(emb[tok * h + i]);
-    resid[(int64_t)t * h + i] = v;
-    ss += v * v;
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int c = threadIdx.x + j * E_THREADS;
+    if (c < nc) {
+      const uint4 raw = reinterpret_cast<const uint4*>(emb + tok * h)[c];
+      const __nv_bfloat162* b = reinterpret_cast<const __nv_bfloat162*>(&raw);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 f = __bfloat1622float2(b[e]);
+        v[j][2 * e] = f.x;
+        v[j][2 * e + 1] = f.y;
+        ss += f.x * f.x + f.y * f.y;
+      }
+      float4* rp = reinterpret_cast<float4*>(resid + (int64_t)t * h) + 2 * c;
+      rp[0] = make_float4(v[j][0], v[j][1], v[j][2], v[j][3]);
+      rp[1] = make_float4(v[j][4], v[j][5], v[j][6], v[j][7]);
+    }
   }
   const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
-  for (int i = threadIdx.x; i < h; i += blockDim.x)
-    x[(int64_t)t * ldx + i] = __float2bfloat16(resid[(int64_t)t * h + i] * inv * __bfloat162float(w[i]));
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const int c = threadIdx.x + j * E_THREADS;
+    if (c < nc) {
+      const uint4 wr = reinterpret_cast<const uint4*>(w)[c];
+      const __nv_bfloat162* wb = reinterpret_cast<const __nv_bfloat162*>(&wr);
+      uint4 o;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float2 wf = __bfloat1622float2(wb[e]);
+        ob[e] = __floats2bfloat162_rn(v[j][2 * e] * inv * wf.x, v[j][2 * e + 1] * inv * wf.y);
+      }
+      reinterpret_cast<uint4*>(x + (int64_t)t * ldx)[c] = o;
+    }
+  }
 }
 
 // ------------------------------------------------------- residual + norm
@@ -159,6 +190,7 @@ using namespace bst;
 extern "C" int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* emb, int h, const void* w, float eps,
                                  float* resid, void* x, int64_t ldx, bst_stream_t stream) {
   BST_REQUIRE(tokens && emb && w && resid && x, "null pointer argument");
+  BST_REQUIRE(h % 8 == 0 && h <= 8 * 4 * E_THREADS && ldx % 8 == 0, "embedding width must be a multiple of 8, <= 8192");
   BST_CUDA(launch_pdl(embed_rmsnorm_kernel, dim3(rows), dim3(E_THREADS), 0, as_stream(stream), 
       tokens, static_cast<const __nv_bfloat16*>(emb), h, static_cast<const __nv_bfloat16*>(w), eps, resid,
       static_cast<__nv_bfloat16*>(x), ldx));
