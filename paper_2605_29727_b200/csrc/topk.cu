@@ -266,10 +266,13 @@ __device__ __forceinline__ float key_logit(unsigned long long k) {
 }
 __device__ __forceinline__ int key_tok(unsigned long long k) { return (int)(0xFFFFFFFFu - (unsigned)(k & 0xFFFFFFFFu)); }
 
-// block-wide: top-n keys (descending) of per-thread candidate lists
+// block-wide: top-n keys (descending) of per-thread candidate lists.  Each warp first
+// extracts its own top-n with warp shuffles (no block barrier per round), then warp 0
+// merges the warps' candidates; keys are unique (token in the low bits).
 __device__ void block_top_keys(unsigned long long (&c)[TK_PER_THREAD], int n, unsigned long long* out) {
-  __shared__ unsigned long long wbest[TK_THREADS / 32];
-  __shared__ unsigned long long gbest;
+  constexpr int NW = TK_THREADS / 32;
+  constexpr int PL = (NW * TK_KP_MAX + 31) / 32;  // merge candidates per lane of warp 0
+  __shared__ unsigned long long cand[NW][TK_KP_MAX];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int r = 0; r < n; ++r) {
     unsigned long long b = 0;
@@ -280,20 +283,35 @@ __device__ void block_top_keys(unsigned long long (&c)[TK_PER_THREAD], int n, un
       const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
       b = ob > b ? ob : b;
     }
-    if (lane == 0) wbest[warp] = b;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long g = 0;
-      for (int w = 0; w < TK_THREADS / 32; ++w) g = wbest[w] > g ? wbest[w] : g;
-      gbest = g;
-      out[r] = g;
-    }
-    __syncthreads();
-    const unsigned long long g = gbest;
+    if (lane == 0) cand[warp][r] = b;
 #pragma unroll
     for (int i = 0; i < TK_PER_THREAD; ++i)
-      if (c[i] == g) c[i] = 0;  // keys are unique (token in the low bits)
+      if (c[i] == b) c[i] = 0;
   }
+  __syncthreads();
+  if (warp == 0) {
+    unsigned long long m[PL];
+#pragma unroll
+    for (int i = 0; i < PL; ++i) {
+      const int j = i * 32 + lane;  // candidate j = (warp j / n, rank j % n)
+      m[i] = j < NW * n ? cand[j / n][j % n] : 0ull;
+    }
+    for (int r = 0; r < n; ++r) {
+      unsigned long long b = 0;
+#pragma unroll
+      for (int i = 0; i < PL; ++i) b = m[i] > b ? m[i] : b;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+        b = ob > b ? ob : b;
+      }
+      if (lane == 0) out[r] = b;
+#pragma unroll
+      for (int i = 0; i < PL; ++i)
+        if (m[i] == b) m[i] = 0;
+    }
+  }
+  __syncthreads();
 }
 
 // A: per (chunk, row): fp32 max m_c, fp64 S_c = sum exp(l - m_c), top-(K+1) keys
