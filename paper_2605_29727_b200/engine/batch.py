@@ -64,7 +64,7 @@ class BatchEngine:
         G1 = self.gamma + 1
         self.G1 = G1
         self.chunk_v = max(1, MAX_ROWS // self.S)          # requests per verify chunk
-        self.chunk_d = max(1, MAX_ROWS // (2 * G1))        # requests per draft chunk
+        self.chunk_d = max(1, MAX_ROWS // G1)              # requests per draft chunk (block rows <= 256)
         self.max_ctx = max_ctx
         self.req_pages = math.ceil((max_ctx + MAX_ROWS + PAGE) / PAGE)
         slots = n_req * self.req_pages * PAGE

@@ -194,7 +194,7 @@ class DrafterModel:
         self.slot = torch.zeros(R, **i32)
         self.qrow = torch.zeros(R, **i32)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h), (h, n_feat * h)]
-        self.partial = torch.empty(_max_partial(shapes, R), **f32)
+        self.partial = torch.empty(_max_partial(shapes, min(R, 256)), **f32)  # every GEMM call has <= 256 rows
         self.attn_ws = torch.zeros(_attn_ws_floats(cfg, QB, self.kv.n_pages), **f32)
         self.attn_splits = 0
         self.logits = torch.empty(dcfg.gamma, cfg.V, **f32)
@@ -261,9 +261,13 @@ class DrafterModel:
         xb, resid = self.X[:QB], self.resid[:QB]
         ops.embed_rmsnorm(self.tokens, QB, self.tw.emb, w.layers[0].in_norm, eps, resid, xb)
         for li, lw in enumerate(w.layers):
-            ops.gemm_qkv_rope(self.X[:M], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm,
-                              lw.k_norm, eps, self.inv_freq, self.pos, self.slot, self.qrow, self.q, self.kv.buf,
-                              li * self.kv.layer_stride, pt, PAGE, state, (B, QB, rs, req_pages * PAGE))
+            # block rows, then context rows: two GEMMs of <= 256 rows each (the K4 row limit), so
+            # a chunk of up to 256 / (gamma + 1) requests shares every drafter weight pass
+            for lo, hi in ((0, QB), (QB, M)):
+                ops.gemm_qkv_rope(self.X[lo:hi], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm,
+                                  lw.k_norm, eps, self.inv_freq, self.pos[lo:], self.slot[lo:], self.qrow[lo:],
+                                  self.q, self.kv.buf, li * self.kv.layer_stride, pt, PAGE, state,
+                                  (B, QB, rs, req_pages * PAGE))
             ops.attention_batch(self.q[:QB], self.attn[:QB], self.kv.buf, self.dcfg.layers, self.kv.n_pages, li, pt,
                                 req_pages, cfg.n_q, cfg.n_kv, n, B, B, req_pages * PAGE, state, rs, MODE_FULL, None,
                                 0, self.attn_ws, n_splits=self.attn_splits)
