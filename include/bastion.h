@@ -166,9 +166,11 @@ int bst_kv_compact(void* kv, int n_layers, int n_kv, int head_dim, int page_size
 typedef struct {
   int32_t n_out, k, m, bn;      /* bn = round_up(m, 16) token columns (<= 256) */
   int32_t n_mt, n_kb, grid, s_max;
-  int64_t units;                /* n_mt * n_kb */
+  int64_t units;                /* ceil(n_mt / pair) * n_kb */
   int32_t tmem_cols, stages;
   int64_t partial_floats;       /* size of the partial buffer */
+  int32_t pair;                 /* weight tiles per stream-K unit (1, or 2 for m > 128: X k-block shared) */
+  int32_t reserved;
 } bst_gemm_sched_t;
 
 int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sched_t* out);

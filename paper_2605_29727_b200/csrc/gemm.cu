@@ -36,6 +36,7 @@ constexpr int G_BK = 64;
 constexpr int G_TILE_W = G_BM * G_BK * 2;  // 16 KiB
 constexpr int G_MAX_STAGES = 12;
 constexpr int G_SMEM_BUDGET = 160 * 1024;  // leaves room for a co-resident epilogue CTA (PDL overlap)
+constexpr int G_SMEM_BUDGET_PAIR = 200 * 1024;  // pair mode: 3 stages of 2 weight tiles + a 256-row X block
 
 // ------------------------------------------------------------ tensor maps
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
@@ -129,7 +130,7 @@ __device__ __forceinline__ void gtrace(int k) {
 }
 
 struct Seg {
-  int tile, kb_lo, kb_hi, slot;
+  int tile, kb_lo, kb_hi, slot;  // tile = super-tile index (first weight tile = tile * TP)
 };
 
 __device__ __forceinline__ bool next_seg(const bst_gemm_sched_t& s, int64_t& u, int64_t u1, Seg& seg) {
@@ -137,11 +138,15 @@ __device__ __forceinline__ bool next_seg(const bst_gemm_sched_t& s, int64_t& u, 
   seg.tile = (int)(u / s.n_kb);
   seg.kb_lo = (int)(u % s.n_kb);
   { const int64_t lim = (int64_t)seg.kb_lo + (u1 - u); seg.kb_hi = (int)(lim < s.n_kb ? lim : s.n_kb); }
-  seg.slot = (int)blockIdx.x - sched_first_cta(s, seg.tile);
+  seg.slot = (int)blockIdx.x - sched_first_st(s, seg.tile);
   u += seg.kb_hi - seg.kb_lo;
   return true;
 }
 
+// TP = weight tiles per unit.  TP = 2 (m > 128): each stage holds two 128-row weight
+// tiles and one X k-block, and the issuer runs two MMAs into two TMEM accumulators,
+// halving the X re-reads from L2 per weight byte (profiles/r1_gemm_m256_tensor.txt).
+template <int TP>
 __global__ void __launch_bounds__(G_THREADS, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
                      bst_gemm_sched_t s, float* __restrict__ partial, int stages, int trigger) {
@@ -156,8 +161,10 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
   const int bn = s.bn;
   const uint32_t x_bytes = (uint32_t)bn * G_BK * 2;
-  const uint32_t stage_bytes = G_TILE_W + x_bytes;
+  const uint32_t stage_bytes = TP * G_TILE_W + x_bytes;
   const uint32_t tcols = s.tmem_cols;
+  // accumulator buffers: two when 2 * TP * bn columns fit in the allocation
+  const int nacc = (int)tcols >= 2 * TP * bn ? 2 : 1;
 
   if (warp == 0 && lane == 0) {
     sm100::prefetch_tmap(&tmW);
@@ -188,16 +195,23 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       int64_t u = u0;
       Seg seg;
       int issued = 0;
+      // weight tiles of super-tile st present in the matrix (the last one may be short)
+      auto ntiles = [&](int st) { return TP == 1 ? 1 : (st * TP + 1 < s.n_mt ? 2 : 1); };
+      auto load_w = [&](uint8_t* sw, uint64_t* bar, int kb, int st, int nt) {
+        for (int t = 0; t < nt; ++t)
+          sm100::tma_load_2d_hint(sw + t * G_TILE_W, &tmW, bar, kb * G_BK, (st * TP + t) * G_BM, pol_w);
+      };
       // pass 1: prologue weights
       {
         int64_t uu = u0;
         Seg sg;
         int st = 0;
         while (st < stages && next_seg(s, uu, u1, sg)) {
+          const int nt = ntiles(sg.tile);
           for (int kb = sg.kb_lo; kb < sg.kb_hi && st < stages; ++kb, ++st) {
             uint8_t* sw = smem + st * stage_bytes;
-            sm100::mbar_add_tx(&full[st], G_TILE_W);
-            sm100::tma_load_2d_hint(sw, &tmW, &full[st], kb * G_BK, sg.tile * G_BM, pol_w);
+            sm100::mbar_add_tx(&full[st], nt * G_TILE_W);
+            load_w(sw, &full[st], kb, sg.tile, nt);
           }
         }
         issued = st;
@@ -207,17 +221,17 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       gtrace(3);
       int idx = 0;
       while (next_seg(s, u, u1, seg)) {
+        const int nt = ntiles(seg.tile);
         for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb, ++idx) {
           uint8_t* sw = smem + stage * stage_bytes;
           if (idx < issued) {  // weights already in flight: add the X tile and arrive
             sm100::mbar_expect_tx(&full[stage], x_bytes);
-            sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
           } else {
             sm100::mbar_wait(&empty[stage], phase ^ 1);
-            sm100::mbar_expect_tx(&full[stage], stage_bytes);
-            sm100::tma_load_2d_hint(sw, &tmW, &full[stage], kb * G_BK, seg.tile * G_BM, pol_w);
-            sm100::tma_load_2d(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
+            sm100::mbar_expect_tx(&full[stage], nt * G_TILE_W + x_bytes);
+            load_w(sw, &full[stage], kb, seg.tile, nt);
           }
+          sm100::tma_load_2d(sw + TP * G_TILE_W, &tmX, &full[stage], kb * G_BK, 0);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -231,21 +245,29 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     Seg seg;
     int j = 0;
     while (next_seg(s, u, u1, seg)) {
-      const int acc = j & 1;
-      sm100::mbar_wait(&tempty[acc], ((j >> 1) & 1) ^ 1);
+      const int acc = nacc == 2 ? (j & 1) : 0;
+      const int use = nacc == 2 ? (j >> 1) : j;
+      const int nt = TP == 1 ? 1 : (seg.tile * TP + 1 < s.n_mt ? 2 : 1);
+      sm100::mbar_wait(&tempty[acc], (use & 1) ^ 1);
       sm100::tc_fence_after();
-      const uint32_t d = tmem + acc * bn;
+      const uint32_t d = tmem + acc * TP * bn;
       for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
         sm100::mbar_wait(&full[stage], phase);
         if (lane == 0) gtrace(8 + (kb - seg.kb_lo) + j * 24);
         sm100::tc_fence_after();
         if (sm100::elect_one()) {
           const uint32_t a_addr = base + stage * stage_bytes;
-          const uint64_t adesc = sm100::desc_k_sw128(a_addr);
-          const uint64_t bdesc = sm100::desc_k_sw128(a_addr + G_TILE_W);
+          const uint64_t bdesc = sm100::desc_k_sw128(a_addr + TP * G_TILE_W);
 #pragma unroll
-          for (int k = 0; k < G_BK / 16; ++k)  // +32 B per K=16 step inside the 128B swizzle atom
-            sm100::umma_f16(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+          for (int t = 0; t < TP; ++t) {
+            if (t < nt) {
+              const uint64_t adesc = sm100::desc_k_sw128(a_addr + t * G_TILE_W);
+#pragma unroll
+              for (int k = 0; k < G_BK / 16; ++k)  // +32 B per K=16 step inside the 128B swizzle atom
+                sm100::umma_f16(d + t * bn, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+            }
+          }
           sm100::umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -263,17 +285,21 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     Seg seg;
     int j = 0;
     while (next_seg(s, u, u1, seg)) {
-      const int acc = j & 1;
-      sm100::mbar_wait(&tfull[acc], (j >> 1) & 1);
+      const int acc = nacc == 2 ? (j & 1) : 0;
+      const int use = nacc == 2 ? (j >> 1) : j;
+      const int nt = TP == 1 ? 1 : (seg.tile * TP + 1 < s.n_mt ? 2 : 1);
+      sm100::mbar_wait(&tfull[acc], use & 1);
       sm100::tc_fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * bn;
-      float* dst = partial + ((int64_t)(seg.tile * s.s_max + seg.slot) * bn) * G_BM + row;
-      for (int c0 = 0; c0 < bn; c0 += 16) {
-        float v[16];
-        sm100::tmem_ld16(taddr + c0, v);
+      for (int t = 0; t < nt; ++t) {
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (acc * TP + t) * bn;
+        float* dst = partial + ((int64_t)((seg.tile * TP + t) * s.s_max + seg.slot) * bn) * G_BM + row;
+        for (int c0 = 0; c0 < bn; c0 += 16) {
+          float v[16];
+          sm100::tmem_ld16(taddr + c0, v);
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-          if (c0 + i < s.m) dst[(int64_t)(c0 + i) * G_BM] = v[i];
+          for (int i = 0; i < 16; ++i)
+            if (c0 + i < s.m) dst[(int64_t)(c0 + i) * G_BM] = v[i];
+        }
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -437,13 +463,23 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   s.bn = ((m + 15) / 16) * 16;
   s.n_mt = (n_out + G_BM - 1) / G_BM;
   s.n_kb = (k + G_BK - 1) / G_BK;
-  s.units = (int64_t)s.n_mt * s.n_kb;
   if (grid <= 0) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     grid = sms;
   }
+  // two weight tiles per unit above pair_min_bn token columns (BST_GEMM_PAIR_MIN_BN:
+  // measurement knob, 0 disables)
+  static int pair_min_bn = -1;
+  if (pair_min_bn < 0) {
+    const char* e = getenv("BST_GEMM_PAIR_MIN_BN");
+    pair_min_bn = e ? atoi(e) : 144;
+  }
+  // pair mode loses TMEM double buffering at bn > 128 and doubles each CTA's partial
+  // tile, so it only pays when every CTA streams at least one full tile (n_mt >= grid)
+  s.pair = (pair_min_bn > 0 && s.bn >= pair_min_bn && s.n_mt >= grid) ? 2 : 1;
+  s.units = (int64_t)((s.n_mt + s.pair - 1) / s.pair) * s.n_kb;
   s.grid = (int)(s.units < grid ? s.units : grid);
   int smax = 1;
   for (int t = 0; t < s.n_mt; ++t) {
@@ -452,15 +488,18 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   }
   s.s_max = smax;
   int tc = 32;
-  while (tc < 2 * s.bn) tc <<= 1;
+  while (tc < 2 * s.pair * s.bn && tc < 512) tc <<= 1;  // double buffered when it fits
   s.tmem_cols = tc;
-  const int stage_bytes = G_TILE_W + s.bn * G_BK * 2;
-  static int budget = 0;
+  const int stage_bytes = s.pair * G_TILE_W + s.bn * G_BK * 2;
+  static int budget = 0, budget_pair = 0;
   if (!budget) {
-    const char* e = getenv("BST_GEMM_SMEM_KB");  // measurement knob
+    const char* e = getenv("BST_GEMM_SMEM_KB");  // measurement knobs
     budget = e ? atoi(e) * 1024 : G_SMEM_BUDGET;
+    e = getenv("BST_GEMM_PAIR_SMEM_KB");
+    budget_pair = e ? atoi(e) * 1024 : G_SMEM_BUDGET_PAIR;
   }
-  int stages = (budget - 1024) / stage_bytes;
+  int stages = ((s.pair == 2 ? budget_pair : budget) - 1024) / stage_bytes;
+  BST_REQUIRE(stages >= 2, "GEMM smem budget too small for two stages");
   s.stages = stages > G_MAX_STAGES ? G_MAX_STAGES : stages;
   s.partial_floats = (int64_t)s.n_mt * s.s_max * s.bn * G_BM;
   *out = s;
@@ -479,11 +518,13 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
   if (rc) return rc;
   rc = make_tmap_bf16(&tx, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)s.bn, G_BK);
   if (rc) return rc;
-  const int smem = s.stages * (G_TILE_W + s.bn * G_BK * 2) + 1024;
-  static int configured = 0;
-  if (smem > configured) {
-    BST_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = smem;
+  BST_REQUIRE(s.pair == 1 || s.pair == 2, "bad schedule (pair=%d)", s.pair);
+  const int smem = s.stages * (s.pair * G_TILE_W + s.bn * G_BK * 2) + 1024;
+  static int configured[3] = {0, 0, 0};
+  auto kern = s.pair == 2 ? gemm_bf16_kernel<2> : gemm_bf16_kernel<1>;
+  if (smem > configured[s.pair]) {
+    BST_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    configured[s.pair] = smem;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(s.grid);
@@ -501,7 +542,7 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
   // BST_GEMM_TRIGGER=0 disables it (measurement).
   static int trigger = -1;
   if (trigger < 0) trigger = getenv("BST_GEMM_TRIGGER") ? atoi(getenv("BST_GEMM_TRIGGER")) : 1;
-  BST_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel, tw, tx, s, partial, (int)s.stages, trigger));
+  BST_CUDA(cudaLaunchKernelEx(&cfg, kern, tw, tx, s, partial, (int)s.stages, trigger));
   return BST_OK;
 }
 

@@ -5,23 +5,33 @@
 
 namespace bst {
 
-// CTA c owns units [floor(c*U/G), floor((c+1)*U/G)); unit = tile*n_kb + k_block.
-__host__ __device__ __forceinline__ int sched_first_cta(const bst_gemm_sched_t& s, int tile) {
-  int64_t a = ((int64_t)tile * s.n_kb + 1) * s.grid;
+// Stream-K over units = (super-tile, k_block); a super-tile is s.pair (1 or 2)
+// consecutive 128-row weight tiles that share each X k-block.  CTA c owns units
+// [floor(c*U/G), floor((c+1)*U/G)); unit = st*n_kb + k_block.
+__host__ __device__ __forceinline__ int tile_st(const bst_gemm_sched_t& s, int tile) { return tile >> (s.pair >> 1); }
+__host__ __device__ __forceinline__ int sched_first_st(const bst_gemm_sched_t& s, int st) {
+  int64_t a = ((int64_t)st * s.n_kb + 1) * s.grid;
   int64_t c = (a + s.units - 1) / s.units - 1;
   return (int)(c < 0 ? 0 : (c >= s.grid ? s.grid - 1 : c));
 }
-__host__ __device__ __forceinline__ int sched_last_cta(const bst_gemm_sched_t& s, int tile) {
-  int64_t a = ((int64_t)(tile + 1) * s.n_kb) * s.grid;
+__host__ __device__ __forceinline__ int sched_last_st(const bst_gemm_sched_t& s, int st) {
+  int64_t a = ((int64_t)(st + 1) * s.n_kb) * s.grid;
   int64_t c = (a + s.units - 1) / s.units - 1;
   return (int)(c < 0 ? 0 : (c >= s.grid ? s.grid - 1 : c));
+}
+__host__ __device__ __forceinline__ int sched_first_cta(const bst_gemm_sched_t& s, int tile) {
+  return sched_first_st(s, tile_st(s, tile));
+}
+__host__ __device__ __forceinline__ int sched_last_cta(const bst_gemm_sched_t& s, int tile) {
+  return sched_last_st(s, tile_st(s, tile));
 }
 
 // 32-bit fast path of the slot lookup (units * grid < 2^32 for every verify shape).
 __device__ __forceinline__ int tile_nslot(const bst_gemm_sched_t& s, int tile) {
   const uint32_t U = (uint32_t)s.units, G = (uint32_t)s.grid, kb = (uint32_t)s.n_kb;
-  const uint32_t first = ((uint32_t)tile * kb + 1) * G;
-  const uint32_t last = ((uint32_t)(tile + 1) * kb) * G;
+  const uint32_t st = (uint32_t)tile_st(s, tile);
+  const uint32_t first = (st * kb + 1) * G;
+  const uint32_t last = ((st + 1) * kb) * G;
   int f = (int)((first + U - 1) / U) - 1, l = (int)((last + U - 1) / U) - 1;
   f = f < 0 ? 0 : (f >= (int)G ? (int)G - 1 : f);
   l = l < 0 ? 0 : (l >= (int)G ? (int)G - 1 : l);

@@ -1,6 +1,7 @@
 """K4 per-shape HBM rate in steady state: a CUDA graph of 36 back-to-back launches of one
 verify shape over 36 distinct weight matrices (>> L2), as in the verify forward."""
 import json
+import os
 import statistics
 import sys
 from pathlib import Path
@@ -12,10 +13,13 @@ from paper_2605_29727_b200 import ops  # noqa: E402
 
 peak = json.loads((Path(__file__).resolve().parents[1] / "MEASURED_PEAKS.json").read_text())["hbm_gbs"]
 shapes = [("qkv", 6144, 4096), ("o", 4096, 4096), ("gate_up", 24576, 4096), ("down", 4096, 12288)]
+if os.environ.get("LM_HEAD"):
+    shapes = [("lm_head", 151936, 4096)]
+NW = int(os.environ.get("NW", "36"))
 st = torch.cuda.Stream()
 for m in [int(a) for a in (sys.argv[1:] or ["16", "64"])]:
     for name, n, k in shapes:
-        ws = [(torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16) for _ in range(36)]
+        ws = [(torch.randn(n, k, device="cuda") * 0.02).to(torch.bfloat16) for _ in range(NW)]
         x = torch.randn(m, k, device="cuda").to(torch.bfloat16)
         buf = ops.gemm_partial(x, ws[0]).buf
 
@@ -37,7 +41,7 @@ for m in [int(a) for a in (sys.argv[1:] or ["16", "64"])]:
             b.record(st)
             b.synchronize()
             if it >= 1:
-                ts.append(a.elapsed_time(b) * 1e-3 / 36)
+                ts.append(a.elapsed_time(b) * 1e-3 / NW)
         t = statistics.median(ts)
         byts = n * k * 2 + m * k * 2
         print(json.dumps(dict(m=m, shape=name, n=n, k=k, us=round(t * 1e6, 2), GBps=round(byts / t / 1e9),

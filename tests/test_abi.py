@@ -85,3 +85,23 @@ def test_cost_model_facade_matches_golden():
         for s, want, want_est in zip(row["s"], row["curve"], row["estimate"]):
             assert curve.latency(s) == unhex(want)
             assert est.estimate(s, row["c"]) == unhex(want_est)
+
+
+def test_gemm_schedule_pair_mode_and_slot_cover():
+    """Stream-K schedule (host side, explicit grid, no GPU): two weight tiles per unit
+    above 128 token columns, and every CTA's unit range maps to a valid partial slot."""
+    from paper_2605_29727_b200 import ops
+    for n_out, k, m, pair in [(24576, 4096, 256, 2), (300, 4096, 256, 1), (4096, 12288, 129, 1), (151936, 4096, 129, 2),
+                              (6144, 4096, 128, 1), (151936, 4096, 64, 1), (128, 4096, 256, 1)]:
+        s = ops.gemm_schedule(n_out, k, m, 148)
+        assert s.pair == pair, (n_out, m, s.pair)
+        n_st = -(-s.n_mt // s.pair)
+        assert s.units == n_st * s.n_kb
+        assert s.partial_floats == s.n_mt * s.s_max * s.bn * 128
+        assert s.tmem_cols <= 512 and s.stages >= 2
+        # every CTA's first unit lies in a super-tile whose slot count covers it
+        for c in range(s.grid):
+            u0 = c * s.units // s.grid
+            st = u0 // s.n_kb
+            first = max(0, min(s.grid - 1, -(-((st * s.n_kb + 1) * s.grid) // s.units) - 1))
+            assert 0 <= c - first < s.s_max

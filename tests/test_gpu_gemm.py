@@ -6,7 +6,9 @@ import torch
 pytestmark = pytest.mark.gpu
 
 SHAPES = [(64, 64, 5), (200, 136, 1), (6144, 4096, 17), (4096, 4096, 1), (24576, 4096, 33), (4096, 12288, 100),
-          (1024, 4096, 256), (300, 4096, 256), (4096, 20480, 17), (151936, 4096, 17), (128, 64, 16)]
+          (1024, 4096, 256), (300, 4096, 256), (4096, 20480, 17), (151936, 4096, 17), (128, 64, 16),
+          # pair mode (two weight tiles per stream-K unit, bn > 128), odd tile counts included
+          (24576, 4096, 256), (151936, 4096, 144), (37888, 4096, 200), (18944, 512, 256)]
 
 
 @pytest.mark.parametrize("n_out,k,m", SHAPES)
