@@ -15,11 +15,15 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
-BUILD = PKG / "_build"
-LIB = PKG / "libbastion.so"
+# measurement builds go to their own directory / library (load with BASTION_LIB=...):
+# BST_TRACE=1 -> libbastion_trace.so; BST_BUILD_TAG=x with BST_NVCC_EXTRA="-D..." -> libbastion_x.so
+_TAG = "trace" if os.environ.get("BST_TRACE") == "1" else os.environ.get("BST_BUILD_TAG", "")
+BUILD = PKG / (f"_build_{_TAG}" if _TAG else "_build")
+LIB = PKG / (f"libbastion_{_TAG}.so" if _TAG else "libbastion.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 TRACE = ["-DBST_TRACE"] if os.environ.get("BST_TRACE") == "1" else []  # phase tracing builds
+TRACE += os.environ.get("BST_NVCC_EXTRA", "").split() if os.environ.get("BST_BUILD_TAG") else []
 BASE = TRACE + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{ROOT / 'include'}",
         "-Xptxas", "-warn-spills", "--expt-relaxed-constexpr", "-diag-suppress", "550,177"]
 # fp64 controller arithmetic must not be contracted into FMAs (bit parity with Python floats)

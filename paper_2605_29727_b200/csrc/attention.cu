@@ -23,6 +23,8 @@
 
 namespace bst {
 
+BST_BND_TRACE_DEF
+
 constexpr int A_D = 128;
 constexpr int A_PAGE = 64;
 constexpr int A_WARPS = 8;
@@ -63,6 +65,7 @@ struct AttnArgs {
   int n_req, req_pages, req_state;
   int rows_per_block;      // key-major kernel: query rows per CTA (row blocks balanced over R)
   bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
+  int seq;                 // boundary-trace launch number (BST_TRACE builds)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
@@ -622,6 +625,26 @@ __global__ void __launch_bounds__(A_THREADS, 1)
 }
 
 
+// ---- distributed shared memory (thread-block clusters)
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
+  float2 v;
+  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // ===========================================================================
 // tcgen05 variant (default): S = Q K^T and O += P V on the 5th-gen tensor cores.
 // One CTA = one KV head x one KV split x up to 128 query rows (UMMA M = 128).
@@ -643,6 +666,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   __shared__ uint32_t tmem_sh;
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) TRACE(31, 0);
+  if (threadIdx.x == 0) BND(a.seq, 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) BND_KIND(a.seq, 5);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
@@ -758,6 +783,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     const float scale = a.scale_log2;
     sm100::grid_dep_wait();  // q is produced by the previous kernel (PDL)
     if (threadIdx.x == 64) TRACE(31, 2);
+    if (threadIdx.x == 64) BND(a.seq, 2);
+    if (threadIdx.x == 64) BND(a.seq, 3);
     if (threadIdx.x == 64) TRACE_MAX(0);
     {  // stage Q row (256 B) into the swizzled K-major tile
       const int4* src = reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D);
@@ -917,6 +944,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     sm100::tc_fence_after();
     sm100::tmem_dealloc(tmem, 256);
   }
+  if (threadIdx.x == 0) BND(a.seq, 1);
 }
 
 
@@ -1294,25 +1322,6 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
   return r;
 }
 
-// ---- distributed shared memory (thread-block clusters)
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
-  float4 v;
-  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
-  float2 v;
-  asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
-  return v;
-}
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 
 // p = 2^(s * scale - ref) for the NP rows of this thread's key (all chunks loaded from
 // TMEM with one wait); masked entries -> 0.  Returns the largest exponent (overflow
@@ -1995,6 +2004,7 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   a.req_state = req_state;
   a.rows_per_block = 128;
   a.pf = take_prefetch();
+  a.seq = bnd_next_seq();
   int& variant = g_attn_variant;
   if (variant < 0) {
     const char* e = getenv("BST_ATTN");
@@ -2273,4 +2283,14 @@ extern "C" int bst_attention_set_variant(int v) {
   BST_REQUIRE(v == -1 || (v >= 1 && v <= 4), "variant must be -1 or 1..4");
   bst::g_attn_variant = v;
   return BST_OK;
+}
+
+extern "C" int bst_debug_bnd_trace_attn(void* buf) {  // BST_TRACE builds only
+#ifdef BST_TRACE
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_bnd, &buf, sizeof(void*)));
+  return BST_OK;
+#else
+  (void)buf;
+  return BST_EINVAL;
+#endif
 }

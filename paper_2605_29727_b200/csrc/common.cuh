@@ -74,6 +74,39 @@ bst_prefetch_t take_prefetch();
 // with pdl_enter() (griddepcontrol.launch_dependents, then griddepcontrol.wait before
 // any global access), so its CTAs may become resident while the predecessor drains and
 // the next PDL kernel may be scheduled early.  BST_PDL=0 disables it (measurement).
+
+// Boundary tracing (BST_TRACE builds, scripts/boundary_trace.py): per launch sequence
+// number, [first CTA entry, first dependency release, last dependency release, last CTA
+// end] in globaltimer ns.  Each translation unit has its own buffer pointer.
+#ifdef BST_TRACE
+#define BST_BND_TRACE_DEF static __device__ unsigned long long* g_bnd = nullptr;
+__device__ __forceinline__ unsigned long long bnd_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define BND(seq, k)                                                                              \
+  do {                                                                                           \
+    if (g_bnd && (seq) > 0 && (seq) < 4096) {                                                   \
+      if ((k) & 1) atomicMax(g_bnd + (int64_t)(seq) * 8 + (k), bnd_now());                      \
+      else atomicMin(g_bnd + (int64_t)(seq) * 8 + (k), bnd_now());                               \
+    }                                                                                            \
+  } while (0)
+#define BND_KIND(seq, v)                                                                         \
+  do {                                                                                           \
+    if (g_bnd && (seq) > 0 && (seq) < 4096) g_bnd[(int64_t)(seq) * 8 + 4] = (v);                \
+  } while (0)
+#else
+#define BST_BND_TRACE_DEF
+#define BND(seq, k) \
+  do {              \
+  } while (0)
+#define BND_KIND(seq, v) \
+  do {                   \
+  } while (0)
+#endif
+int bnd_next_seq();
+void bnd_reset_seq();
 int pdl_enabled();
 __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

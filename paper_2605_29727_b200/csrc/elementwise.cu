@@ -96,12 +96,18 @@ __global__ void embed_rmsnorm_kernel(const int32_t* __restrict__ tokens, const _
 // One CTA (1024 threads) per row; each thread owns groups of 4 columns.
 // partial == nullptr: only normalise.  resid == nullptr: normalise Y itself.
 constexpr int R_THREADS = 1024;
+BST_BND_TRACE_DEF
+
 __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
     const float* __restrict__ partial, bst_gemm_sched_t s, float* resid, int h, const __nv_bfloat16* __restrict__ w,
     float eps, __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf, int rows, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) BND(s.reserved, 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0) BND_KIND(s.reserved, 2);
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   sm100::grid_dep_wait();  // PDL launch: the producer GEMM's partials are complete past this point
+  if (threadIdx.x == 0) BND(s.reserved, 2);
+  if (threadIdx.x == 0) BND(s.reserved, 3);
   __shared__ float sh[32];
   __shared__ float4 vals[2048];
   const int t = blockIdx.x;
@@ -134,14 +140,22 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
       xp[1] = __floats2bfloat162_rn(v.z * inv * w23.x, v.w * inv * w23.y);
     }
   }
+#ifdef BST_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) BND(s.reserved, 1);
+#endif
 }
 
 // ------------------------------------------------------------- q/k/v + rope
 // One CTA per (token row, group of 16 heads); one warp per head (d = 128, 4 values per lane).
 __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, RopeArgs ra, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) BND(s.reserved, 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) BND_KIND(s.reserved, 3);
   if (threadIdx.x == 0 && blockIdx.y == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
   sm100::grid_dep_wait();
+  if (threadIdx.x == 0) BND(s.reserved, 2);
+  if (threadIdx.x == 0) BND(s.reserved, 3);
   const int t = blockIdx.x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
@@ -151,6 +165,10 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
     float v[4] = {y4.x, y4.y, y4.z, y4.w};
     rope_store_head(ra, t, hd, v, lane);
   }
+#ifdef BST_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) BND(s.reserved, 1);
+#endif
 }
 
 // ---------------------------------------------------------------- swiglu
@@ -159,7 +177,11 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
   const int t = blockIdx.y;
   sm100::grid_dep_launch();
+  if (threadIdx.x == 0) BND(s.reserved, 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) BND_KIND(s.reserved, 4);
   sm100::grid_dep_wait();
+  if (threadIdx.x == 0) BND(s.reserved, 2);
+  if (threadIdx.x == 0) BND(s.reserved, 3);
   for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (ffn >> 2); g += gridDim.x * blockDim.x) {
     const float4 gt = gemm_load4(partial, s, t, g * 4);
     const float4 up = gemm_load4(partial, s, t, ffn + g * 4);
@@ -168,6 +190,10 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
     ap[0] = __floats2bfloat162_rn(si(gt.x) * up.x, si(gt.y) * up.y);
     ap[1] = __floats2bfloat162_rn(si(gt.z) * up.z, si(gt.w) * up.w);
   }
+#ifdef BST_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) BND(s.reserved, 1);
+#endif
 }
 
 // ------------------------------------------------------------ gather rows
@@ -205,6 +231,7 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   BST_REQUIRE(!partial || sched, "partial without schedule");
   bst_gemm_sched_t s{};
   if (sched) s = *sched;
+  s.reserved = bnd_next_seq();
   BST_CUDA(launch_pdl(residual_rmsnorm_kernel, dim3(rows), dim3(R_THREADS), 0, as_stream(stream), partial, s, resid, h,
                       static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
                       static_cast<__nv_bfloat16*>(feat), ldf, rows, take_prefetch()));
@@ -256,8 +283,10 @@ extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* 
   const RopeArgs ra = make_rope_args(n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, q_tok_stride,
                                      kv, layer_off_elems, page_table, page_size, state, state_c_idx, req_rows,
                                      req_span, req_state, req_slots);
+  bst_gemm_sched_t s = *sched;
+  s.reserved = bnd_next_seq();
   BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows, (n_q + 2 * n_kv + 15) / 16), dim3(512), 0, as_stream(stream),
-                      partial, *sched, ra, take_prefetch()));
+                      partial, s, ra, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }
@@ -277,7 +306,9 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
   BST_REQUIRE(partial && sched && act, "null pointer argument");
   BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
   dim3 grid((ffn / 4 + 255) / 256, rows);
-  BST_CUDA(launch_pdl(swiglu_kernel, grid, dim3(256), 0, as_stream(stream), partial, *sched, ffn,
+  bst_gemm_sched_t s = *sched;
+  s.reserved = bnd_next_seq();
+  BST_CUDA(launch_pdl(swiglu_kernel, grid, dim3(256), 0, as_stream(stream), partial, s, ffn,
                       static_cast<__nv_bfloat16*>(act), lda, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
@@ -414,4 +445,14 @@ extern "C" int bst_commit_state(int32_t* state, const int32_t* accept_meta, cons
                                                         tree_meta, surrogate, log_i32, log_f64, log_cap));
   BST_LAUNCH_CHECK();
   return BST_OK;
+}
+
+extern "C" int bst_debug_bnd_trace_elem(void* buf) {  // BST_TRACE builds only
+#ifdef BST_TRACE
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_bnd, &buf, sizeof(void*)));
+  return BST_OK;
+#else
+  (void)buf;
+  return BST_EINVAL;
+#endif
 }

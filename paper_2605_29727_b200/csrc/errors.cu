@@ -42,3 +42,21 @@ int pdl_enabled() {
   return v;
 }
 }  // namespace bst
+
+namespace bst {
+// launch sequence numbers for boundary tracing (host side; 0 = untraced)
+static int g_bnd_seq = 0;
+int bnd_next_seq() {
+#ifdef BST_TRACE
+  return (++g_bnd_seq) % 4096;
+#else
+  return 0;
+#endif
+}
+void bnd_reset_seq() { g_bnd_seq = 0; }
+}  // namespace bst
+
+extern "C" int bst_debug_bnd_reset(void) {  // restart the boundary-trace launch numbering
+  bst::bnd_reset_seq();
+  return BST_OK;
+}

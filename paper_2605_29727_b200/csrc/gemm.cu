@@ -129,6 +129,8 @@ __device__ __forceinline__ void gtrace(int k) {
 #endif
 }
 
+BST_BND_TRACE_DEF
+
 struct Seg {
   int tile, kb_lo, kb_hi, slot;  // tile = super-tile index (first weight tile = tile * TP)
 };
@@ -156,6 +158,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) gtrace(0);
+  if (threadIdx.x == 0) BND(s.reserved, 0);
+  if (threadIdx.x == 0 && blockIdx.x == 0) BND_KIND(s.reserved, 1000000ull + s.n_out);
   if (trigger) sm100::grid_dep_launch();
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
@@ -219,6 +223,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
       gtrace(2);
       sm100::grid_dep_wait();
       gtrace(3);
+      BND(s.reserved, 2);
+      BND(s.reserved, 3);
       int idx = 0;
       while (next_seg(s, u, u1, seg)) {
         const int nt = ntiles(seg.tile);
@@ -314,6 +320,7 @@ __global__ void __launch_bounds__(G_THREADS, 1)
     sm100::tmem_dealloc(tmem, tcols);
   }
   if (threadIdx.x == 0) gtrace(7);
+  if (threadIdx.x == 0) BND(s.reserved, 1);
 }
 
 // ------------------------------------------------------ reduction kernels
@@ -510,7 +517,8 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
                         size_t partial_bytes, bst_stream_t stream) {
   using namespace bst;
   BST_REQUIRE(w && x && sched && partial, "null pointer argument");
-  const bst_gemm_sched_t s = *sched;
+  bst_gemm_sched_t s = *sched;
+  s.reserved = bnd_next_seq();
   BST_REQUIRE(partial_bytes >= (size_t)s.partial_floats * sizeof(float), "partial buffer too small");
   BST_REQUIRE(ld_x >= s.k, "ld_x < K");
   CUtensorMap tw, tx;
@@ -625,4 +633,14 @@ extern "C" int bst_debug_gemm_trace(void* buf, int cta) {
   BST_CUDA(cudaMemcpyToSymbol(bst::g_gemm_trace, &buf, sizeof(void*)));
   BST_CUDA(cudaMemcpyToSymbol(bst::g_trace_cta, &cta, sizeof(int)));
   return BST_OK;
+}
+
+extern "C" int bst_debug_bnd_trace_gemm(void* buf) {  // BST_TRACE builds only
+#ifdef BST_TRACE
+  BST_CUDA(cudaMemcpyToSymbol(bst::g_bnd, &buf, sizeof(void*)));
+  return BST_OK;
+#else
+  (void)buf;
+  return BST_EINVAL;
+#endif
 }
