@@ -170,7 +170,9 @@ typedef struct {
   int32_t tmem_cols, stages;
   int64_t partial_floats;       /* size of the partial buffer */
   int32_t pair;                 /* weight tiles per stream-K unit (1, or 2 for m > 128: X k-block shared) */
-  int32_t reserved;
+  int32_t reserved;             /* trace builds: launch sequence number */
+  int32_t cta2;                 /* 1: CTA-pair kernel (tcgen05 cta_group::2), grid = number of pairs */
+  int32_t pad_;
 } bst_gemm_sched_t;
 
 int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sched_t* out);

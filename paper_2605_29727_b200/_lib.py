@@ -47,7 +47,8 @@ class GemmSched(C.Structure):
     _fields_ = [("n_out", C.c_int32), ("k", C.c_int32), ("m", C.c_int32), ("bn", C.c_int32),
                 ("n_mt", C.c_int32), ("n_kb", C.c_int32), ("grid", C.c_int32), ("s_max", C.c_int32),
                 ("units", C.c_int64), ("tmem_cols", C.c_int32), ("stages", C.c_int32),
-                ("partial_floats", C.c_int64), ("pair", C.c_int32), ("reserved", C.c_int32)]
+                ("partial_floats", C.c_int64), ("pair", C.c_int32), ("reserved", C.c_int32),
+                ("cta2", C.c_int32), ("pad_", C.c_int32)]
 
 
 class Prefetch(C.Structure):

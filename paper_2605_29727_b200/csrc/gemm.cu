@@ -323,6 +323,167 @@ __global__ void __launch_bounds__(G_THREADS, 1)
   if (threadIdx.x == 0) BND(s.reserved, 1);
 }
 
+// CTA-pair variant (s.cta2, m > 128 on even tile counts): a cluster of two CTAs owns
+// a 256-row weight super-tile; tcgen05.mma.cta_group::2 (M = 256, N = bn) reads the
+// weights split along M (128 rows per CTA) and the X k-block split along N (bn / 2
+// token rows per CTA), so each SM ingests 16 KiB of weights + bn / 2 x 128 B of X per
+// k-block instead of the full X block: half the L2 -> SM traffic of the one-CTA kernel
+// at full tensor rate.  Stream-K runs over pairs (s.grid = number of pairs); each CTA
+// writes the partial of its own 128-row tile.  Only rank 0 issues MMAs; both CTAs load.
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
+    gemm_bf16_2cta_kernel(const __grid_constant__ CUtensorMap tmW, const __grid_constant__ CUtensorMap tmX,
+                          bst_gemm_sched_t s, float* __restrict__ partial, int stages, int trigger) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  __shared__ __align__(8) uint64_t full[G_MAX_STAGES], empty[G_MAX_STAGES], tfull[2], tempty[2];
+  __shared__ uint32_t tmem_base_sh;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (trigger) sm100::grid_dep_launch();
+  const uint32_t rank = sm100::cluster_ctarank();
+  const int pair = (int)blockIdx.x >> 1;
+  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
+  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
+  const int bn = s.bn, hn = bn >> 1;
+  const uint32_t xh_bytes = (uint32_t)hn * G_BK * 2;
+  const uint32_t stage_bytes = G_TILE_W + xh_bytes;
+  const uint32_t tcols = s.tmem_cols;
+  const int nacc = (int)tcols >= 2 * bn ? 2 : 1;
+
+  if (warp == 0 && lane == 0) {
+    sm100::prefetch_tmap(&tmW);
+    sm100::prefetch_tmap(&tmX);
+    for (int i = 0; i < stages; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { sm100::mbar_init(&tfull[i], 1); sm100::mbar_init(&tempty[i], 8); }
+    sm100::fence_mbar_init();
+  }
+  if (warp == 1) sm100::tmem_alloc2(&tmem_base_sh, tcols);
+  sm100::tc_fence_before();
+  sm100::cluster_sync();  // barriers of both CTAs initialised before any remote arrival
+  sm100::tc_fence_after();
+  const uint32_t tmem = tmem_base_sh;
+
+  const int64_t u0 = (int64_t)pair * s.units / s.grid;
+  const int64_t u1 = (int64_t)(pair + 1) * s.units / s.grid;
+  auto seg_next = [&](int64_t& u, Seg& seg) {
+    if (u >= u1) return false;
+    seg.tile = (int)(u / s.n_kb);
+    seg.kb_lo = (int)(u % s.n_kb);
+    const int64_t lim = (int64_t)seg.kb_lo + (u1 - u);
+    seg.kb_hi = (int)(lim < s.n_kb ? lim : s.n_kb);
+    seg.slot = pair - sched_first_st(s, seg.tile);
+    u += seg.kb_hi - seg.kb_lo;
+    return true;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs): own weight half + own X half
+    if (lane == 0) {
+      const uint64_t pol_w = sm100::policy_evict_first(), pol_x = sm100::policy_evict_last();
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t u = u0;
+      Seg seg;
+      int issued = 0;
+      {
+        int64_t uu = u0;
+        Seg sg;
+        int st = 0;
+        while (st < stages && seg_next(uu, sg)) {
+          for (int kb = sg.kb_lo; kb < sg.kb_hi && st < stages; ++kb, ++st) {
+            if (rank == 0) sm100::mbar_add_tx(&full[st], 2 * G_TILE_W);
+            sm100::tma_load_2d_2cta(smem + st * stage_bytes, &tmW, &full[st], kb * G_BK,
+                                    (sg.tile * 2 + (int)rank) * G_BM, pol_w);
+          }
+        }
+        issued = st;
+      }
+      sm100::grid_dep_wait();
+      int idx = 0;
+      while (seg_next(u, seg)) {
+        for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb, ++idx) {
+          uint8_t* sw = smem + stage * stage_bytes;
+          if (idx >= issued) {
+            sm100::mbar_wait(&empty[stage], phase ^ 1);
+            if (rank == 0) sm100::mbar_add_tx(&full[stage], 2 * G_TILE_W);
+            sm100::tma_load_2d_2cta(sw, &tmW, &full[stage], kb * G_BK, (seg.tile * 2 + (int)rank) * G_BM, pol_w);
+          }
+          if (rank == 0) sm100::mbar_expect_tx(&full[stage], 2 * xh_bytes);  // the leader's arrival
+          sm100::tma_load_2d_2cta(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, (int)rank * hn, pol_x);
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- UMMA issuer (leader only)
+    if (rank == 0) {
+      const uint32_t idesc = sm100::idesc_bf16(2 * G_BM, bn);
+      int stage = 0;
+      uint32_t phase = 0;
+      int64_t u = u0;
+      Seg seg;
+      int j = 0;
+      while (seg_next(u, seg)) {
+        const int acc = nacc == 2 ? (j & 1) : 0;
+        const int use = nacc == 2 ? (j >> 1) : j;
+        sm100::mbar_wait_cluster(&tempty[acc], (use & 1) ^ 1);
+        sm100::tc_fence_after();
+        const uint32_t d = tmem + acc * bn;
+        for (int kb = seg.kb_lo; kb < seg.kb_hi; ++kb) {
+          sm100::mbar_wait(&full[stage], phase);
+          sm100::tc_fence_after();
+          if (sm100::elect_one()) {
+            const uint32_t a_addr = base + stage * stage_bytes;
+            const uint64_t adesc = sm100::desc_k_sw128(a_addr);
+            const uint64_t bdesc = sm100::desc_k_sw128(a_addr + G_TILE_W);
+#pragma unroll
+            for (int k = 0; k < G_BK / 16; ++k)
+              sm100::umma_f16_2cta(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+            sm100::umma_commit_2cta(&empty[stage], 0x3);
+          }
+          __syncwarp();
+          if (++stage == stages) { stage = 0; phase ^= 1; }
+        }
+        if (sm100::elect_one()) sm100::umma_commit_2cta(&tfull[acc], 0x3);
+        __syncwarp();
+        ++j;
+      }
+    }
+  } else {
+    // ---------------- epilogue (both CTAs): TMEM -> fp32 partial slot of the own tile
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    int64_t u = u0;
+    Seg seg;
+    int j = 0;
+    while (seg_next(u, seg)) {
+      const int acc = nacc == 2 ? (j & 1) : 0;
+      const int use = nacc == 2 ? (j >> 1) : j;
+      sm100::mbar_wait(&tfull[acc], use & 1);
+      sm100::tc_fence_after();
+      const int tile = seg.tile * 2 + (int)rank;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + acc * bn;
+      float* dst = partial + ((int64_t)(tile * s.s_max + seg.slot) * bn) * G_BM + row;
+      for (int c0 = 0; c0 < bn; c0 += 16) {
+        float v[16];
+        sm100::tmem_ld16(taddr + c0, v);
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+          if (c0 + i < s.m) dst[(int64_t)(c0 + i) * G_BM] = v[i];
+      }
+      sm100::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) sm100::mbar_arrive_remote(&tempty[acc], 0);
+      ++j;
+    }
+  }
+  sm100::tc_fence_before();
+  sm100::cluster_sync();  // both CTAs done with TMEM and with remote barriers
+  if (warp == 1) {
+    sm100::tc_fence_after();
+    sm100::tmem_dealloc2(tmem, tcols);
+  }
+}
+
 // ------------------------------------------------------ reduction kernels
 __global__ void gemm_reduce_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, float* y_f32,
                                    __nv_bfloat16* y_bf16, int64_t ldy) {
@@ -486,6 +647,14 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   // pair mode loses TMEM double buffering at bn > 128 and doubles each CTA's partial
   // tile, so it only pays when every CTA streams at least one full tile (n_mt >= grid)
   s.pair = (pair_min_bn > 0 && s.bn >= pair_min_bn && s.n_mt >= grid) ? 2 : 1;
+  // CTA-pair mode (cta_group::2) for m > 128 on even tile counts (BST_GEMM_2CTA=0/1)
+  static int cta2_on = -1;
+  if (cta2_on < 0) cta2_on = getenv("BST_GEMM_2CTA") ? atoi(getenv("BST_GEMM_2CTA")) : 1;
+  s.cta2 = (cta2_on && s.bn >= 144 && s.n_mt % 2 == 0 && grid >= 2) ? 1 : 0;
+  if (s.cta2) {
+    s.pair = 2;
+    grid /= 2;  // stream-K over CTA pairs
+  }
   s.units = (int64_t)((s.n_mt + s.pair - 1) / s.pair) * s.n_kb;
   s.grid = (int)(s.units < grid ? s.units : grid);
   int smax = 1;
@@ -495,9 +664,9 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   }
   s.s_max = smax;
   int tc = 32;
-  while (tc < 2 * s.pair * s.bn && tc < 512) tc <<= 1;  // double buffered when it fits
+  while (tc < 2 * (s.cta2 ? 1 : s.pair) * s.bn && tc < 512) tc <<= 1;  // double buffered when it fits
   s.tmem_cols = tc;
-  const int stage_bytes = s.pair * G_TILE_W + s.bn * G_BK * 2;
+  const int stage_bytes = s.cta2 ? G_TILE_W + (s.bn / 2) * G_BK * 2 : s.pair * G_TILE_W + s.bn * G_BK * 2;
   static int budget = 0, budget_pair = 0;
   if (!budget) {
     const char* e = getenv("BST_GEMM_SMEM_KB");  // measurement knobs
@@ -505,6 +674,7 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
     e = getenv("BST_GEMM_PAIR_SMEM_KB");
     budget_pair = e ? atoi(e) * 1024 : G_SMEM_BUDGET_PAIR;
   }
+  // pair and CTA-pair modes (m > 128): deeper weight prefetch, no co-resident epilogue needed
   int stages = ((s.pair == 2 ? budget_pair : budget) - 1024) / stage_bytes;
   BST_REQUIRE(stages >= 2, "GEMM smem budget too small for two stages");
   s.stages = stages > G_MAX_STAGES ? G_MAX_STAGES : stages;
@@ -527,6 +697,33 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
   rc = make_tmap_bf16(&tx, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)s.bn, G_BK);
   if (rc) return rc;
   BST_REQUIRE(s.pair == 1 || s.pair == 2, "bad schedule (pair=%d)", s.pair);
+  if (s.cta2) {
+    CUtensorMap tw2, tx2;
+    int rc2 = cached_tmap(&tw2, w, (uint64_t)s.n_out, (uint64_t)s.k, (uint64_t)s.k, G_BM, G_BK);
+    if (rc2) return rc2;
+    rc2 = make_tmap_bf16(&tx2, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)(s.bn / 2), G_BK);
+    if (rc2) return rc2;
+    const int smem2 = s.stages * (G_TILE_W + (s.bn / 2) * G_BK * 2) + 1024;
+    static int configured2 = 0;
+    if (smem2 > configured2) {
+      BST_CUDA(cudaFuncSetAttribute(gemm_bf16_2cta_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem2));
+      configured2 = smem2;
+    }
+    cudaLaunchConfig_t cfg2{};
+    cfg2.gridDim = dim3(2 * s.grid);
+    cfg2.blockDim = dim3(G_THREADS);
+    cfg2.dynamicSmemBytes = smem2;
+    cfg2.stream = as_stream(stream);
+    cudaLaunchAttribute at2[1];
+    at2[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at2[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg2.attrs = at2;
+    cfg2.numAttrs = 1;
+    static int trig2 = -1;
+    if (trig2 < 0) trig2 = getenv("BST_GEMM_TRIGGER") ? atoi(getenv("BST_GEMM_TRIGGER")) : 1;
+    BST_CUDA(cudaLaunchKernelEx(&cfg2, gemm_bf16_2cta_kernel, tw2, tx2, s, partial, (int)s.stages, trig2));
+    return BST_OK;
+  }
   const int smem = s.stages * (s.pair * G_TILE_W + s.bn * G_BK * 2) + 1024;
   static int configured[3] = {0, 0, 0};
   auto kern = s.pair == 2 ? gemm_bf16_kernel<2> : gemm_bf16_kernel<1>;

@@ -91,10 +91,14 @@ def test_gemm_schedule_pair_mode_and_slot_cover():
     """Stream-K schedule (host side, explicit grid, no GPU): two weight tiles per unit
     above 128 token columns, and every CTA's unit range maps to a valid partial slot."""
     from paper_2605_29727_b200 import ops
-    for n_out, k, m, pair in [(24576, 4096, 256, 2), (300, 4096, 256, 1), (4096, 12288, 129, 1), (151936, 4096, 129, 2),
-                              (6144, 4096, 128, 1), (151936, 4096, 64, 1), (128, 4096, 256, 1)]:
+    # (n_out, k, m, pair, cta2): CTA pairs for m > 128 on even tile counts (stream-K over 74
+    # pairs), two-tile units on one CTA for odd wide outputs
+    for n_out, k, m, pair, cta2 in [(24576, 4096, 256, 2, 1), (300, 4096, 256, 1, 0), (4096, 12288, 129, 2, 1),
+                                    (151936, 4096, 129, 2, 0), (6144, 4096, 128, 1, 0), (151936, 4096, 64, 1, 0),
+                                    (128, 4096, 256, 1, 0)]:
         s = ops.gemm_schedule(n_out, k, m, 148)
-        assert s.pair == pair, (n_out, m, s.pair)
+        assert (s.pair, s.cta2) == (pair, cta2), (n_out, m, s.pair, s.cta2)
+        assert s.grid == (74 if cta2 else min(148, s.units))
         n_st = -(-s.n_mt // s.pair)
         assert s.units == n_st * s.n_kb
         assert s.partial_floats == s.n_mt * s.s_max * s.bn * 128
