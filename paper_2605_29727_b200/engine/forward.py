@@ -32,12 +32,14 @@ MODE_TREE, MODE_CAUSAL, MODE_FULL = 0, 1, 2
 _ABLATE = set(filter(None, os.environ.get("BST_ABLATE", "").split(",")))
 # L2 weight prefetch during DRAM-idle kernels: off by default (measured no gain: the small
 # GEMMs are bound by per-SM TMA issue + DRAM burst latency, not by DRAM bytes); BST_PREFETCH=1
-_PREFETCH = os.environ.get("BST_PREFETCH", "0") == "1"
+# (BST_PREFETCH=o,gate_up,down,qkv selects single sites for measurement)
+_PF_ENV = os.environ.get("BST_PREFETCH", "0")
+_PREFETCH = {"o", "gate_up", "down", "qkv"} if _PF_ENV == "1" else set(filter(None, _PF_ENV.split(","))) - {"0"}
 MB = 1 << 20
 
 
-def _pf(*ranges) -> None:
-    if _PREFETCH:
+def _pf(site: str, *ranges) -> None:
+    if site in _PREFETCH:
         ops.set_prefetch(*ranges)
 SKIP_SLOT = -(2**31)
 
@@ -127,7 +129,7 @@ class TargetModel:
                                   eps, self.inv_freq, self.pos, self.slot, None, self.q, kv.buf, li * kv.layer_stride,
                                   pt, PAGE, state, req)
             if "attn" not in _ABLATE:
-                _pf((lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB))
+                _pf("o", (lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB) if "gate_up" in _PREFETCH else None)
                 if batch is None:
                     ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, cfg.n_q,
                                   cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
@@ -139,11 +141,11 @@ class TargetModel:
                                         mask_words, self.attn_ws, n_splits=self.attn_splits)
             p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
             if "resid" not in _ABLATE:
-                _pf((lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
+                _pf("gate_up", (lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
                 ops.residual_rmsnorm(p, resid, n, cfg.h, lw.post_norm, eps, x=x)
             p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
             if "swiglu" not in _ABLATE:
-                _pf((lw.down, 16 * MB))
+                _pf("down", (lw.down, 16 * MB))
                 ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
             p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
             nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
@@ -152,7 +154,7 @@ class TargetModel:
                 j = self.feat_layers.index(li)
                 feat = self.feat[:n, j * cfg.h:(j + 1) * cfg.h]
             if "resid" not in _ABLATE:
-                _pf((nxt_l.qkv, 64 * MB) if nxt_l is not None else (w.lm_head, 48 * MB))
+                _pf("qkv", (nxt_l.qkv, nxt_l.qkv.numel() * 2) if nxt_l is not None else (w.lm_head, 48 * MB))
                 ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
         if head == "argmax":
             p = ops.gemm_partial(x, w.lm_head, out=self.partial)

@@ -200,9 +200,10 @@ def commit_state(state, accept_meta, committed, max_path, out_tokens, tree_meta=
 def set_prefetch(*ranges) -> None:
     """L2 prefetch hint for the next K3/K5 launch: up to two (tensor, max_bytes) ranges."""
     pf = _lib.Prefetch()
-    for i, (t, nbytes) in enumerate(ranges[:2]):
-        if t is None:
+    for i, r in enumerate(ranges[:2]):
+        if r is None or r[0] is None:
             continue
+        t, nbytes = r
         n = min(int(nbytes), t.numel() * t.element_size()) & ~15
         pf.ptr[i] = t.data_ptr()
         pf.bytes[i] = n
