@@ -822,35 +822,34 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       float mx8[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) mx8[k] = -INFINITY;
+      // max over the raw scores (scale > 0 commutes with max); the scale is folded into
+      // the exponent's FMA below (as in tc2)
       if (__all_sync(0xffffffffu, vis == ~0ull)) {  // prefix tile: no masking
 #pragma unroll
-        for (int k = 0; k < 64; ++k) {
-          sv[k] *= scale;
-          mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
-        }
+        for (int k = 0; k < 64; ++k) mx8[k & 7] = fmaxf(mx8[k & 7], sv[k]);
       } else {
 #pragma unroll
         for (int k = 0; k < 64; ++k) {
-          const float v = ((vis >> k) & 1ull) ? sv[k] * scale : -INFINITY;
+          const float v = ((vis >> k) & 1ull) ? sv[k] : -INFINITY;
           sv[k] = v;
           mx8[k & 7] = fmaxf(mx8[k & 7], v);
         }
       }
-      const float mt = fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
-                             fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
+      const float mt = scale * fmaxf(fmaxf(fmaxf(mx8[0], mx8[1]), fmaxf(mx8[2], mx8[3])),
+                                     fmaxf(fmaxf(mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7])));
       const float m_new = fmaxf(m_run, mt);
       const bool rescale = (m_run == -INFINITY) ? (m_new != -INFINITY) : (m_new > m_run + T_RESCALE);
       const float m_ref = rescale ? m_new : m_run;
       const float alpha = (rescale && m_run != -INFINITY) ? ex2(m_run - m_ref) : (rescale ? 0.f : 1.f);
-      const float msub = m_ref == -INFINITY ? 0.f : m_ref;  // all-masked row: ex2(-inf) = 0
+      const float nsub = m_ref == -INFINITY ? 0.f : -m_ref;  // all-masked row: ex2(-inf) = 0
       float rs8[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) rs8[k] = 0.f;
       uint32_t pk[32];
 #pragma unroll
       for (int k = 0; k < 64; k += 2) {
-        const float p0 = ex2(sv[k] - msub);
-        const float p1 = ex2(sv[k + 1] - msub);
+        const float p0 = ex2(fmaf(sv[k], scale, nsub));
+        const float p1 = ex2(fmaf(sv[k + 1], scale, nsub));
         rs8[(k >> 1) & 7] += p0 + p1;
         pk[k >> 1] = pack_bf16(p0, p1);
       }
