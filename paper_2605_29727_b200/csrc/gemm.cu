@@ -343,8 +343,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
   const int pair = (int)blockIdx.x >> 1;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-  const int bn = s.bn, hn = bn >> 1;
-  const uint32_t xh_bytes = (uint32_t)hn * G_BK * 2;
+  // bn > 256: two N chunks of bn / 2 token columns; each CTA loads the rank's half of each
+  const int bn = s.bn, nch = bn > 256 ? 2 : 1, cn = bn / nch, hn = cn >> 1;
+  const uint32_t xh_bytes = (uint32_t)(nch * hn) * G_BK * 2;
   const uint32_t stage_bytes = G_TILE_W + xh_bytes;
   const uint32_t tcols = s.tmem_cols;
   const int nacc = (int)tcols >= 2 * bn ? 2 : 1;
@@ -408,7 +409,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
             sm100::tma_load_2d_2cta(sw, &tmW, &full[stage], kb * G_BK, (seg.tile * 2 + (int)rank) * G_BM, pol_w);
           }
           if (rank == 0) sm100::mbar_expect_tx(&full[stage], 2 * xh_bytes);  // the leader's arrival
-          sm100::tma_load_2d_2cta(sw + G_TILE_W, &tmX, &full[stage], kb * G_BK, (int)rank * hn, pol_x);
+          for (int c = 0; c < nch; ++c)
+            sm100::tma_load_2d_2cta(sw + G_TILE_W + c * hn * 128, &tmX, &full[stage], kb * G_BK, c * cn + (int)rank * hn,
+                                    pol_x);
           if (++stage == stages) { stage = 0; phase ^= 1; }
         }
       }
@@ -416,7 +419,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
   } else if (warp == 1) {
     // ---------------- UMMA issuer (leader only)
     if (rank == 0) {
-      const uint32_t idesc = sm100::idesc_bf16(2 * G_BM, bn);
+      const uint32_t idesc = sm100::idesc_bf16(2 * G_BM, cn);
       int stage = 0;
       uint32_t phase = 0;
       int64_t u = u0;
@@ -434,10 +437,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G_THREADS, 1)
           if (sm100::elect_one()) {
             const uint32_t a_addr = base + stage * stage_bytes;
             const uint64_t adesc = sm100::desc_k_sw128(a_addr);
-            const uint64_t bdesc = sm100::desc_k_sw128(a_addr + G_TILE_W);
+            for (int c = 0; c < nch; ++c) {
+              const uint64_t bdesc = sm100::desc_k_sw128(a_addr + G_TILE_W + c * hn * 128);
 #pragma unroll
-            for (int k = 0; k < G_BK / 16; ++k)
-              sm100::umma_f16_2cta(d, adesc + 2 * k, bdesc + 2 * k, idesc, (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+              for (int k = 0; k < G_BK / 16; ++k)
+                sm100::umma_f16_2cta(d + c * cn, adesc + 2 * k, bdesc + 2 * k, idesc,
+                                     (kb > seg.kb_lo || k > 0) ? 1u : 0u);
+            }
             sm100::umma_commit_2cta(&empty[stage], 0x3);
           }
           __syncwarp();
@@ -622,13 +628,13 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   using namespace bst;
   BST_REQUIRE(out, "null schedule");
   BST_REQUIRE(n_out >= 1 && k >= 1, "bad GEMM shape n_out=%d k=%d", n_out, k);
-  BST_REQUIRE(m >= 1 && m <= 256, "m must be in [1, 256] (got %d); chunk larger batches", m);
+  BST_REQUIRE(m >= 1 && m <= 512, "m must be in [1, 512] (got %d); chunk larger batches", m);
   BST_REQUIRE(k % 8 == 0, "K must be a multiple of 8 (16-byte TMA rows), got %d", k);
   bst_gemm_sched_t s{};
   s.n_out = n_out;
   s.k = k;
   s.m = m;
-  s.bn = ((m + 15) / 16) * 16;
+  s.bn = m > 256 ? ((m + 31) / 32) * 32 : ((m + 15) / 16) * 16;  // > 256: two N chunks of bn / 2
   s.n_mt = (n_out + G_BM - 1) / G_BM;
   s.n_kb = (k + G_BK - 1) / G_BK;
   if (grid <= 0) {
@@ -655,6 +661,7 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
     s.pair = 2;
     grid /= 2;  // stream-K over CTA pairs
   }
+  BST_REQUIRE(m <= 256 || s.cta2, "m > 256 needs the CTA-pair kernel (even tile count, got n_out=%d m=%d)", n_out, m);
   s.units = (int64_t)((s.n_mt + s.pair - 1) / s.pair) * s.n_kb;
   s.grid = (int)(s.units < grid ? s.units : grid);
   int smax = 1;
@@ -665,6 +672,7 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   s.s_max = smax;
   int tc = 32;
   while (tc < 2 * (s.cta2 ? 1 : s.pair) * s.bn && tc < 512) tc <<= 1;  // double buffered when it fits
+  if (tc < s.bn) tc = 512;
   s.tmem_cols = tc;
   const int stage_bytes = s.cta2 ? G_TILE_W + (s.bn / 2) * G_BK * 2 : s.pair * G_TILE_W + s.bn * G_BK * 2;
   static int budget = 0, budget_pair = 0;
@@ -691,17 +699,13 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
   s.reserved = bnd_next_seq();
   BST_REQUIRE(partial_bytes >= (size_t)s.partial_floats * sizeof(float), "partial buffer too small");
   BST_REQUIRE(ld_x >= s.k, "ld_x < K");
-  CUtensorMap tw, tx;
-  int rc = cached_tmap(&tw, w, (uint64_t)s.n_out, (uint64_t)s.k, (uint64_t)s.k, G_BM, G_BK);
-  if (rc) return rc;
-  rc = make_tmap_bf16(&tx, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)s.bn, G_BK);
-  if (rc) return rc;
   BST_REQUIRE(s.pair == 1 || s.pair == 2, "bad schedule (pair=%d)", s.pair);
   if (s.cta2) {
     CUtensorMap tw2, tx2;
     int rc2 = cached_tmap(&tw2, w, (uint64_t)s.n_out, (uint64_t)s.k, (uint64_t)s.k, G_BM, G_BK);
     if (rc2) return rc2;
-    rc2 = make_tmap_bf16(&tx2, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)(s.bn / 2), G_BK);
+    rc2 = make_tmap_bf16(&tx2, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x,
+                         (uint32_t)(s.bn > 256 ? s.bn / 4 : s.bn / 2), G_BK);
     if (rc2) return rc2;
     const int smem2 = s.stages * (G_TILE_W + (s.bn / 2) * G_BK * 2) + 1024;
     static int configured2 = 0;
@@ -724,6 +728,11 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
     BST_CUDA(cudaLaunchKernelEx(&cfg2, gemm_bf16_2cta_kernel, tw2, tx2, s, partial, (int)s.stages, trig2));
     return BST_OK;
   }
+  CUtensorMap tw, tx;
+  int rc = cached_tmap(&tw, w, (uint64_t)s.n_out, (uint64_t)s.k, (uint64_t)s.k, G_BM, G_BK);
+  if (rc) return rc;
+  rc = make_tmap_bf16(&tx, x, (uint64_t)s.m, (uint64_t)s.k, (uint64_t)ld_x, (uint32_t)s.bn, G_BK);
+  if (rc) return rc;
   const int smem = s.stages * (s.pair * G_TILE_W + s.bn * G_BK * 2) + 1024;
   static int configured[3] = {0, 0, 0};
   auto kern = s.pair == 2 ? gemm_bf16_kernel<2> : gemm_bf16_kernel<1>;

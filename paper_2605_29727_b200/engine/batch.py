@@ -36,6 +36,9 @@ from ..lattice import topk_logits_into
 from ..verify_sim import accept_device
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
 from .decode import MAX_ROWS, ST_BONUS, ST_C, ST_COMMITTED, ST_CYCLE
+from .forward import _gemm_rows
+
+VERIFY_ROWS = 512  # rows per batched verify launch (K4 CTA-pair kernel takes up to 512)
 from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
 from .weights import DrafterWeights, TargetWeights
 
@@ -63,14 +66,19 @@ class BatchEngine:
             raise ValueError(f"fixed budget must be <= {MAX_ROWS - 1}")
         G1 = self.gamma + 1
         self.G1 = G1
-        self.chunk_v = max(1, MAX_ROWS // self.S)          # requests per verify chunk
+        # verify chunks of up to 512 rows when every layer GEMM takes them (CTA-pair kernel):
+        # the weights stream once per chunk, so wider chunks stream them fewer times
+        layer_shapes = [(cfg.qkv_out, cfg.h), (cfg.h, cfg.h_q), (2 * cfg.h_ffn, cfg.h), (cfg.h, cfg.h_ffn)]
+        vrows = VERIFY_ROWS if all(_gemm_rows(n_, k_, VERIFY_ROWS) == VERIFY_ROWS for n_, k_ in layer_shapes) \
+            else MAX_ROWS
+        self.chunk_v = max(1, vrows // self.S)             # requests per verify chunk
         self.chunk_d = max(1, MAX_ROWS // G1)              # requests per draft chunk (block rows <= 256)
         self.max_ctx = max_ctx
         self.req_pages = math.ceil((max_ctx + MAX_ROWS + PAGE) / PAGE)
         slots = n_req * self.req_pages * PAGE
         self.tw = TargetWeights.random(cfg, seed, dev)
         self.dw = DrafterWeights.random(cfg, self.dcfg, len(feat), seed, dev)
-        self.target = TargetModel(cfg, self.tw, slots, MAX_ROWS, feat, dev)
+        self.target = TargetModel(cfg, self.tw, slots, max(MAX_ROWS, self.chunk_v * self.S), feat, dev)
         self.drafter = DrafterModel(cfg, self.dcfg, self.dw, self.tw, slots, len(feat), dev, n_req_max=self.chunk_d)
         i32 = dict(dtype=torch.int32, device=dev)
         self.state = torch.zeros(n_req, 8, **i32)

@@ -75,7 +75,19 @@ def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
 
 
 def _max_partial(shapes, max_rows: int) -> int:
-    return max(ops.gemm_schedule(n, k, max_rows).partial_floats for n, k in shapes)
+    return max(ops.gemm_schedule(n, k, _gemm_rows(n, k, max_rows)).partial_floats for n, k in shapes)
+
+
+def _gemm_rows(n: int, k: int, rows: int) -> int:
+    """Largest row count <= rows one K4 launch of this shape takes: up to 512 on the
+    CTA-pair kernel (even tile counts), else 256."""
+    if rows <= 256:
+        return rows
+    try:
+        ops.gemm_schedule(n, k, rows)
+        return rows
+    except ValueError:
+        return 256
 
 
 class TargetModel:
@@ -156,16 +168,23 @@ class TargetModel:
             if "resid" not in _ABLATE:
                 _pf("qkv", (nxt_l.qkv, nxt_l.qkv.numel() * 2) if nxt_l is not None else (w.lm_head, 48 * MB))
                 ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
-        if head == "argmax":
-            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
-            ops.gemm_argmax(p, out=self.argmax[:n], scratch=self.amx_scratch)
-        elif head == "sample":
-            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
-            ops.gemm_sample(p, self.pos, state, self.temperature, self.sample_seed, out=self.argmax[:n],
-                            scratch=self.amx_scratch)
-        elif head == "logits":
-            p = ops.gemm_partial(x, w.lm_head, out=self.partial)
-            self.logits = ops.gemm_reduce(p)
+        # LM head in row chunks the K4 schedule accepts (odd vocab tile counts: <= 256 rows)
+        hr = _gemm_rows(w.lm_head.shape[0], cfg.h, n)
+        logits = []
+        for r0 in range(0, n, hr):
+            r1 = min(n, r0 + hr)
+            if head == "argmax":
+                p = ops.gemm_partial(x[r0:r1], w.lm_head, out=self.partial)
+                ops.gemm_argmax(p, out=self.argmax[r0:r1], scratch=self.amx_scratch[r0:])
+            elif head == "sample":
+                p = ops.gemm_partial(x[r0:r1], w.lm_head, out=self.partial)
+                ops.gemm_sample(p, self.pos[r0:], state, self.temperature, self.sample_seed, out=self.argmax[r0:r1],
+                                scratch=self.amx_scratch[r0:])
+            elif head == "logits":
+                p = ops.gemm_partial(x[r0:r1], w.lm_head, out=self.partial)
+                logits.append(ops.gemm_reduce(p))
+        if head == "logits":
+            self.logits = logits[0] if len(logits) == 1 else torch.cat(logits)
 
 
 class DrafterModel:

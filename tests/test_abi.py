@@ -95,13 +95,13 @@ def test_gemm_schedule_pair_mode_and_slot_cover():
     # pairs), two-tile units on one CTA for odd wide outputs
     for n_out, k, m, pair, cta2 in [(24576, 4096, 256, 2, 1), (300, 4096, 256, 1, 0), (4096, 12288, 129, 2, 1),
                                     (151936, 4096, 129, 2, 0), (6144, 4096, 128, 1, 0), (151936, 4096, 64, 1, 0),
-                                    (128, 4096, 256, 1, 0)]:
+                                    (128, 4096, 256, 1, 0), (24576, 4096, 455, 2, 1)]:
         s = ops.gemm_schedule(n_out, k, m, 148)
         assert (s.pair, s.cta2) == (pair, cta2), (n_out, m, s.pair, s.cta2)
         assert s.grid == (74 if cta2 else min(148, s.units))
         n_st = -(-s.n_mt // s.pair)
         assert s.units == n_st * s.n_kb
-        assert s.partial_floats == s.n_mt * s.s_max * s.bn * 128
+        assert s.partial_floats == s.n_mt * s.s_max * s.bn * 128 and s.bn >= m
         assert s.tmem_cols <= 512 and s.stages >= 2
         # every CTA's first unit lies in a super-tile whose slot count covers it
         for c in range(s.grid):
@@ -109,3 +109,13 @@ def test_gemm_schedule_pair_mode_and_slot_cover():
             st = u0 // s.n_kb
             first = max(0, min(s.grid - 1, -(-((st * s.n_kb + 1) * s.grid) // s.units) - 1))
             assert 0 <= c - first < s.s_max
+
+
+def test_gemm_schedule_rejects_wide_m_without_cta_pairs():
+    """m > 256 rows run only on the CTA-pair kernel (two N chunks); odd tile counts raise."""
+    import pytest
+    from paper_2605_29727_b200 import ops
+    with pytest.raises(ValueError):
+        ops.gemm_schedule(151936, 4096, 300, 148)
+    with pytest.raises(ValueError):
+        ops.gemm_schedule(4096, 4096, 513, 148)

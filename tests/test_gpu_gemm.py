@@ -55,7 +55,7 @@ def test_gemm_argmax_lowest_index_ties():
 
 
 @pytest.mark.parametrize("n_out,k,m", [(24576, 4096, 256), (4096, 12288, 160), (1024, 4096, 136), (256, 200, 129),
-                                       (200, 4096, 250)])
+                                       (200, 4096, 250), (4096, 4096, 512), (24576, 4096, 455), (6144, 4096, 300)])
 def test_cta_pair_gemm_matches_single_cta_kernel(n_out, k, m):
     """The CTA-pair kernel (tcgen05 cta_group::2, schedule cta2) against the one-CTA
     kernel on the same operands: fp32 partials reduce to the same Y up to summation order,
