@@ -164,7 +164,8 @@ int bst_kv_compact(void* kv, int n_layers, int n_kv, int head_dim, int page_size
  * the fused epilogue kernels of the model forward).
  * ---------------------------------------------------------------------- */
 typedef struct {
-  int32_t n_out, k, m, bn;      /* bn = round_up(m, 16) token columns (<= 256) */
+  int32_t n_out, k, m, bn;      /* bn = round_up(m, 16) token columns (<= 256); m in 257..512 only on
+                                   the CTA-pair kernel (even tile counts): bn = round_up(m, 32) */
   int32_t n_mt, n_kb, grid, s_max;
   int64_t units;                /* ceil(n_mt / pair) * n_kb */
   int32_t tmem_cols, stages;
