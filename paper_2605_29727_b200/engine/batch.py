@@ -25,6 +25,7 @@ from __future__ import annotations
 
 import ctypes as C
 import math
+import os
 
 import numpy as np
 import torch
@@ -38,7 +39,8 @@ from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
 from .decode import MAX_ROWS, ST_BONUS, ST_C, ST_COMMITTED, ST_CYCLE
 from .forward import _gemm_rows
 
-VERIFY_ROWS = 512  # rows per batched verify launch (K4 CTA-pair kernel takes up to 512)
+# rows per batched verify launch (K4 CTA-pair kernel takes up to 512); BST_VERIFY_ROWS: measurement
+VERIFY_ROWS = min(512, int(os.environ.get("BST_VERIFY_ROWS", "512")))
 from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
 from .weights import DrafterWeights, TargetWeights
 
@@ -72,6 +74,12 @@ class BatchEngine:
         vrows = VERIFY_ROWS if all(_gemm_rows(n_, k_, VERIFY_ROWS) == VERIFY_ROWS for n_, k_ in layer_shapes) \
             else MAX_ROWS
         self.chunk_v = max(1, vrows // self.S)             # requests per verify chunk
+        # keep the chunk's batched attention grid (n_kv x row blocks x requests, one split)
+        # to one wave of CTAs when that costs at most ~15% more weight passes
+        n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+        wave = max(1, n_sm // (cfg.n_kv * math.ceil(cfg.n_q // cfg.n_kv * self.S / 128)))
+        if wave < self.chunk_v and math.ceil(n_req / wave) <= 1.15 * math.ceil(n_req / self.chunk_v):
+            self.chunk_v = wave
         self.chunk_d = max(1, MAX_ROWS // G1)              # requests per draft chunk (block rows <= 256)
         self.max_ctx = max_ctx
         self.req_pages = math.ceil((max_ctx + MAX_ROWS + PAGE) / PAGE)
