@@ -30,7 +30,7 @@ sys.path.insert(0, str(ROOT))
 
 METRIC = "decode tokens/s + tree-verify µs/step (Qwen3-8B shape, greedy); mean accept len"
 WORKLOAD = ("config2: Qwen3-8B-shape target + DFlash-style 5-layer block drafter, random-init bf16, batch 1 "
-            "per GPU, 2048-token context, gamma 16, top-K 8, adaptive budget (Algorithm 1, N_max 255)")
+            "per GPU, 2048-token context, gamma 16, top-K 8, adaptive budget (Algorithm 1, N_max 1024)")
 
 
 def load_peaks() -> dict:
@@ -89,83 +89,66 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------- CPU baseline
-def cpu_reference_cycles(n_cycles: int, seed: int = 0, context: int = 2048, vocab: int = 151936, gamma: int = 16,
-                         top_k: int = 8) -> dict:
-    """The reference planning path on this host (oracle port of specplan): per cycle
-    fp64 softmax + MarginalBlock validation + top_k_truncate + run_cycle (adaptive,
-    Qwen3-8B roofline at c) + linearize (c + t)^2 mask + verify_tree walk + commit."""
-    import numpy as np
-
-    from oracle import specplan_port as O
-    rng = np.random.default_rng(seed)
-    peaks = load_peaks()
-    dims = O.Dims(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=vocab, bp=2,
-                  peak_flops=peaks["bf16_tflops"] * 1e12, bandwidth=peaks["hbm_gbs"] * 1e9)
-    committed = 0
-    times = []
-    for i in range(n_cycles):
-        lg = (rng.standard_normal((gamma, vocab), dtype=np.float32) * 6.0)
-        lg = (lg.view(np.uint32) & 0xFFFF0000).view(np.float32)  # bf16-valued logits
-        c = context + committed
-        t0 = time.perf_counter()
-        probs = O.softmax_rows_f64(lg)
-        if np.any(probs < 0) or np.any(probs > 1) or np.any(np.abs(probs.sum(1) - 1) > 1e-9):  # lattice.py:47-53
-            raise ValueError("invalid block")
-        tok, prob = O.topk_rows(probs, top_k)
-        l_ar = O.roofline(dims, 1, c)
-        dec = O.controller(tok, prob, 255, O.curve_for(dims, c), 5e-4, 0.0, l_ar)
-        mask = O.linear_mask(dec.tree.parent, c)
-        am = rng.integers(0, vocab, dec.tree.size + 1)  # random-init target: the tree is rejected at the root
-        path, bonus = O.accept_from_argmax(dec.tree.parent, dec.tree.token, am)
-        toks = O.committed_tokens(path, dec.tree.token, bonus)
-        times.append(time.perf_counter() - t0)
-        committed += len(toks)
-        del mask
-    total = sum(times)
-    return {"tokens": committed, "seconds": total, "cycles": n_cycles, "median_cycle_s": statistics.median(times)}
+def cost_params_dict(peaks: dict) -> dict:
+    return dict(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=151936, bp=2,
+                peak_flops=peaks["bf16_tflops"] * 1e12, bandwidth=peaks["hbm_gbs"] * 1e9)
 
 
-def _reference_worker(job) -> dict:
+def _reference_stream(job) -> dict:
     """One independent decode stream of the reference planning path (one process, one thread)."""
-    seed, warmup, steps = job
+    seed, warmup, steps, params, latencies, context, n_max = job
     for var in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[var] = "1"
-    cpu_reference_cycles(warmup, seed=1000 + seed)
-    return cpu_reference_cycles(steps, seed=seed)
+    from oracle import ref_replay as R
+    if warmup:
+        R.reference_decode(R.synthetic_cycles(warmup, 1000 + seed, n_max=n_max), params, latencies, context, n_max,
+                           check=False)
+    return R.reference_decode(R.synthetic_cycles(steps, seed, n_max=n_max), params, latencies, context, n_max,
+                              check=False)
 
 
 def run_reference(args) -> None:
-    """The reference's CPU path on the same workload as our arm: N GPUs decode N independent
-    requests, so the reference decodes N independent streams, each in its own process (the
-    reference harness parallelises streams as processes, sp/harness.py:249-252).  One
-    stream is sequential Python/numpy, so one thread is all a stream can use; N streams use
-    min(N, host cores) processes."""
+    """The reference's own CPU implementation of the path (the unmodified specplan package
+    from baseline/_ref, else the oracle port) on the same workload as our arm: N GPUs decode
+    N independent requests, so the reference decodes N independent streams, one process per
+    stream (the reference harness parallelises runs as processes, sp/harness.py:249-252).
+    Each cycle replays config-2-shaped drafter rows (16 x 151936 fp64 from bf16 logits)
+    through specplan's decode_full: MarginalBlock validation, top_k_truncate, run_cycle
+    (adaptive, N_max 1024, Qwen3-8B roofline at the measured B200 peaks), linearize,
+    verify_tree, commit."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import multiprocessing as mp
+
+    from oracle import ref_replay as R
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     streams = max(1, world)
     cores = max(1, min(streams, os.cpu_count() or 1))
+    peaks = load_peaks()
+    params = cost_params_dict(peaks)
+    lat = dict(t_draft=8e-4, t_aux=0.0, l_ar=3.3e-3)  # our arm's measured draft / AR step (BENCH_r01)
+    jobs = [(i, args.warmup, args.steps, params, lat, args.context, 1024) for i in range(streams)]
     if streams == 1:
-        res = [_reference_worker((0, args.warmup, args.steps))]
+        res = [_reference_stream(jobs[0])]
     else:
         with mp.get_context("spawn").Pool(cores) as pool:
-            res = pool.map(_reference_worker, [(i, args.warmup, args.steps) for i in range(streams)])
+            res = pool.map(_reference_stream, jobs)
     tokens = sum(r["tokens"] for r in res)
     seconds = max(r["seconds"] for r in res)  # streams run concurrently: the slowest one bounds the job
     value = tokens / seconds
-    r = {"seconds": seconds}
-    sample = (f"{streams} stream(s) on {cores} process(es) x {args.steps} cycles of the reference planning path on config-2 shapes "
-              f"(gamma 16 x V 151936 bf16 drafter logits, c=2048, adaptive N_max 255): fp64 softmax+validation, "
-              f"top_k_truncate, run_cycle, linearize, verify_tree, commit; one process per stream, one thread each; "
-              f"model forward not included (the reference has none)")
+    info = R.host_info()
+    sample = (f"{streams} stream(s) on {cores} process(es) x {args.steps} cycles of the {res[0]['kind']} "
+              f"planning path (specplan decode_full over config-2-shaped drafter rows: 16 x 151936 fp64 from bf16 "
+              f"logits, c=2048, adaptive N_max 1024); one thread per stream; model forward not included (the "
+              f"reference has none); median {1e3 * statistics.median(r['median_cycle_s'] for r in res):.0f} ms/cycle")
     print(json.dumps({
         "metric": METRIC, "value": value, "unit": "tokens/s", "impl": "reference", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * r["seconds"] / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * seconds / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": WORKLOAD},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": res[0]["kind"], "sample": sample,
+                         **info},
         "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -201,8 +184,11 @@ def attention_roofline(peaks: dict, c: int, s: int, layers: int = 36) -> dict:
     g = torch.cuda.CUDAGraph()
     with torch.cuda.graph(g, stream=st):
         run()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
     ts = []
     for it in range(6):
+        with torch.cuda.stream(st):
+            flush.fill_(it)  # 256 MB > L2: every replay reads its KV from HBM
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
         with torch.cuda.stream(st):
@@ -214,12 +200,124 @@ def attention_roofline(peaks: dict, c: int, s: int, layers: int = 36) -> dict:
     t = statistics.median(ts)
     byts = 2 * (2 * (c + s) * n_kv * 128 + 2 * s * n_q * 128) + s * words * 4
     achieved = byts / t / 1e9
-    del kv, g
+    del kv, g, flush
     torch.cuda.empty_cache()
-    return {"bound": "hbm", "kernel": "attn_tc2_kernel (K3)", "context": c, "tree_rows": s, "layer_us": t * 1e6,
+    pages = (c + s + 63) // 64
+    kern = "attn_tc2_kernel (K3)" if pages // max(1, 148 // (n_kv * ((4 * s + 127) // 128))) >= 8 else "attn_tc_kernel (K3)"
+    return {"bound": "hbm", "kernel": kern, "context": c, "tree_rows": s, "layer_us": t * 1e6,
             "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
             "algorithmic_bytes_per_launch": byts, "traffic": "DRAM read = algorithmic (profiles/attn_tc2_ncu_summary.txt)",
-            "timing": "CUDA events around a graph of 36 launches over distinct layers (config-4 verify context)"}
+            "timing": "CUDA events around a graph of 36 launches over distinct layers, L2 flushed before each replay"}
+
+
+def step_bytes(p: dict, s: int, c: int) -> int:
+    """Fused-minimum bytes of one verify step: weights + KV + activations once,
+    no materialised score matrix; the embedding table counts as the s rows gathered."""
+    L, h, hq, hkv, hf, V, bp = p["L"], p["h"], p["n_q"] * p["d"], p["n_kv"] * p["d"], p["h_ffn"], p["V"], p["bp"]
+    weights = bp * (L * (2 * h * hq + 2 * h * hkv + 3 * h * hf) + V * h + s * h)
+    kv = bp * L * (2 * c * hkv + 2 * s * hkv)
+    act = bp * L * (4 * s * h + 4 * s * hq + 2 * s * hkv + 4 * s * hf) + bp * s * (h + V)
+    return weights + kv + act
+
+
+def step_flops(p: dict, s: int, c: int) -> int:
+    L, h, hq, hkv, hf, V = p["L"], p["h"], p["n_q"] * p["d"], p["n_kv"] * p["d"], p["h_ffn"], p["V"]
+    return L * (4 * s * h * hq + 4 * s * h * hkv + 4 * s * (c + s) * hq + 6 * s * h * hf) + 2 * s * h * V
+
+
+def draft_bytes(p: dict, layers: int, n_feat: int, c: int, gamma: int) -> int:
+    """One drafter block: its layers' weights, fc, the shared LM head, its context KV."""
+    h, hq, hkv, hf, V, bp = p["h"], p["n_q"] * p["d"], p["n_kv"] * p["d"], p["h_ffn"], p["V"], p["bp"]
+    per_layer = 2 * h * hq + 2 * h * hkv + 3 * h * hf
+    return bp * (layers * per_layer + n_feat * h * h + V * h + layers * 2 * (c + 2 * (gamma + 1)) * hkv)
+
+
+def gemm_replay_roofline(eng, cfg, peaks: dict, s_med: int) -> dict:
+    """K4: the step's 145 GEMMs (36 x qkv/o/gate_up/down + LM head) at m = s_med, replayed
+    back to back in a graph; achieved = algorithmic bytes (weights + X rows) / time."""
+    import torch
+
+    from paper_2605_29727_b200 import ops
+    t = eng.target
+    seq = []
+    for lw in eng.tw.layers:
+        for w in (lw.qkv, lw.o, lw.gate_up, lw.down):
+            seq.append((w, {cfg.h: t.x, cfg.h_q: t.attn, cfg.h_ffn: t.act}[w.shape[1]][:s_med]))
+    seq.append((eng.tw.lm_head, t.x[:min(s_med, 256)]))
+
+    def gemm_seq():
+        for w, xin in seq:
+            ops.gemm_partial(xin, w, out=t.partial)
+    with torch.cuda.stream(eng.stream):
+        gemm_seq()
+    eng.stream.synchronize()
+    gg = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(gg, stream=eng.stream):
+        gemm_seq()
+    reps = []
+    for _ in range(5):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(eng.stream)
+        with torch.cuda.stream(eng.stream):
+            gg.replay()
+        b.record(eng.stream)
+        b.synchronize()
+        reps.append(a.elapsed_time(b) * 1e-3)
+    g_time = statistics.median(reps[1:])
+    g_bytes = sum(w.numel() * 2 + x.shape[0] * w.shape[1] * 2 for w, x in seq)
+    achieved = g_bytes / g_time / 1e9
+    traffic = None
+    prof = ROOT / "profiles" / "gemm_dram_bytes.json"
+    if prof.exists():
+        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    del gg
+    return {"bound": "hbm", "kernel": "gemm_bf16_kernel (K4, tcgen05 weight streaming)", "achieved": achieved,
+            "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "peak_src": peaks["src"], "avg_launch_us": 1e6 * g_time / len(seq),
+            "algorithmic_bytes": f"bf16 weights + X rows per launch, 36x(qkv,o,gate_up,down)+lm_head at m={s_med}",
+            "timing": "CUDA events around a graph of the step's 145 GEMM launches (back to back, PDL)"}
+
+
+def run_config3(args, world: int, rank: int, local: int, cfg, peaks: dict) -> dict | None:
+    """BASELINE config 3 at N GPUs: 64 requests (prompt seeds 0..63) sharded contiguously,
+    each rank decodes its shard batched in one BatchEngine (fixed N = 64), no collective on
+    the data path; tokens/s = all committed tokens / max over ranks of the device time."""
+    import numpy as np
+    import torch
+
+    from paper_2605_29727_b200.dist import reduce_throughput, shard
+    from paper_2605_29727_b200.engine.batch import BatchEngine
+    from paper_2605_29727_b200.engine.config import DrafterConfig
+    mine = list(shard(args.c3_requests, world, rank))
+    prompts = [np.random.default_rng(r).integers(0, cfg.V - 1, args.context + 1).tolist() for r in mine]
+    cycles = args.c3_cycles
+    be = BatchEngine(cfg, DrafterConfig(layers=5, gamma=16, logit_scale=args.logit_scale), n_req=len(mine),
+                     n_fixed=args.c3_budget, max_ctx=args.context + 17 * (cycles + 8) + 64, seed=0)
+    be.reset(prompts)
+    for _ in range(3):
+        be.cycle()
+    base = be.committed_counts().copy()
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(be.stream)
+    for _ in range(cycles):
+        be.cycle()
+    e1.record(be.stream)
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3
+    tokens = float((be.committed_counts() - base).sum())
+    t_max, tok_all, value = reduce_throughput(t, tokens)
+    out = {"workload": f"config3: {args.c3_requests} requests (Qwen3-8B shape, 2048-token prompts) sharded "
+                       f"data-parallel over {world} GPU(s), batched per GPU, fixed N={args.c3_budget}",
+           "value": value, "unit": "tokens/s", "n_gpus": world, "requests_per_gpu": len(mine),
+           "cycles": cycles, "ms_per_cycle": 1e3 * t_max / cycles, "scaling": "strong (64 requests in total)",
+           "graph_kernels_per_cycle": be.graph_kernels, "mean_accept_len": tok_all / (cycles * args.c3_requests)}
+    del be
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours(args) -> None:
@@ -227,7 +325,8 @@ def run_ours(args) -> None:
     import torch
 
     import paper_2605_29727_b200 as P
-    from paper_2605_29727_b200 import _lib, ops
+    from paper_2605_29727_b200 import _lib
+    from paper_2605_29727_b200.dist import reduce_throughput
     from paper_2605_29727_b200.engine.config import MODELS, DrafterConfig
     from paper_2605_29727_b200.engine.decode import ST_COMMITTED, B200Engine
 
@@ -241,15 +340,16 @@ def run_ours(args) -> None:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = load_peaks()
     cfg = MODELS[args.model]
-    steps_total = args.warmup + args.steps + args.e2e_cycles + 64
-    eng = B200Engine(cfg, DrafterConfig(layers=5, gamma=16, logit_scale=args.logit_scale),
-                     max_ctx=args.context + 17 * steps_total + 256, seed=rank, n_cap=255, top_k=8)
+    pdict = cost_params_dict(peaks)
+    steps_total = args.warmup + args.steps + args.e2e_cycles + args.cpu_cycles + 64
+    dcfg = DrafterConfig(layers=5, gamma=16, logit_scale=args.logit_scale)
+    eng = B200Engine(cfg, dcfg, max_ctx=args.context + 17 * steps_total + 256, seed=rank, n_cap=1024, top_k=8)
     prompt = np.random.default_rng(1000 + rank).integers(0, cfg.V - 1, args.context + 1).tolist()
     eng.reset(prompt)
     params = cfg.cost_params(peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9)
 
     if args.profile:  # short run for ncu launch lists: fixed budget, graphs, no calibration/e2e/cpu legs
-        eng.set_policy("fixed", n=31)
+        eng.set_policy("fixed", n=args.profile_n)
         for _ in range(args.warmup):
             eng.cycle()
         torch.cuda.synchronize()
@@ -262,7 +362,7 @@ def run_ours(args) -> None:
     # ---- K7: measure l_ar / t_draft, static calibration of the verify roofline
     l_ar = eng.measure_ar_step()
     calib = []
-    for n in (15, 47, 95, 159, 255):
+    for n in (15, 47, 95, 159, 255, 511):
         eng.reset(prompt)
         eng.set_policy("fixed", n=n)
         obs = []
@@ -280,12 +380,15 @@ def run_ours(args) -> None:
     est = P.VerifyLatencyEstimator(params, variant="static", fit=fit)
     lat = P.CycleLatencies(t_draft=t_draft, t_aux=0.0, l_ar=l_ar)
 
+    def set_policy():
+        if args.policy == "adaptive":
+            eng.set_policy("adaptive", estimator=est, latencies=lat, n_max=1024)
+        else:
+            eng.set_policy("fixed", n=int(args.policy.split("-")[1]))
+
     # ---- device-timed decode (inputs resident, graphs)
     eng.reset(prompt)
-    if args.policy == "adaptive":
-        eng.set_policy("adaptive", estimator=est, latencies=lat, n_max=255)
-    else:
-        eng.set_policy("fixed", n=int(args.policy.split("-")[1]))
+    set_policy()
     for _ in range(args.warmup):
         eng.cycle()
     eng.stream.synchronize()
@@ -296,8 +399,7 @@ def run_ours(args) -> None:
         dist.barrier()
     torch.cuda.synchronize()
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    per = []
-    buckets = []
+    per, buckets = [], []
     with ClockSampler(local) as clk:
         start.record(eng.stream)
         for _ in range(args.steps):
@@ -315,120 +417,132 @@ def run_ours(args) -> None:
     stats = eng.read_log()[cyc0:cyc0 + args.steps]
     t_ver = [e[1].elapsed_time(e[2]) * 1e-3 for e in per]  # seconds
     t_dr = [e[0].elapsed_time(e[1]) * 1e-3 for e in per]
-    from paper_2605_29727_b200.dist import reduce_throughput
     elapsed, tokens_all, _ = reduce_throughput(elapsed, float(tokens))
     value = tokens_all / elapsed
-    # exact kernel count: nodes of the graphs replayed in the timed region
     kd = eng.graph_kernels[id(eng.graph_d)]
     kv = {b: eng.graph_kernels[id(g)] for b, g in eng.graphs_v.items()}
-    gpu_launches = sum(kd + kv[b] for b in buckets)
+    gpu_launches = sum(kd + kv[b] for b in buckets)  # exact: nodes of the graphs replayed in the timed region
 
-    # ---- e2e: the public API (façade decode -> engine fast path, EMA estimator re-planned every cycle)
-    eng.reset(prompt)
-    est_ema = P.VerifyLatencyEstimator(params, variant="ema_calib", fit=fit, bias=P.EmaBias())
-    sim = P.SimConfig(controller=P.ControllerConfig(n_max=255, latencies=lat, variant="ema_calib",
+    # ---- step-level and decode-level rooflines of the timed cycles
+    bw, pk = peaks["hbm_gbs"] * 1e9, peaks["bf16_tflops"] * 1e12
+    v_roof = [max(step_bytes(pdict, st.tree_size + 1, st.context) / bw,
+                  step_flops(pdict, st.tree_size + 1, st.context) / pk) for st in stats]
+    d_roof = [draft_bytes(pdict, dcfg.layers, len(eng.target.feat_layers), st.context, 16) / bw for st in stats]
+    v_bytes = [step_bytes(pdict, st.tree_size + 1, st.context) for st in stats]
+    accepted = sum(st.accepted_len for st in stats)
+    decode_roof = accepted / (sum(v_roof) + sum(d_roof))
+    step_roof = {"bound": "hbm", "what": "whole verify step (target forward over the tree + LM-head argmax + "
+                 "accept + KV compaction), CUDA events on the engine stream per timed cycle",
+                 "algorithmic_bytes_per_step_mean": statistics.mean(v_bytes),
+                 "achieved": statistics.mean(b / t for b, t in zip(v_bytes, t_ver)) / 1e9,
+                 "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                 "frac": statistics.mean(r / t for r, t in zip(v_roof, t_ver)),
+                 "verify_roof_us_mean": 1e6 * statistics.mean(v_roof), "verify_us_mean": 1e6 * statistics.mean(t_ver),
+                 "draft_roof_us_mean": 1e6 * statistics.mean(d_roof), "draft_us_mean": 1e6 * statistics.mean(t_dr),
+                 "bytes_formula": "SURVEY §8d fused minimum: weights (embedding as gathered rows) + KV(c+s) + "
+                                  "activations, no score matrix; time roof = max(bytes/BW, flops/peak)"}
+
+    # ---- cycles exported for the CPU reference replay (same inputs as the GPU)
+    exported = []
+    if rank == 0 and world == 1 and not args.no_cpu:
+        eng.reset(prompt)
+        set_policy()
+        eng.export = True
+        for _ in range(args.cpu_cycles):
+            eng.cycle()
+        eng.export = False
+        exported = [dict(probs=e["probs"], parent=e["parent"], token=e["token"], argmax=e["argmax"],
+                         path=e["path"].tolist(), bonus=e["bonus"]) for e in eng.exported]
+        eng.exported = []
+
+    # ---- e2e: the public API, same estimator as the timed region; prompt upload + prefill inside
+    sim = P.SimConfig(controller=P.ControllerConfig(n_max=1024, latencies=lat, variant="static",
                                                     context_len=args.context), run_length=args.e2e_cycles,
                       top_k=8)
     torch.cuda.synchronize()
-    e_start, e_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e_start.record(eng.stream)
     t0 = time.perf_counter()
-    records, toks_e2e = P.decode_full(eng, sim, P.Policy.adaptive(), est_ema)
-    e_end.record(eng.stream)
-    e_end.synchronize()
-    e2e_time = max(e_start.elapsed_time(e_end) * 1e-3, time.perf_counter() - t0)
+    eng.reset(prompt)  # H2D of the prompt from host memory + causal prefill
+    records, toks_e2e = P.decode_full(eng, sim, P.Policy.adaptive() if args.policy == "adaptive"
+                                      else P.Policy.fixed(int(args.policy.split("-")[1])), est)
+    torch.cuda.synchronize()
+    e2e_time = time.perf_counter() - t0
     e2e_tokens = sum(r.accepted_len for r in records)
     e2e_val = reduce_throughput(e2e_time, float(e2e_tokens))[2]
-    aal_e2e = e2e_tokens / max(1, len(records))
 
-    # ---- roofline of the dominant kernel (K4 GEMM) at the timed region's median verify size
+    # ---- dominant kernel (K4) and K3 probes
     s_med = int(statistics.median(buckets))
-    t = eng.target
-    x = t.x[:s_med]
-    shapes = []
-    for lw in eng.tw.layers:
-        shapes += [lw.qkv, lw.o, lw.gate_up, lw.down]
-    shapes.append(eng.tw.lm_head)
-    seq = []
-    for w in shapes:
-        k = w.shape[1]
-        seq.append((w, {cfg.h: t.x, cfg.h_q: t.attn, cfg.h_ffn: t.act}[k][:s_med]))
-
-    def gemm_seq():
-        for w, xin in seq:
-            ops.gemm_partial(xin, w, out=t.partial)
-    with torch.cuda.stream(eng.stream):
-        gemm_seq()  # warm-up (tensor maps, attributes)
-    eng.stream.synchronize()
-    gg = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(gg, stream=eng.stream):
-        gemm_seq()
-    reps = []
-    for _ in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(eng.stream)
-        with torch.cuda.stream(eng.stream):
-            gg.replay()
-        b.record(eng.stream)
-        b.synchronize()
-        reps.append(a.elapsed_time(b) * 1e-3)
-    g_time = statistics.median(reps[1:])
-    g_bytes = sum(w.numel() * 2 + s_med * w.shape[1] * 2 for w, _ in seq)
-    achieved = g_bytes / g_time / 1e9
-    n_launch = len(seq)
-    traffic = None
-    prof = ROOT / "profiles" / "gemm_dram_bytes.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
-
-    # ---- K3 tree-verify attention in its verify-graph context (config 4 shape: c=32K, s=17):
-    # a graph of 36 back-to-back launches over 36 distinct layers (36 x 134 MB >> L2)
-    attn = None
+    gemm = gemm_replay_roofline(eng, cfg, peaks, s_med)
+    attn = attn2k = None
     if not args.no_attn:
+        attn2k = attention_roofline(peaks, args.context, s_med)
         attn = attention_roofline(peaks, 32768, 17)
 
-    # ---- CPU baseline (rank 0, N=1 only): bounded sample of the reference planning path
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        r = cpu_reference_cycles(args.cpu_cycles)
-        cpu = {"value": r["tokens"] / r["seconds"], "unit": "tokens/s", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_cycles} cycles of the specplan planning path (oracle port) at config-2 shapes; "
-                         f"fp64 softmax/validation, top_k_truncate, run_cycle, linearize, verify_tree, commit; "
-                         f"no model forward (the reference has none); median {r['median_cycle_s'] * 1e3:.0f} ms/cycle"}
+    # ---- CPU baseline (rank 0, N=1 only): the reference decode over the GPU's own cycles
+    cpu = cpu3 = None
+    if exported:
+        from oracle import ref_replay as R
+        latd = dict(t_draft=lat.t_draft, t_aux=lat.t_aux, l_ar=lat.l_ar)
+        r = R.reference_decode(exported, pdict, latd, args.context, 1024, policy=args.policy,
+                               fit=(fit.slope, fit.intercept), check=True)
+        cpu = {"value": r["tokens"] / r["seconds"], "unit": "tokens/s", "cores": 1, "kind": r["kind"],
+               "sample": f"{r['cycles']} decode cycles of this run's workload: the GPU's own fp64 drafter rows and "
+                         f"verify argmax per cycle replayed through {'specplan' if r['kind'] == 'reference' else 'the oracle port'}"
+                         f".decode_full (MarginalBlock validation, top_k_truncate, run_cycle, linearize, verify_tree, "
+                         f"commit); trees identical to the GPU's (checked); no model forward (the reference has "
+                         f"none); median {1e3 * r['median_cycle_s']:.0f} ms/cycle, 1 of {os.cpu_count()} host cores",
+               "trees_match_gpu": True, **R.host_info()}
+        del exported
+        if not args.no_cpu3:
+            c3 = R.process_pool_streams(args.c3_requests, 2, pdict, latd, args.context, 1024)
+            cpu3 = {"value": c3["tokens_per_s_wall"], "unit": "tokens/s", "cores": c3["workers"], "kind": c3["kind"],
+                    "sample": f"config 3: {c3['streams']} reference decode streams x {c3['cycles_per_stream']} cycles, "
+                              f"a process pool of {c3['workers']} workers (sp/harness.py:249-252), wall clock"}
+
+    c3 = None
+    if not args.no_config3:
+        del eng
+        torch.cuda.empty_cache()
+        c3 = run_config3(args, world, rank, local, cfg, peaks)
 
     if rank != 0:
+        if dist:
+            dist.destroy_process_group()
         return
-    n_exp = [s.tree_size for s in stats]
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (random-init bf16 weights, uniform random prompt tokens)",
         "config": {"workload": WORKLOAD, "context": args.context, "policy": args.policy, "gamma": 16, "top_k": 8,
-                   "drafter_logit_scale": args.logit_scale,
+                   "n_max": 1024, "drafter_logit_scale": args.logit_scale,
                    "l2": "inputs larger than L2: 16.4 GB of target weights + 1.9 GB drafter streamed per step"},
         "tree_verify_us_per_step": 1e6 * statistics.mean(t_ver), "draft_us_per_step": 1e6 * statistics.mean(t_dr),
         "mean_accept_len": statistics.mean(s.accepted_len for s in stats),
-        "mean_tree_size": statistics.mean(n_exp), "verify_rows_bucket_median": s_med,
+        "mean_tree_size": statistics.mean(s.tree_size for s in stats), "verify_rows_bucket_median": s_med,
         "l_ar_us": l_ar * 1e6, "ar_tokens_per_s_equiv": 1.0 / l_ar,
+        "decode_roofline": {"tokens_per_s": decode_roof, "frac": value / decode_roof,
+                            "what": "AAL / (T_draft_roof + T_verify_roof(N*, c)) over the timed cycles"},
         "calibration": {"slope": fit.slope, "intercept": fit.intercept, "rmse_before": fit.rmse_before,
                         "rmse_after": fit.rmse_after, "points": [[s, tv] for s, _, tv in calib]},
-        "roofline": {"bound": "hbm", "kernel": "gemm_bf16_kernel (K4, tcgen05 weight streaming)",
-                     "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"],
-                     "traffic": traffic, "peak_src": peaks["src"],
-                     "algorithmic_bytes": "bf16 weights + X rows per launch, 36x(qkv,o,gate_up,down)+lm_head "
-                                          f"at m={s_med}", "avg_launch_us": 1e6 * g_time / n_launch,
-                     "timing": "CUDA events around a graph of the step's 145 GEMM launches (back to back, PDL)"},
-        "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": 200,
-                "d2h_bytes_per_step": 64 + 40 + int(4 * aal_e2e), "api": "paper_2605_29727_b200.decode_full(engine, "
-                "SimConfig, Policy.adaptive(), VerifyLatencyEstimator(ema_calib))", "cycles": len(records)},
+        "roofline": {**gemm, "step": step_roof},
+        "e2e": {"value": e2e_val, "unit": "tokens/s", "h2d_bytes_per_step": 4 * len(prompt) // max(1, len(records)),
+                "d2h_bytes_per_step": 64 + 4 * int(round(e2e_tokens / max(1, len(records)))),
+                "api": "engine.reset(prompt) + paper_2605_29727_b200.decode_full(engine, SimConfig, policy, "
+                       "VerifyLatencyEstimator(static, fit)) — prompt upload and prefill inside the timed region",
+                "cycles": len(records), "mean_tree_size": statistics.mean(r.tree_size for r in records)},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
     }
+    if attn2k:
+        line["verify_attention_roofline_c2k"] = attn2k
     if attn:
         line["verify_attention_roofline"] = attn
     if cpu:
         line["cpu_baseline"] = cpu
+    if cpu3:
+        line["cpu_baseline_config3"] = cpu3
+    if c3:
+        line["config3"] = c3
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
@@ -444,9 +558,15 @@ def main() -> None:
     ap.add_argument("--context", type=int, default=2048)
     ap.add_argument("--policy", default="adaptive")
     ap.add_argument("--logit-scale", type=float, default=6.0)
-    ap.add_argument("--e2e-cycles", type=int, default=30)
-    ap.add_argument("--cpu-cycles", type=int, default=30)
+    ap.add_argument("--e2e-cycles", type=int, default=64)
+    ap.add_argument("--cpu-cycles", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu3", action="store_true", help="skip the config-3 process-pool CPU leg")
+    ap.add_argument("--no-config3", action="store_true", help="skip the config-3 (64 requests sharded) GPU leg")
+    ap.add_argument("--c3-requests", type=int, default=64)
+    ap.add_argument("--c3-budget", type=int, default=64)
+    ap.add_argument("--c3-cycles", type=int, default=8)
+    ap.add_argument("--profile-n", type=int, default=63)
     ap.add_argument("--no-attn", action="store_true", help="skip the K3 roofline probe (c=32K, s=17)")
     ap.add_argument("--profile", action="store_true", help="only the cycle loop (for ncu --profile-from-start off)")
     args = ap.parse_args()

@@ -233,12 +233,18 @@ int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t 
                         int c_idx, int mode, const uint32_t* anc, int mask_words, int n_splits, float* ws,
                         size_t ws_bytes, bst_stream_t stream);
 size_t bst_attention_workspace(int n_q, int s, int n_splits);
-/* K3 kernel family: 3 = row-major tcgen05 (tc1 / tc2, default), 4 = key-major tcgen05
- * (S^T = K Q^T, reference-max softmax, cluster or L2 split merge), 2 = tc1 only,
- * 1 = mma.sync; -1 = from the BST_ATTN environment variable.
- * Split partials alternate between two workspace banks with the layer index, so the
- * workspace holds 2 x n_splits x s x n_q x 130 floats after the counter head. */
-int bst_attention_set_variant(int variant);
+/* Split partials alternate between two workspace banks with the layer index, so the
+ * workspace holds 2 x n_splits x s x n_q x 130 floats after the counter head.
+ * bst_attention picks its kernel by shape only: the single-softmax-group row-major
+ * tcgen05 kernel for short per-CTA page runs, the two-group one from 8 pages on. */
+/* Key-major K3 (S^T = K Q^T: one key per TMEM lane, every query row in the columns;
+ * reference-max softmax; cluster/DSMEM or L2 split merge).  Same arguments and
+ * results as bst_attention; a separate kernel kept for the measurements of DESIGN §5. */
+int bst_attention_keymajor(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                           int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv,
+                           int s, int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
+                           const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
+                           bst_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * K5 — fused elementwise epilogues of the target/drafter forward.

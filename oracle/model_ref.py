@@ -38,9 +38,9 @@ def rope(x: torch.Tensor, pos: torch.Tensor, inv_freq: torch.Tensor) -> torch.Te
 class RefModel:
     """Holds fp32 CPU copies of the engine's bf16 weights."""
 
-    def __init__(self, cfg, tw, dw=None, feat_layers=(), inv_freq=None):
-        f = lambda t: t.detach().to("cpu", torch.float32)  # noqa: E731
-        self.cfg = cfg
+    def __init__(self, cfg, tw, dw=None, feat_layers=(), inv_freq=None, device="cpu"):
+        f = lambda t: t.detach().to(device, torch.float32)  # noqa: E731
+        self.cfg, self.device = cfg, torch.device(device)
         self.emb, self.final_norm, self.lm_head = f(tw.emb), f(tw.final_norm), f(tw.lm_head)
         self.layers = [{k: f(getattr(lw, k)) for k in lw.__dataclass_fields__} for lw in tw.layers]
         self.feat_layers = tuple(feat_layers)
@@ -81,8 +81,9 @@ class RefModel:
     def target(self, tokens, pos, mask):
         """Dense target forward: tokens/pos [T], mask [T, T] -> (logits fp32 [T, V], features [T, n_feat*h])."""
         cfg = self.cfg
-        tokens = torch.as_tensor(tokens, dtype=torch.long)
-        pos = torch.as_tensor(pos)
+        tokens = torch.as_tensor(tokens, dtype=torch.long, device=self.device)
+        pos = torch.as_tensor(pos, device=self.device)
+        mask = mask.to(self.device)
         resid = self.emb[tokens].clone()
         feats = []
         for li, lw in enumerate(self.layers):
@@ -105,17 +106,18 @@ class RefModel:
         non-causal.  Returns logits [gamma, V] of the mask positions.
         """
         cfg = self.cfg
-        x_ctx = bf(rmsnorm(ctx_feat @ self.fc.t(), self.hidden_norm, cfg.eps)) if c > 0 else None
-        toks = torch.tensor([bonus] + [mask_token] * gamma)
-        bpos = torch.arange(c, c + gamma + 1)
-        cpos = torch.arange(0, c)
+        x_ctx = bf(rmsnorm(ctx_feat.to(self.device) @ self.fc.t(), self.hidden_norm, cfg.eps)) if c > 0 else None
+        dev = self.device
+        toks = torch.tensor([bonus] + [mask_token] * gamma, device=dev)
+        bpos = torch.arange(c, c + gamma + 1, device=dev)
+        cpos = torch.arange(0, c, device=dev)
         resid = self.emb[toks].clone()
         B = gamma + 1
         for li, lw in enumerate(self.d_layers):
             x = bf(rmsnorm(resid, lw["in_norm"], cfg.eps))
             kv_x = torch.cat([x_ctx, x]) if x_ctx is not None else x
             kv_pos = torch.cat([cpos, bpos])
-            mask = torch.ones(B, kv_x.shape[0], dtype=torch.bool)
+            mask = torch.ones(B, kv_x.shape[0], dtype=torch.bool, device=dev)
             resid = resid + self._attn_block(lw, x, bpos, kv_x, kv_pos, mask, cfg)
             x = bf(rmsnorm(resid, lw["post_norm"], cfg.eps))
             resid = resid + self._mlp(lw, x)
@@ -135,3 +137,45 @@ def verify_mask(c: int, anc: torch.Tensor) -> torch.Tensor:
     m[c:, :c] = True
     m[c:, c:] = anc
     return m
+
+
+class RefPlugin:
+    """The reference plugin protocol (sp/verify_sim.py:125-126,158-169) over :class:`RefModel`:
+    fp64 drafter rows and greedy target tokens of the oracle model, for decoding config 1
+    end to end on the CPU with ``specplan_port.decode_loop``.
+
+    Alignment (SURVEY §8a′): with committed stream ``prefix``, the model sees
+    ``prompt + prefix``; its last token is the pending root, the drafter's context is
+    every earlier position.  ``near_ties`` collects the decisions whose fp32 margin is
+    below ``tol`` x the row's max |logit| (top-2 target logits; the K-th/(K+1)-th drafter
+    logits of a row): a GPU run may legitimately decide those differently (bf16 storage,
+    fp32 sums in another order), no other.  A drafter near-tie can only change that
+    cycle's tree; a target near-tie can change the committed stream.
+    """
+
+    def __init__(self, ref: RefModel, prompt, gamma: int, mask_token: int, top_k: int, tol: float = 2e-2):
+        self.ref, self.prompt = ref, [int(t) for t in prompt]
+        self.gamma, self.mask_token, self.top_k, self.tol = gamma, mask_token, top_k, tol
+        self.near_ties: list[tuple[str, int]] = []  # (kind, committed length)
+
+    def drafter_marginals(self, prefix):
+        full = self.prompt + [int(t) for t in prefix]
+        c = len(full) - 1
+        _, feat = self.ref.target(full[:-1], list(range(c)), causal_mask(c))
+        lg = self.ref.drafter(feat, c, full[-1], self.gamma, self.mask_token)
+        top = lg.topk(self.top_k + 1, dim=-1).values
+        scale = lg.abs().amax(-1)
+        if bool(((top[:, self.top_k - 1] - top[:, self.top_k]) < self.tol * scale).any()):
+            self.near_ties.append(("drafter", len(prefix)))
+        return torch.softmax(lg.double(), -1).cpu().numpy()
+
+    def next_token(self, seq, temperature: float = 0.0) -> int:
+        if temperature != 0.0:
+            raise ValueError("the oracle plugin decodes greedily")
+        full = self.prompt + [int(t) for t in seq]
+        n = len(full)
+        lg, _ = self.ref.target(full, list(range(n)), causal_mask(n))
+        top = lg[-1].topk(2).values
+        if float(top[0] - top[1]) < self.tol * float(lg[-1].abs().max()):
+            self.near_ties.append(("target", len(seq)))
+        return int(torch.argmax(lg[-1]))  # first max on ties, as np.argmax (sp/verify_sim.py:107-109)

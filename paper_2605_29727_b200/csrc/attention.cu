@@ -11,9 +11,9 @@
 // head and a contiguous run of pages (flash-decoding split); all GQA query
 // rows of that head (group x tokens) are processed against each tile, so
 // every K/V byte is read from HBM once.  Tiles arrive by TMA (two 64-column
-// boxes with 128-byte swizzle) into a 3-stage mbarrier ring; QK^T and PV run
-// on mma.sync bf16 (the bytes/flop ratio at s <= 64 is HBM bound); softmax is
-// the online exp2 form in fp32.  Splits are merged by attn_combine_kernel.
+// boxes with 128-byte swizzle) into an mbarrier ring; S = QK^T and O += PV run on
+// tcgen05 with TMEM accumulators; softmax is the online exp2 form in fp32.
+// Splits merge in-kernel (last-arriving CTA) or in attn_combine_kernel.
 #include <cuda_bf16.h>
 #include <stdlib.h>
 
@@ -73,31 +73,6 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-__device__ __forceinline__ void mma_bf16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-
-// Byte address of (row, 16B-chunk q in 0..15) inside a K/V tile written by TMA as
-// two [64 rows][128 B] boxes with the 128B swizzle (chunk ^= row % 8).
-__device__ __forceinline__ uint32_t tile_addr(uint32_t tile, int row, int q) {
-  const int half = q >> 3, cq = q & 7;
-  return tile + half * (A_PAGE * 128) + row * 128 + ((cq ^ (row & 7)) << 4);
-}
 
 // 64-bit visibility of keys slot0..slot0+63 for query row `tok`:
 // prefix (< c) always, tree/causal part per mode, nothing at or beyond n_keys.
@@ -405,225 +380,6 @@ __device__ __forceinline__ void split_pages(const AttnArgs& a, int n_keys, int s
   page0 = split * live / a.n_splits;
   n_tiles = (split + 1) * live / a.n_splits - page0;
 }
-
-__device__ __forceinline__ bool visible(const AttnArgs& a, int tok, int slot, const uint32_t* mrow) {
-  if (slot >= a.n_keys) return false;
-  if (a.mode == 2) return true;
-  if (slot < a.c) return true;
-  if (a.mode == 1) return slot <= a.c + tok;
-  const int j = slot - a.c;
-  return (mrow[j >> 5] >> (j & 31)) & 1u;
-}
-
-__global__ void __launch_bounds__(A_THREADS, 1)
-    attn_tree_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  __shared__ __align__(8) uint64_t full[A_STAGES], empty[A_STAGES];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
-  uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-
-  sm100::grid_dep_launch();
-  const int head = blockIdx.x;  // kv head
-  const int split = blockIdx.y;
-  const int c_ctx = a.state ? a.state[a.c_idx] : a.c;
-  const int n_keys = c_ctx + a.keys_after_c;
-  const int R = a.group * a.s;  // query rows of this kv head: r = t * group + g
-  const int page0 = split * a.pages_per_split;
-  const int n_pages_keys = (n_keys + A_PAGE - 1) / A_PAGE;
-  const int page1 = min(page0 + a.pages_per_split, n_pages_keys);
-  const int n_tiles = max(page1 - page0, 0);
-
-  if (threadIdx.x == 0) {
-    sm100::prefetch_tmap(&tmKV);
-    for (int i = 0; i < A_STAGES; ++i) { sm100::mbar_init(&full[i], 1); sm100::mbar_init(&empty[i], A_WARPS); }
-    sm100::fence_mbar_init();
-  }
-  __syncthreads();
-
-  // producer: thread 0 issues TMA for tile i into stage i % A_STAGES
-  auto issue = [&](int i) {
-    const int st = i % A_STAGES;
-    const int phys = a.page_table[page0 + i];
-    const int64_t rowK = ((((int64_t)a.layer * a.n_pages_total + phys) * 2 + 0) * a.n_kv + head) * A_PAGE;
-    const int64_t rowV = rowK + (int64_t)a.n_kv * A_PAGE;
-    uint8_t* dst = smem + st * A_STAGE_BYTES;
-    sm100::mbar_expect_tx(&full[st], A_STAGE_BYTES);
-    sm100::tma_load_2d(dst, &tmKV, &full[st], 0, (int)rowK);
-    sm100::tma_load_2d(dst + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowK);
-    sm100::tma_load_2d(dst + A_TILE_BYTES, &tmKV, &full[st], 0, (int)rowV);
-    sm100::tma_load_2d(dst + A_TILE_BYTES + A_PAGE * 128, &tmKV, &full[st], 64, (int)rowV);
-  };
-  if (threadIdx.x == 0)
-    for (int i = 0; i < min(n_tiles, A_STAGES); ++i) issue(i);
-
-  // this warp's 16 query rows
-  const int row0 = (blockIdx.z * A_WARPS + warp) * 16;
-  const bool active = row0 < R;
-  const int g = lane >> 2, cq = lane & 3;
-  int tok[2], qh[2];
-  bool rv[2];
-  const uint32_t* mrow[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int r = row0 + g + 8 * h;
-    rv[h] = r < R;
-    const int rr = rv[h] ? r : 0;
-    tok[h] = rr / a.group;
-    qh[h] = head * a.group + rr % a.group;
-    mrow[h] = a.mode == 0 ? a.anc + (int64_t)tok[h] * a.mask_words : nullptr;
-  }
-  // Q fragments: 8 k-steps of 16 dims
-  uint32_t qf[8][4];
-#pragma unroll
-  for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const __nv_bfloat16* qp = a.q + (int64_t)tok[h] * a.q_tok_stride + (int64_t)qh[h] * A_D + ks * 16 + 2 * cq;
-      qf[ks][h] = rv[h] ? *reinterpret_cast<const uint32_t*>(qp) : 0u;
-      qf[ks][h + 2] = rv[h] ? *reinterpret_cast<const uint32_t*>(qp + 8) : 0u;
-    }
-  }
-  float o[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-
-  for (int i = 0; i < n_tiles; ++i) {
-    const int st = i % A_STAGES;
-    sm100::mbar_wait(&full[st], (i / A_STAGES) & 1);
-    const uint32_t kt = base + st * A_STAGE_BYTES;
-    const uint32_t vt = kt + A_TILE_BYTES;
-    const int slot0 = (page0 + i) * A_PAGE;
-    if (active) {
-      // S = Q K^T : 16 rows x 64 keys (8 n-tiles of 8 keys)
-      float sacc[8][4];
-#pragma unroll
-      for (int n = 0; n < 8; ++n) sacc[n][0] = sacc[n][1] = sacc[n][2] = sacc[n][3] = 0.f;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-#pragma unroll
-        for (int n2 = 0; n2 < 4; ++n2) {  // two n-tiles per ldmatrix.x4
-          // matrices: (keys n2*16+0..7, chunk 2ks), (same keys, chunk 2ks+1), (keys +8.., 2ks), (+8.., 2ks+1)
-          const int mi = lane >> 3, rr = lane & 7;
-          const int key = n2 * 16 + (mi >> 1) * 8 + rr;
-          const int q = 2 * ks + (mi & 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4(tile_addr(kt, key, q), b0, b1, b2, b3);
-          mma_bf16(sacc[2 * n2], qf[ks], b0, b1);
-          mma_bf16(sacc[2 * n2 + 1], qf[ks], b2, b3);
-        }
-      }
-      // mask + online softmax (rows g and g+8 of this warp's block)
-      float mx[2] = {-INFINITY, -INFINITY};
-      const uint64_t vis0 = rv[0] ? row_vis64(a.mode, c_ctx, n_keys, tok[0], slot0, mrow[0], a.mask_words) : 0ull;
-      const uint64_t vis1 = rv[1] ? row_vis64(a.mode, c_ctx, n_keys, tok[1], slot0, mrow[1], a.mask_words) : 0ull;
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int h = e >> 1;
-          const int k = n * 8 + 2 * cq + (e & 1);
-          const float v = (((h ? vis1 : vis0) >> k) & 1ull) ? sacc[n][e] * a.scale_log2 : -INFINITY;
-          sacc[n][e] = v;
-          mx[h] = fmaxf(mx[h], v);
-        }
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 1));
-        mx[h] = fmaxf(mx[h], __shfl_xor_sync(0xffffffffu, mx[h], 2));
-      }
-      float alpha[2], mnew[2];
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        mnew[h] = fmaxf(m_run[h], mx[h]);
-        alpha[h] = (mnew[h] == -INFINITY) ? 1.f : exp2f(m_run[h] - mnew[h]);
-        m_run[h] = mnew[h];
-      }
-      float rs[2] = {0.f, 0.f};
-      uint32_t pf[4][4];  // P as A fragments: 4 k-steps of 16 keys
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        float p[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int h = e >> 1;
-          p[e] = (mnew[h] == -INFINITY) ? 0.f : exp2f(sacc[n][e] - mnew[h]);
-          rs[h] += p[e];
-        }
-        const int ks = n >> 1, hi = n & 1;
-        pf[ks][hi * 2 + 0] = pack_bf16(p[0], p[1]);
-        pf[ks][hi * 2 + 1] = pack_bf16(p[2], p[3]);
-      }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) l_run[h] = l_run[h] * alpha[h] + rs[h];
-#pragma unroll
-      for (int n = 0; n < 16; ++n) {
-        o[n][0] *= alpha[0];
-        o[n][1] *= alpha[0];
-        o[n][2] *= alpha[1];
-        o[n][3] *= alpha[1];
-      }
-      // O += P V : V tile [64 keys][128 d], B fragments via ldmatrix.trans
-#pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        // A regs order expected: a0=(g, k 0-7), a1=(g+8, k 0-7), a2=(g, k 8-15), a3=(g+8, k 8-15)
-        uint32_t af[4] = {pf[ks][0], pf[ks][1], pf[ks][2], pf[ks][3]};
-#pragma unroll
-        for (int dn = 0; dn < 8; ++dn) {  // 16 d-columns per ldmatrix.x4.trans -> two n-tiles
-          const int mi = lane >> 3, rr = lane & 7;
-          const int key = ks * 16 + (mi & 1) * 8 + rr;
-          const int q = dn * 2 + (mi >> 1);
-          uint32_t b0, b1, b2, b3;
-          ldsm_x4_t(tile_addr(vt, key, q), b0, b1, b2, b3);
-          mma_bf16(o[2 * dn], af, b0, b1);
-          mma_bf16(o[2 * dn + 1], af, b2, b3);
-        }
-      }
-    }
-    __syncwarp();
-    if (lane == 0) sm100::mbar_arrive(&empty[st]);
-    if (threadIdx.x == 0 && i + A_STAGES < n_tiles) {
-      sm100::mbar_wait(&empty[st], (i / A_STAGES) & 1);
-      issue(i + A_STAGES);
-    }
-    __syncwarp();
-  }
-  if (!active) return;
-  // row sums across the 4 lanes of a row
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    l_run[h] += __shfl_xor_sync(0xffffffffu, l_run[h], 1);
-    l_run[h] += __shfl_xor_sync(0xffffffffu, l_run[h], 2);
-  }
-  if (a.n_splits == 1) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (!rv[h]) continue;
-      const float inv = l_run[h] > 0.f ? 1.f / l_run[h] : 0.f;
-      __nv_bfloat16* op = a.out + (int64_t)tok[h] * a.o_tok_stride + (int64_t)qh[h] * A_D;
-#pragma unroll
-      for (int n = 0; n < 16; ++n)
-        *reinterpret_cast<uint32_t*>(op + n * 8 + 2 * cq) = pack_bf16(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
-    }
-  } else {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (!rv[h]) continue;
-      const int64_t row = (int64_t)split * a.s * a.n_q + (int64_t)tok[h] * a.n_q + qh[h];
-      float* op = a.ws_o + row * A_D;
-#pragma unroll
-      for (int n = 0; n < 16; ++n)
-        *reinterpret_cast<float2*>(op + n * 8 + 2 * cq) = make_float2(o[n][2 * h], o[n][2 * h + 1]);
-      if (cq == 0) {
-        a.ws_ml[row * 2 + 0] = m_run[h];
-        a.ws_ml[row * 2 + 1] = l_run[h];
-      }
-    }
-  }
-}
-
 
 // ---- distributed shared memory (thread-block clusters)
 __device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
@@ -951,6 +707,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 // MMA completes, a V stage when its PV MMA completes, so K runs further ahead of
 // the softmax than a joint K+V ring of the same size allows.
 constexpr int T2_KS = 5, T2_VS = 4;
+constexpr int T2_MIN_PAGES = 8;  // per-CTA page run from which the two-group kernel is used
 constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
 constexpr int T2_THREADS = 384;  // warps 0-1 K TMA / S issuer, 2-9 softmax groups, 10 V TMA, 11 PV issuer
 
@@ -1931,13 +1688,12 @@ static int kt_cluster_occupancy(int nch, int cs) {
   return n;
 }
 
-static int g_attn_variant = -1;  // -1: from BST_ATTN on first use; bst_attention_set_variant overrides
 
 static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
                           int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
                           int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
                           const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes, int n_req,
-                          int req_pages, int req_state, bst_stream_t stream) {
+                          int req_pages, int req_state, bool keymajor, bst_stream_t stream) {
   BST_REQUIRE(q && out && kv_cache && page_table, "null pointer argument");
   BST_REQUIRE(n_req >= 1 && (n_req == 1 || (req_pages >= 1 && (state == nullptr || req_state >= 1))),
               "batched attention needs per-request page and state strides");
@@ -1952,11 +1708,17 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   const int pages = (max_keys + A_PAGE - 1) / A_PAGE;
   BST_REQUIRE(pages <= n_pages_total, "context exceeds the page table");
   if (n_req > 1) BST_REQUIRE(req_pages >= pages, "request page slice (%d) smaller than the context (%d pages)", req_pages, pages);
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    BST_CUDA(cudaGetDevice(&dev));
+    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
   const int n_splits_arg = n_splits;
   if (n_splits <= 0) {
     // one wave of CTAs: per-tile work (GQA group x tokens rows against 64 keys)
     // dominates a CTA's fixed cost, so spread the pages over every SM
-    int want = 148 / (n_kv * row_blocks * n_req);
+    int want = n_sm / (n_kv * row_blocks * n_req);
     n_splits = want < 1 ? 1 : want;
   }
   if (n_splits > pages) n_splits = pages;
@@ -2004,32 +1766,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   a.rows_per_block = 128;
   a.pf = take_prefetch();
   a.seq = bnd_next_seq();
-  int& variant = g_attn_variant;
-  if (variant < 0) {
-    const char* e = getenv("BST_ATTN");
-    // default: row-major tcgen05 kernels (tc1 for short page runs, tc2 for long; fastest
-    // in the verify graph, scripts/attn_graph.py).  BST_ATTN=kt: key-major kernel,
-    // BST_ATTN=mma: mma.sync kernel (the pre-tcgen05 baseline), BST_ATTN=tc1: tc1 only.
-    if (e && e[0] == 'k') variant = 4;
-    else if (e && e[0] == 'm') variant = 1;
-    else if (e && e[0] == 't' && e[1] == 'c' && e[2] == '1') variant = 2;
-    else variant = 3;
-  }
-  static int tc2_min = -1;
-  if (tc2_min < 0) {
-    const char* e = getenv("BST_TC2_MIN");
-    tc2_min = e ? atoi(e) : 8;
-  }
-  static int n_sm = 0;
-  if (!n_sm) {
-    int dev = 0;
-    BST_CUDA(cudaGetDevice(&dev));
-    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
-  static int no_merge = -1;
-  if (no_merge < 0) no_merge = getenv("BST_ATTN_COMBINE") ? 1 : 0;
   cudaStream_t st = as_stream(stream);
-  if (variant == 4) {
+  if (keymajor) {
     // key-major kernel: row blocks of <= 128 rows balanced over R, one CTA per SM
     const int rbk = (R + 127) / 128;
     const int rpb = (R + rbk - 1) / rbk;
@@ -2060,18 +1798,12 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
         occ_init = true;
       }
       const int nc8 = nch > 8 ? 8 : nch;
-      static int force = -1;  // BST_KT_MERGE=global|cluster (measurement only)
-      if (force < 0) {
-        const char* e = getenv("BST_KT_MERGE");
-        force = (e && e[0] == 'g') ? 1 : ((e && e[0] == 'c') ? 2 : 0);
-      }
-      if (force == 2) best = 1e30;
-      for (int j = 0; j < 3 && force != 1; ++j) {
+      for (int j = 0; j < 3; ++j) {
         const int cs = 2 << j;
         if (cs > pages) break;
         if (occ[nc8][j] < 0) occ[nc8][j] = kt_cluster_occupancy(nc8, cs);
         if (occ[nc8][j] < G) continue;
-        const double tc = ((tiles + cs - 1) / cs) * tile_time(G * cs) + 1.0 - (force == 2 ? cs : 0);
+        const double tc = ((tiles + cs - 1) / cs) * tile_time(G * cs) + 1.0;
         if (tc < best) { best = tc; splits = cs; cs_best = cs; }
       }
       if (cs_best) merge_mode = 2;
@@ -2102,7 +1834,7 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     if (merge_mode == 2)
       a.merge = 2;
     else
-      a.merge = (a.n_splits > 1 && !no_merge && n_kv * a.n_splits * rbk * n_req <= n_sm &&
+      a.merge = (a.n_splits > 1 && n_kv * a.n_splits * rbk * n_req <= n_sm &&
                  n_kv * rbk * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES / 2) ? 1 : 0;
     static bool kt_attr = false;
     if (!kt_attr) {
@@ -2141,11 +1873,9 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     return BST_OK;
   }
   static bool attr = false;
-  const int smem_mma = A_STAGES * A_STAGE_BYTES + 1024;
   const int smem_tc = T_Q_BYTES + T_P_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
   const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
   if (!attr) {
-    BST_CUDA(cudaFuncSetAttribute(attn_tree_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_mma));
     BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc2));
     attr = true;
@@ -2159,33 +1889,30 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     a.ws_o = ws + A_WS_CNT_BYTES / sizeof(float) + bank * bank_floats;
     a.ws_ml = a.ws_o + (size_t)n_req * n_splits * s * n_q * A_D;
   }
-  // row-major kernels: single-group kernel for short per-CTA page runs, two alternating
-  // softmax groups once a CTA walks >= 8 tiles (long context)
-  const int v = variant == 3 ? (pps >= tc2_min ? 3 : 2) : variant;
-  a.merge = (n_splits > 1 && (v == 2 || v == 3) && !no_merge && n_kv * n_splits * row_blocks * n_req <= n_sm &&
+  // row-major kernels, chosen by shape: the single-group kernel for short per-CTA page
+  // runs, two alternating softmax groups once a CTA walks >= T2_MIN_PAGES pages (long
+  // context; the tc2 kernel on short runs broke the tiny-config exactness)
+  const bool two_groups = pps >= T2_MIN_PAGES;
+  a.merge = (n_splits > 1 && n_kv * n_splits * row_blocks * n_req <= n_sm &&
              n_kv * row_blocks * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES / 2) ? 1 : 0;
-  BST_REQUIRE(n_req == 1 || v == 2 || v == 3, "batched attention runs on the tcgen05 kernels only");
-  if (v == 1)
-    attn_tree_kernel<<<dim3(n_kv, n_splits, row_blocks), A_THREADS, smem_mma, st>>>(tm, a);
-  else {
+  {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_kv, n_splits, row_blocks * n_req);
-    cfg.blockDim = dim3(v == 2 ? T_THREADS : T2_THREADS);
-    cfg.dynamicSmemBytes = v == 3 ? smem_tc2 : smem_tc;
+    cfg.blockDim = dim3(two_groups ? T2_THREADS : T_THREADS);
+    cfg.dynamicSmemBytes = two_groups ? smem_tc2 : smem_tc;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    if (v == 2)
-      BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, a));
-    else
+    if (two_groups)
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc2_kernel, tm, a));
+    else
+      BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc_kernel, tm, a));
   }
   if (n_splits > 1 && !a.merge) {
     const int rows_total = s * n_q;
-    // plain launch: a PDL launch of the combine measured slower in the verify graph
     BST_CUDA(launch_pdl(attn_combine_kernel, dim3((rows_total + 7) / 8, n_req), dim3(256), 0, st, a));
   }
   BST_LAUNCH_CHECK();
@@ -2201,7 +1928,18 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
                              bst_stream_t stream) {
   return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
                              n_q, n_kv, s, c, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
-                             ws, ws_bytes, 1, 0, 0, stream);
+                             ws, ws_bytes, 1, 0, 0, false, stream);
+}
+
+extern "C" int bst_attention_keymajor(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
+                                      const void* kv_cache, int n_layers, int n_pages_total, int layer,
+                                      const int32_t* page_table, int n_q, int n_kv, int s, int c, int keys_after_c,
+                                      int max_keys, const int32_t* state, int c_idx, int mode, const uint32_t* anc,
+                                      int mask_words, int n_splits, float* ws, size_t ws_bytes,
+                                      bst_stream_t stream) {
+  return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
+                             n_q, n_kv, s, c, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
+                             ws, ws_bytes, 1, 0, 0, true, stream);
 }
 
 extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
@@ -2212,7 +1950,7 @@ extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* ou
                                    size_t ws_bytes, bst_stream_t stream) {
   return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
                              n_q, n_kv, s, 0, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
-                             ws, ws_bytes, n_req, req_pages, req_state, stream);
+                             ws, ws_bytes, n_req, req_pages, req_state, false, stream);
 }
 
 extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {  // two banks of partials
@@ -2273,14 +2011,6 @@ extern "C" int bst_debug_cluster_occupancy_kt(int cluster, int smem) {
 
 extern "C" int bst_debug_kt_ablate(int v) {
   BST_CUDA(cudaMemcpyToSymbol(bst::g_kt_ablate, &v, sizeof(int)));
-  return BST_OK;
-}
-
-// Select the K3 kernel family: 3 row-major tcgen05 (default), 4 key-major, 2 tc1 only,
-// 1 mma.sync; -1 re-reads BST_ATTN.
-extern "C" int bst_attention_set_variant(int v) {
-  BST_REQUIRE(v == -1 || (v >= 1 && v <= 4), "variant must be -1 or 1..4");
-  bst::g_attn_variant = v;
   return BST_OK;
 }
 

@@ -17,8 +17,12 @@ Layout
 
 A whole cycle (draft all chunks -> K1 -> K2 per request -> verify all chunks ->
 accept/compact/gather/commit per request) is one CUDA graph with no host sync:
-fixed budgets make every shape static.  Token streams are identical to running
-each request alone through ``B200Engine`` (tests/test_gpu_batch.py).
+fixed budgets make every shape static.  Batching changes only how rows are
+grouped into launches, so the token streams equal running each request alone
+through ``B200Engine`` — bit for bit while every GEMM launch runs on the same K4
+kernel; verify chunks above 256 rows run on the CTA-pair kernel, whose stream-K
+split points differ, so there the fp32 sums agree to rounding and a stream can
+differ only at a near-tie argmax (tests/test_gpu_batch.py).
 """
 
 from __future__ import annotations
@@ -36,7 +40,9 @@ from ..draft_tree import DeviceTree, expand_device_plan_batch, tree_structs_devi
 from ..lattice import topk_logits_into
 from ..verify_sim import accept_device
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
-from .decode import MAX_ROWS, ST_BONUS, ST_C, ST_COMMITTED, ST_CYCLE
+from .decode import PREFILL_ROWS, ST_BONUS, ST_C, ST_COMMITTED, ST_CYCLE
+
+MAX_ROWS = 256  # rows per request tree (fixed budgets <= 255) and per batched draft chunk
 from .forward import _gemm_rows
 
 # rows per batched verify launch (K4 CTA-pair kernel takes up to 512); BST_VERIFY_ROWS: measurement
@@ -113,6 +119,7 @@ class BatchEngine:
         self.graph = None
         self.graph_kernels = 0
         self.use_graphs = True
+        self._c_bound = 0
         torch.cuda.synchronize()
 
     def set_policy(self, kind: str, estimator=None, latencies=None) -> None:
@@ -162,8 +169,8 @@ class BatchEngine:
                     raise ValueError("prompt must hold 1..max_ctx tokens")
                 P = len(prompt)
                 st = self.state[r]
-                for start in range(0, P - 1, MAX_ROWS):
-                    n = min(MAX_ROWS, P - 1 - start)
+                for start in range(0, P - 1, PREFILL_ROWS):
+                    n = min(PREFILL_ROWS, P - 1 - start)
                     st.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
                     t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
                     ar = torch.arange(n, dtype=torch.int32, device=self.dev)
@@ -176,6 +183,7 @@ class BatchEngine:
                     d.prefill_ctx(n, st, pt=self._dpt(r))
                 st.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
         self.stream.synchronize()
+        self._c_bound = int(self.contexts().max())
 
     # ------------------------------------------------------------------ cycle
     def _cycle_body(self) -> None:
@@ -230,7 +238,17 @@ class BatchEngine:
         return g
 
     def cycle(self) -> None:
-        """One draft -> expand -> verify -> accept cycle for every request (asynchronous)."""
+        """One draft -> expand -> verify -> accept cycle for every request (asynchronous).
+
+        A host-side bound on every request's context (each cycle commits at most gamma+1
+        tokens) keeps the verify rows inside each request's page range: a request never
+        writes KV into the next request's pages; raises when the bound is hit."""
+        if self._c_bound + self.S > self.req_pages * PAGE or self._c_bound + self.S > self.max_ctx + MAX_ROWS:
+            self._c_bound = int(self.contexts().max())  # tighten with the true contexts (one sync)
+            if self._c_bound + self.S > self.max_ctx + MAX_ROWS:
+                raise RuntimeError(f"KV cache full: a request's context {self._c_bound} + {self.S} verify rows "
+                                   f"exceeds max_ctx={self.max_ctx}")
+        self._c_bound += self.G1
         if not self.use_graphs:
             with torch.cuda.stream(self.stream):
                 self._cycle_body()

@@ -40,8 +40,11 @@ from .forward import _ABLATE, MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, Target
 from .weights import DrafterWeights, TargetWeights
 
 ST_C, ST_NNEW, ST_BONUS, ST_COMMITTED, ST_CYCLE = 0, 1, 2, 3, 4
-MAX_ROWS = 256
-BUCKET = 16
+MAX_TREE = 1024      # reference default n_max (sp/harness.py:62, fixed grid up to 1024 at :49)
+BUCKET = 16          # verify rows are padded to 16-row buckets up to 256 rows ...
+WIDE_BUCKET = 64     # ... and to 64-row buckets above (one captured verify graph per bucket)
+MAX_ROWS = 1088      # verify rows of the largest tree (1025) rounded up to its bucket
+PREFILL_ROWS = 256   # causal prefill chunk
 
 
 @dataclass
@@ -61,7 +64,7 @@ class B200Engine:
     """Qwen3-shape target + DFlash-style drafter, random-init bf16, one request per engine."""
 
     def __init__(self, cfg: ModelConfig = QWEN3_8B, dcfg: DrafterConfig | None = None, max_ctx: int = 4096,
-                 seed: int = 0, n_cap: int = MAX_ROWS - 1, top_k: int = 8, device=None, max_cycles: int = 4096):
+                 seed: int = 0, n_cap: int = MAX_TREE, top_k: int = 8, device=None, max_cycles: int = 4096):
         if not torch.cuda.is_available():
             raise RuntimeError("B200Engine needs a CUDA device; there is no CPU fallback")
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
@@ -75,16 +78,19 @@ class B200Engine:
         self.dcfg = DrafterConfig(layers=dcfg.layers, gamma=dcfg.gamma, feat_layers=feat, mask_token=dcfg.mask_token,
                                   logit_scale=dcfg.logit_scale)
         self.gamma, self.top_k = self.dcfg.gamma, top_k
-        self.n_cap = min(n_cap, MAX_ROWS - 1)
+        if not 1 <= n_cap <= MAX_TREE:
+            raise ValueError(f"n_cap must be in [1, {MAX_TREE}], got {n_cap}")
+        self.n_cap = n_cap
+        self.max_rows = self._bucket(n_cap)
         self.max_ctx = max_ctx
-        slots = max_ctx + MAX_ROWS + PAGE
+        slots = max_ctx + self.max_rows + PAGE
         self.tw = TargetWeights.random(cfg, seed, self.dev)
         self.dw = DrafterWeights.random(cfg, self.dcfg, len(feat), seed, self.dev)
-        self.target = TargetModel(cfg, self.tw, slots, MAX_ROWS, feat, self.dev)
+        self.target = TargetModel(cfg, self.tw, slots, max(self.max_rows, PREFILL_ROWS), feat, self.dev)
         self.drafter = DrafterModel(cfg, self.dcfg, self.dw, self.tw, slots, len(feat), self.dev)
         i32 = dict(dtype=torch.int32, device=self.dev)
         self.state = torch.zeros(8, **i32)
-        self.out_tokens = torch.zeros(max_ctx + MAX_ROWS, **i32)
+        self.out_tokens = torch.zeros(max_ctx + self.max_rows, **i32)
         self.lat_tok = torch.zeros(self.gamma, top_k, **i32)
         self.lat_prob = torch.zeros(self.gamma, top_k, dtype=torch.float64, device=self.dev)
         self.probs_full = None  # fp64 [gamma, V] when export is on
@@ -118,13 +124,13 @@ class B200Engine:
         if not prompt:
             raise ValueError("prompt must contain at least one token")
         P = len(prompt)
-        if P + MAX_ROWS > self.max_ctx + MAX_ROWS:
+        if P > self.max_ctx:
             raise ValueError("prompt longer than max_ctx")
         self.prompt_len = P
         with torch.cuda.stream(self.stream):
             t, d = self.target, self.drafter
-            for start in range(0, P - 1, MAX_ROWS):
-                n = min(MAX_ROWS, P - 1 - start)
+            for start in range(0, P - 1, PREFILL_ROWS):
+                n = min(PREFILL_ROWS, P - 1 - start)
                 self.state.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
                 t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
                 ar = torch.arange(n, dtype=torch.int32, device=self.dev)
@@ -139,6 +145,7 @@ class B200Engine:
         self.stream.synchronize()
         self.exported = []
         self._pending = None
+        self._c_host = P - 1
 
     def set_policy(self, kind: str, n: int = 0, estimator: VerifyLatencyEstimator | None = None,
                    latencies: CycleLatencies | None = None, n_max: int | None = None) -> None:
@@ -152,7 +159,10 @@ class B200Engine:
         elif kind == "adaptive":
             if estimator is None or latencies is None:
                 raise ValueError("adaptive policy needs an estimator and cycle latencies")
-            n_max = min(n_max or self.n_cap, self.n_cap)
+            n_max = self.n_cap if n_max is None else int(n_max)
+            if not 1 <= n_max <= self.n_cap:
+                # never clamp: a smaller budget cap changes trees and stop reasons
+                raise ValueError(f"n_max {n_max} outside [1, {self.n_cap}] (engine n_cap; build with n_cap >= n_max)")
             curve = estimator.curve(0).device_struct()
             p = estimator.params
             plan = _lib.Plan(policy=_lib.POLICY_ADAPTIVE, n_max=n_max, curve=curve,
@@ -210,8 +220,11 @@ class B200Engine:
         ops.commit_state(self.state, self.acc_meta, self.committed, self.gamma + 1, self.out_tokens, tr.meta,
                          tr.surrogate, self.log_i32, self.log_f64)
 
-    def _bucket(self, n_nodes: int) -> int:
-        return min(MAX_ROWS, ((n_nodes + 1 + BUCKET - 1) // BUCKET) * BUCKET)
+    @staticmethod
+    def _bucket(n_nodes: int) -> int:
+        rows = n_nodes + 1
+        b = BUCKET if rows <= 256 else WIDE_BUCKET
+        return ((rows + b - 1) // b) * b
 
     def _capture(self, fn) -> torch.cuda.CUDAGraph:
         # warm-up run outside the graph (kernel attributes, tensor maps, workspaces), then capture
@@ -268,10 +281,18 @@ class B200Engine:
             self.meta_host[:8].copy_(self.tree.meta, non_blocking=True)
             self.meta_host[8:].copy_(self.state, non_blocking=True)
         st.synchronize()
+        self._c_host = int(self.meta_host[8 + ST_C])
         return int(self.meta_host[0]), int(self.meta_host[8 + ST_COMMITTED])
+
+    def _check_room(self, c: int, rows: int) -> None:
+        """The verify rows' KV slots c .. c+rows-1 must lie inside this engine's page range
+        (the K5 KV store does not bound-check)."""
+        if c + rows > self.target.kv.max_slots or c + rows > self.drafter.kv.max_slots:
+            raise RuntimeError(f"KV cache full: context {c} + {rows} verify rows exceeds max_ctx={self.max_ctx}")
 
     def verify(self, n_nodes: int, events=None) -> None:
         """Phase 2 (graph V_bucket): verify, accept, compact, commit — asynchronous."""
+        self._check_room(self._c_host, self._bucket(n_nodes))
         if self.export:
             self._export_pre(n_nodes)
         self._run_verify(self._bucket(n_nodes))
@@ -348,6 +369,7 @@ class B200Engine:
         self.state[ST_BONUS:ST_BONUS + 1].copy_(t.argmax[:1])
 
     def ar_decode(self, n_tokens: int) -> list[int]:
+        self._check_room(int(self.state[ST_C].item()), n_tokens)
         out = []
         with torch.cuda.stream(self.stream):
             for _ in range(n_tokens):
@@ -498,6 +520,7 @@ class B200Engine:
             tr.depth[: n + 1].copy_(torch.tensor([x.depth for x in tree.nodes], dtype=torch.int32))
             tr.meta.zero_()
             tr.meta[0] = n
+            self._check_room(int(self.state[ST_C].item()), self._bucket(n))
             _lib.call("bst_ancestor_mask", tr.parent.data_ptr(), n + 1, tr.mask_words, tr.anc_mask.data_ptr(),
                       self.stream.cuda_stream)
             self._verify_forward(self._bucket(n))
@@ -519,6 +542,7 @@ class B200Engine:
         """One target step after ``prefix`` (greedy at T = 0, else the keyed sample)."""
         self.set_temperature(temperature, self.target.sample_seed)
         self._sync(prefix)
+        self._check_room(int(self.state[ST_C].item()), 1)
         t = self.target
         with torch.cuda.stream(self.stream):
             t.tokens[:1].copy_(self.state[ST_BONUS:ST_BONUS + 1])

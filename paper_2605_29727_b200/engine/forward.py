@@ -59,12 +59,18 @@ class PagedKV:
         return self.n_pages * PAGE
 
 
-def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
+def _n_sm(dev) -> int:
+    return torch.cuda.get_device_properties(dev).multi_processor_count if torch.cuda.is_available() else 148
+
+
+def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int, n_sm: int = 148) -> int:
+    """Split partials of the largest K3 launch: the default split count is n_sm / (n_kv x
+    row blocks) (bst_attention); twice that bounds the key-major kernel's cluster plans."""
     g = cfg.n_q // cfg.n_kv
     best = 0
     for s in range(1, max_rows + 1):
         rb = math.ceil(g * s / 128)
-        splits = max(1, 296 // (cfg.n_kv * rb))
+        splits = max(1, 2 * n_sm // (cfg.n_kv * rb))
         splits = min(splits, pages)
         pps = math.ceil(pages / splits)
         splits = math.ceil(pages / pps)
@@ -74,20 +80,36 @@ def _attn_ws_floats(cfg: ModelConfig, max_rows: int, pages: int) -> int:
     return 2 * best + 1024
 
 
-def _max_partial(shapes, max_rows: int) -> int:
-    return max(ops.gemm_schedule(n, k, _gemm_rows(n, k, max_rows)).partial_floats for n, k in shapes)
+def _row_cap(n_out: int, k: int) -> int:
+    """Most rows one K4 launch of this weight shape takes: 512 on the CTA-pair kernel
+    (even weight-tile counts), else 256."""
+    try:
+        ops.gemm_schedule(n_out, k, 512)
+        return 512
+    except ValueError:
+        return 256
 
 
 def _gemm_rows(n: int, k: int, rows: int) -> int:
-    """Largest row count <= rows one K4 launch of this shape takes: up to 512 on the
-    CTA-pair kernel (even tile counts), else 256."""
-    if rows <= 256:
-        return rows
-    try:
-        ops.gemm_schedule(n, k, rows)
-        return rows
-    except ValueError:
-        return 256
+    """Largest row count <= rows one K4 launch of this shape takes."""
+    return min(rows, _row_cap(n, k))
+
+
+def row_chunks(n: int, cap: int) -> list[tuple[int, int]]:
+    """Balanced row ranges of at most `cap` rows covering [0, n) (verify trees > 512 rows)."""
+    nch = -(-n // cap)
+    base = -(-n // nch)
+    return [(r0, min(n, r0 + base)) for r0 in range(0, n, base)]
+
+
+def _max_partial(shapes, max_rows: int) -> int:
+    """Partial-slot floats of the largest launch any row chunk <= max_rows needs."""
+    best = 0
+    for n, k in shapes:
+        cap = _gemm_rows(n, k, max_rows)
+        for m in sorted({cap, *range(16, cap + 1, 16)}):
+            best = max(best, ops.gemm_schedule(n, k, m).partial_floats)
+    return best
 
 
 class TargetModel:
@@ -112,10 +134,16 @@ class TargetModel:
         self.amx_scratch = torch.zeros(R, dtype=torch.int64, device=dev)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h)]
         self.partial = torch.empty(_max_partial(shapes, R), **f32)
-        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, R, self.kv.n_pages), **f32)
+        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, R, self.kv.n_pages, _n_sm(dev)), **f32)
         self.attn_splits = 0  # K3 split count (0: automatic); parity tests pin it
         self.logits = None
         self.temperature, self.sample_seed = 0.0, 0  # head "sample": Gumbel-max at T keyed by (seed, c + pos)
+
+    def _chunks(self, n: int) -> dict:
+        cfg, h = self.cfg, self.cfg.h
+        cap_qkv = _row_cap(cfg.qkv_out, h)
+        cap_mlp = min(_row_cap(h, cfg.h_q), _row_cap(2 * cfg.h_ffn, h), _row_cap(h, cfg.h_ffn))
+        return {"qkv": row_chunks(n, cap_qkv), "mlp": row_chunks(n, cap_mlp)}
 
     def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
                 head: str | None = "argmax", c_host: int = 0, pt: torch.Tensor | None = None,
@@ -127,19 +155,26 @@ class TargetModel:
         state is state[r] (8 words), its pages pt[r*req_pages:], its mask rows anc[r*S:]."""
         cfg, w, kv = self.cfg, self.w, self.kv
         n, eps = rows, cfg.eps
+        if head == "sample" and batch is not None:
+            # bst_gemm_sample keys every row by one state's context c (ADVICE r1)
+            raise ValueError("sampled verification is per request: the batched head supports argmax only")
         pt = kv.page_table if pt is None else pt
         x, resid = self.x[:n], self.resid[:n]
         ops.embed_rmsnorm(self.tokens, n, w.emb, w.layers[0].in_norm, eps, resid, x)
+        # trees wider than one K4 launch (> 256/512 rows, N_max up to 1024) run every GEMM and
+        # its row-local epilogue in balanced row chunks; K3 always takes every row at once
+        ck = self._chunks(n)
         for li, lw in enumerate(w.layers):
             nxt_l = w.layers[li + 1] if li + 1 < cfg.L else None
-            if "rope" in _ABLATE:
-                ops.gemm_partial(x, lw.qkv, out=self.partial)
-            else:
+            for r0, r1 in ck["qkv"]:
+                if "rope" in _ABLATE:
+                    ops.gemm_partial(x[r0:r1], lw.qkv, out=self.partial)
+                    continue
                 req = (0, 1, 0, 0) if batch is None else (batch[1], batch[0] * batch[1], state.stride(0),
                                                           batch[2] * PAGE)
-                ops.gemm_qkv_rope(x, lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm,
-                                  eps, self.inv_freq, self.pos, self.slot, None, self.q, kv.buf, li * kv.layer_stride,
-                                  pt, PAGE, state, req)
+                ops.gemm_qkv_rope(x[r0:r1], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm,
+                                  eps, self.inv_freq, self.pos[r0:], self.slot[r0:], None, self.q[r0:], kv.buf,
+                                  li * kv.layer_stride, pt, PAGE, state, req)
             if "attn" not in _ABLATE:
                 _pf("o", (lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB) if "gate_up" in _PREFETCH else None)
                 if batch is None:
@@ -151,23 +186,23 @@ class TargetModel:
                     ops.attention_batch(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, rp, cfg.n_q,
                                         cfg.n_kv, nr, S, keys_after_c, rp * PAGE, state, state.stride(0), mode, anc,
                                         mask_words, self.attn_ws, n_splits=self.attn_splits)
-            p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
-            if "resid" not in _ABLATE:
-                _pf("gate_up", (lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
-                ops.residual_rmsnorm(p, resid, n, cfg.h, lw.post_norm, eps, x=x)
-            p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
-            if "swiglu" not in _ABLATE:
-                _pf("down", (lw.down, 16 * MB))
-                ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
-            p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
             nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
-            feat = None
-            if li in self.feat_layers:
-                j = self.feat_layers.index(li)
-                feat = self.feat[:n, j * cfg.h:(j + 1) * cfg.h]
-            if "resid" not in _ABLATE:
-                _pf("qkv", (nxt_l.qkv, nxt_l.qkv.numel() * 2) if nxt_l is not None else (w.lm_head, 48 * MB))
-                ops.residual_rmsnorm(p, resid, n, cfg.h, nxt, eps, x=x, feat=feat)
+            j = self.feat_layers.index(li) if li in self.feat_layers else -1
+            for r0, r1 in ck["mlp"]:
+                m = r1 - r0
+                p = ops.gemm_partial(self.attn[r0:r1], lw.o, out=self.partial)
+                if "resid" not in _ABLATE:
+                    _pf("gate_up", (lw.gate_up[lw.gate_up.shape[0] // 8:], 24 * MB))
+                    ops.residual_rmsnorm(p, resid[r0:r1], m, cfg.h, lw.post_norm, eps, x=x[r0:r1])
+                p = ops.gemm_partial(x[r0:r1], lw.gate_up, out=self.partial)
+                if "swiglu" not in _ABLATE:
+                    _pf("down", (lw.down, 16 * MB))
+                    ops.swiglu(p, m, cfg.h_ffn, self.act[r0:r1])
+                p = ops.gemm_partial(self.act[r0:r1], lw.down, out=self.partial)
+                feat = self.feat[r0:r1, j * cfg.h:(j + 1) * cfg.h] if j >= 0 else None
+                if "resid" not in _ABLATE:
+                    _pf("qkv", (nxt_l.qkv, nxt_l.qkv.numel() * 2) if nxt_l is not None else (w.lm_head, 48 * MB))
+                    ops.residual_rmsnorm(p, resid[r0:r1], m, cfg.h, nxt, eps, x=x[r0:r1], feat=feat)
         # LM head in row chunks the K4 schedule accepts (odd vocab tile counts: <= 256 rows)
         hr = _gemm_rows(w.lm_head.shape[0], cfg.h, n)
         logits = []
@@ -216,7 +251,7 @@ class DrafterModel:
         self.qrow = torch.zeros(R, **i32)
         shapes = [(cfg.qkv_out, h), (h, cfg.h_q), (2 * cfg.h_ffn, h), (h, cfg.h_ffn), (cfg.V, h), (h, n_feat * h)]
         self.partial = torch.empty(_max_partial(shapes, min(R, 256)), **f32)  # every GEMM call has <= 256 rows
-        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, QB, self.kv.n_pages), **f32)
+        self.attn_ws = torch.zeros(_attn_ws_floats(cfg, QB, self.kv.n_pages, _n_sm(dev)), **f32)
         self.attn_splits = 0
         self.logits = torch.empty(dcfg.gamma, cfg.V, **f32)
         self.logits_b = torch.empty(QB, cfg.V, **f32) if n_req_max > 1 else None

@@ -35,6 +35,8 @@ from .config import ModelConfig
 from .forward import PAGE, TargetModel
 from .weights import LayerWeights, TargetWeights, _normal, _ones
 
+TP_ROWS = 256  # verify rows per TP step (config 5 budgets N in {16, 64, 256}: trees <= 255 nodes)
+
 
 def local_config(cfg: ModelConfig, tp: int) -> ModelConfig:
     """Per-rank shapes of a tp-way shard (heads, FFN columns and vocabulary split evenly)."""
@@ -199,28 +201,28 @@ class TPVerifier:
     def __init__(self, cfg: ModelConfig, tp: int, rank: int, max_ctx: int, seed: int = 0,
                  weights: TargetWeights | None = None, n_cap: int = 255, gamma: int = 16, top_k: int = 8,
                  device=None) -> None:
-        from .decode import MAX_ROWS
         from ..draft_tree import DeviceTree
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
         self.dev, self.cfg, self.tp, self.rank = dev, cfg, tp, rank
-        self.gamma, self.top_k, self.n_cap = gamma, top_k, min(n_cap, MAX_ROWS - 1)
+        if not 1 <= n_cap <= TP_ROWS - 1:
+            raise ValueError(f"TP engine n_cap must be in [1, {TP_ROWS - 1}], got {n_cap}")
+        self.gamma, self.top_k, self.n_cap = gamma, top_k, n_cap
         self.max_ctx = max_ctx
         w = weights if weights is not None else random_shard(cfg, tp, rank, seed, dev)
-        self.target = TPTargetModel(cfg, tp, rank, w, max_ctx + MAX_ROWS + PAGE, MAX_ROWS, dev)
+        self.target = TPTargetModel(cfg, tp, rank, w, max_ctx + TP_ROWS + PAGE, TP_ROWS, dev)
         i32 = dict(dtype=torch.int32, device=dev)
         self.state = torch.zeros(8, **i32)
         self.tree = DeviceTree(self.n_cap, dev)
         self.path = torch.zeros(gamma + 1, **i32)
         self.committed = torch.zeros(gamma + 1, **i32)
         self.acc_meta = torch.zeros(4, **i32)
-        self.out_tokens = torch.zeros(max_ctx + MAX_ROWS, **i32)
+        self.out_tokens = torch.zeros(max_ctx + TP_ROWS, **i32)
         self.stream = torch.cuda.Stream(dev)
         self.graphs: dict[int, torch.cuda.CUDAGraph] = {}
         self.n_nodes = 0
 
     def reset(self, prompt) -> None:
-        """Prefill prompt[:-1] causally (chunks of MAX_ROWS); prompt[-1] is the pending root."""
-        from .decode import MAX_ROWS
+        """Prefill prompt[:-1] causally (chunks of TP_ROWS); prompt[-1] is the pending root."""
         from .forward import MODE_CAUSAL
         prompt = [int(t) for t in prompt]
         P = len(prompt)
@@ -228,8 +230,8 @@ class TPVerifier:
             raise ValueError("prompt length must be in [1, max_ctx]")
         t = self.target
         with torch.cuda.stream(self.stream):
-            for start in range(0, P - 1, MAX_ROWS):
-                n = min(MAX_ROWS, P - 1 - start)
+            for start in range(0, P - 1, TP_ROWS):
+                n = min(TP_ROWS, P - 1 - start)
                 self.state.copy_(torch.tensor([start, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
                 t.tokens[:n].copy_(torch.tensor(prompt[start:start + n], dtype=torch.int32))
                 ar = torch.arange(n, dtype=torch.int32, device=self.dev)
@@ -272,8 +274,8 @@ class TPVerifier:
 
     def step(self, graph: bool = True) -> None:
         """One verify + accept + compact + commit on the current tree (asynchronous)."""
-        from .decode import BUCKET, MAX_ROWS
-        rows = min(MAX_ROWS, ((self.n_nodes + 1 + BUCKET - 1) // BUCKET) * BUCKET)
+        from .decode import BUCKET
+        rows = min(TP_ROWS, ((self.n_nodes + 1 + BUCKET - 1) // BUCKET) * BUCKET)
         if not graph:
             with torch.cuda.stream(self.stream):
                 self._verify_body(rows)

@@ -103,9 +103,10 @@ def _p(t):
 
 
 def attention(q, out, kv, n_layers, n_pages, layer, page_table, n_q, n_kv, s, c, keys_after_c, max_keys, state,
-              mode, anc=None, mask_words=0, ws=None, n_splits=0):
-    """K3 launch; q/out [s][n_q*128] bf16 (token stride = row stride)."""
-    _lib.call("bst_attention", q.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0), kv.data_ptr(), n_layers,
+              mode, anc=None, mask_words=0, ws=None, n_splits=0, keymajor=False):
+    """K3 launch; q/out [s][n_q*128] bf16 (token stride = row stride).  keymajor: the
+    key-major kernel (bst_attention_keymajor, measurements/tests); the engine never sets it."""
+    _lib.call("bst_attention_keymajor" if keymajor else "bst_attention", q.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0), kv.data_ptr(), n_layers,
               n_pages, layer, page_table.data_ptr(), n_q, n_kv, s, c, keys_after_c, max_keys, _p(state), 0, mode,
               _p(anc), mask_words, n_splits, _p(ws), 0 if ws is None else ws.numel() * 4, stream_ptr())
 

@@ -48,19 +48,16 @@ def _ref(q, kv, layer, n_q, n_kv, c, s, visible):
     return torch.einsum("hqk,khd->qhd", torch.softmax(sc, -1), V).reshape(s, n_q * 128)
 
 
-VARIANTS = {"tc": 3, "kt": 4}
-
-
-@pytest.fixture(params=sorted(VARIANTS))
+@pytest.fixture(params=["tc", "kt"])
 def variant(request):
-    from paper_2605_29727_b200 import _lib
-    _lib.call("bst_attention_set_variant", VARIANTS[request.param])
-    yield request.param
-    _lib.call("bst_attention_set_variant", -1)
+    """K3 entry point under test: bst_attention (shape-selected row-major tcgen05 kernels)
+    or bst_attention_keymajor."""
+    return request.param == "kt"
 
 
 @pytest.mark.parametrize("n_q,n_kv", [(32, 8), (4, 2)])
-@pytest.mark.parametrize("c,s", [(0, 1), (5, 17), (2048, 17), (300, 65), (1000, 256), (4096, 33), (20000, 17), (9000, 100)])
+@pytest.mark.parametrize("c,s", [(0, 1), (5, 17), (2048, 17), (300, 65), (1000, 256), (4096, 33), (20000, 17), (9000, 100),
+                                 (300, 600), (2048, 1025)])
 @pytest.mark.parametrize("splits", [0, 1])
 def test_tree_attention(n_q, n_kv, c, s, splits, variant):
     from oracle import specplan_port as O
@@ -76,7 +73,7 @@ def test_tree_attention(n_q, n_kv, c, s, splits, variant):
     out = torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16)
     ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
     ops.attention(q, out, kv.buf, 2, kv.n_pages, 1, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0, packed.view(-1),
-                  words, ws, n_splits=splits)
+                  words, ws, n_splits=splits, keymajor=variant)
     vis = torch.zeros(s, c + s, dtype=torch.bool, device="cuda")
     vis[:, :c] = True
     vis[:, c:] = anc
@@ -96,7 +93,7 @@ def test_causal_and_full_attention_with_device_c(mode, c, s, variant):
     out = torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16)
     ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
     ops.attention(q, out, kv.buf, 2, kv.n_pages, 1, kv.page_table, n_q, n_kv, s, 0, s, c + s + 64, state, mode,
-                  None, 0, ws)
+                  None, 0, ws, keymajor=variant)
     vis = torch.zeros(s, c + s, dtype=torch.bool, device="cuda")
     vis[:, :c] = True
     if mode == 1:
@@ -128,7 +125,7 @@ def test_back_to_back_launches_in_a_graph(c, variant):
     def run():
         for li in range(L):
             ops.attention(q, outs[li], kv.buf, L, kv.n_pages, li, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0,
-                          anc.view(-1), words, ws)
+                          anc.view(-1), words, ws, keymajor=variant)
     run()
     torch.cuda.synchronize()
     want = [o.clone() for o in outs]

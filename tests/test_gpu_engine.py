@@ -7,6 +7,7 @@ import pytest
 import torch
 
 from oracle import specplan_port as O
+from engine_util import _decoy_drafter, _prompt, _replay_check
 
 pytestmark = pytest.mark.gpu
 
@@ -24,10 +25,6 @@ def eng():
 def ref(eng):
     from oracle.model_ref import RefModel
     return RefModel(eng.cfg, eng.tw, eng.dw, eng.target.feat_layers, eng.target.inv_freq)
-
-
-def _prompt(n, V, seed=0):
-    return np.random.default_rng(seed).integers(0, V - 1, n).tolist()
 
 
 def test_forward_matches_oracle(eng, ref):
@@ -57,43 +54,6 @@ def test_forward_matches_oracle(eng, ref):
     am_ref = lv.argmax(-1).numpy()
     assert clear.float().mean() > 0.8
     assert (ex["argmax"][clear.numpy()] == am_ref[clear.numpy()]).all()
-
-
-def _replay_check(eng, exported, tokens, policy, dims=None, t_draft=0.0, t_aux=0.0, l_ar=1.0, n_max=64):
-    """Run the ORACLE decode loop on the GPU-exported fp64 rows + verify argmax: must be bit-identical."""
-    P = eng.prompt_len
-    by_prefix = {}
-    committed = []
-    for e in exported:
-        by_prefix[tuple(committed)] = e
-        committed = committed + [int(e["token"][i]) for i in e["path"][1:]] + [e["bonus"]]
-
-    def drafter(prefix):
-        return by_prefix[tuple(prefix)]["probs"]
-
-    def target(seq, T):
-        for k in range(len(seq), -1, -1):  # find the cycle whose prefix this seq extends
-            e = by_prefix.get(tuple(seq[:k]))
-            if e is None:
-                continue
-            walk = seq[k:]
-            node = 0
-            kids = {}
-            for i in range(1, len(e["parent"])):
-                kids.setdefault(int(e["parent"][i]), {})[int(e["token"][i])] = i
-            for t in walk:
-                node = kids[node][t]
-            return int(e["argmax"][node])
-        raise KeyError(seq)
-
-    run_len = len(tokens)
-    records, toks = O.decode_loop(drafter, target, run_len, eng.top_k, policy, n_max, dims, P - 1, t_draft, t_aux,
-                                  l_ar)
-    assert list(toks) == list(tokens)
-    for rec, e in zip(records, exported):
-        assert rec["tree_size"] == int(e["meta"][0])
-        assert rec["surrogate"] == e["surrogate"]
-    return records
 
 
 def test_planning_bit_parity_fixed(eng):
@@ -127,22 +87,6 @@ def test_planning_bit_parity_adaptive(eng):
         want = O.controller(e["tok"], e["prob"], 64, O.curve_for(dims, c), 3e-4, 2e-5, l_ar)
         assert np.array(want.trace).tobytes() == e["trace"].tobytes()
         assert want.budget == int(e["meta"][0])
-
-
-def _decoy_drafter(ar, gamma, V, seed):
-    """Test drafter: the target's greedy token competes with decoys so the accepted path is non-contiguous."""
-    rng = np.random.default_rng(seed)
-
-    def fn(e):
-        k = int(e.state[3].item())  # committed so far
-        lg = torch.zeros(gamma, V, device="cuda")
-        for j in range(gamma):
-            dec = int(rng.integers(0, V))
-            lg[j, dec] = 10.3  # a decoy ranked above the target's token
-            if k + j < len(ar):
-                lg[j, ar[k + j]] = 10.0
-        return lg
-    return fn
 
 
 @pytest.mark.parametrize("graphs", [False, True])
@@ -262,3 +206,49 @@ def test_beam_policy_runs_through_the_plugin_protocol(eng):
         recs, toks = P.decode_full(eng, sim, pol, est)
         assert len(toks) >= 20 and all(r.tree_size >= 1 for r in recs)
         assert tuple(eng.tokens())[: len(toks) - recs[-1].accepted_len] == tuple(toks)[: len(toks) - recs[-1].accepted_len]
+
+
+def test_ema_observe_replans_every_cycle(eng):
+    """K7 wiring (sp/cost_model.py:184-189,266-270): every measured verify time goes through
+    ``observe``; the EMA ratio follows ``ema_update`` bit for bit, and each cycle's tree is
+    Algorithm 1 at the ratio its plan was uploaded with (the previous cycle's observation
+    is applied after the next draft: one cycle of lag, engine_decode)."""
+    import paper_2605_29727_b200 as P
+    from paper_2605_29727_b200.engine.config import QWEN3_8B
+    params = QWEN3_8B.cost_params(1649.1e12, 6457.7e9)
+    est = P.VerifyLatencyEstimator(params, variant="ema", bias=P.EmaBias(ratio_bias=1.0, alpha=0.1))
+    l_ar = est.estimate(1, 1000)
+    lat = P.CycleLatencies(t_draft=3e-4, t_aux=2e-5, l_ar=l_ar)
+    prompt = _prompt(60, eng.cfg.V, seed=9)
+    sim = P.SimConfig(controller=P.ControllerConfig(n_max=64, latencies=lat, variant="ema",
+                                                    context_len=len(prompt) - 1), run_length=24, top_k=eng.top_k)
+    plan_ratios, observed = [], []
+    orig_set, orig_obs = eng.set_policy, est.observe
+
+    def set_policy(kind, n=0, estimator=None, latencies=None, n_max=None):
+        plan_ratios.append(estimator.bias.ratio_bias)
+        return orig_set(kind, n=n, estimator=estimator, latencies=latencies, n_max=n_max)
+
+    def observe(s, c, obs):
+        before = est.bias.ratio_bias
+        orig_obs(s, c, obs)
+        observed.append((s, c, obs, before, est.bias.ratio_bias))
+    eng.set_policy, est.observe = set_policy, observe
+    eng.reset(prompt)
+    eng.export = True
+    try:
+        records, toks = P.decode_full(eng, sim, P.Policy.adaptive(), est)
+    finally:
+        eng.export = False
+        del eng.set_policy
+    dims = O.Dims(**{k: getattr(params, k) for k in ("L", "h", "n_q", "n_kv", "d", "h_ffn", "V", "bp")},
+                  peak_flops=params.peak_flops, bandwidth=params.bandwidth)
+    assert len(observed) >= len(records) - 1 and len(records) >= 3
+    for s, c, obs, before, after in observed:  # ema_update arithmetic, bit for bit
+        assert after == O.ema_step(before, 0.1, O.roofline(dims, s, c), obs)
+    assert len({r for r in plan_ratios}) > 1, "the plan never changed"
+    for k, e in enumerate(eng.exported):
+        ratio = plan_ratios[max(0, k - 1)]
+        want = O.controller(e["tok"], e["prob"], 64, O.curve_for(dims, e["c"], "ema", ratio=ratio), 3e-4, 2e-5, l_ar)
+        assert want.budget == int(e["meta"][0]), k
+        assert np.array(want.trace).tobytes() == e["trace"].tobytes(), k

@@ -274,7 +274,13 @@ class ReplayTreePlugin(ReplayPlugin):
         return torch.tensor(am, dtype=torch.int32, device="cuda")
 
 
-@pytest.mark.parametrize("plugin_cls", [ReplayPlugin, ReplayTreePlugin])
+def _target_rule(P, run):
+    """The synthetic pair itself (paper_2605_29727_b200.TargetRule), not a replay."""
+    return P.TargetRule.from_config(P.SyntheticPairConfig(gamma=run["gamma"], vocab_size=run["V"], alignment=0.8,
+                                                          concentration=0.1, seed=run["seed"]))
+
+
+@pytest.mark.parametrize("plugin_cls", [ReplayPlugin, ReplayTreePlugin, _target_rule])
 def test_decode_loop_golden(P, plugin_cls):
     g = load("decode")
     prof = load("controller")["profiles"]["crossover"]
