@@ -40,6 +40,9 @@ typedef struct {
   int64_t bytes_const, bytes_lin, bytes_quad; /* cost_model.py:292-294 */
   double inv_peak, inv_bw;                   /* cost_model.py:295-296 */
   double slope, intercept, ratio;            /* cost_model.py:297-303 */
+  /* Batched verify (extension, 0 for one request): flops of the other requests
+   * verified in the same pass; compute = (flops_const + (lin + quad s) s) / peak. */
+  int64_t flops_const;
 } bst_curve_t;
 
 /* Host-side evaluation of LatencyCurve.latency(s) with the device arithmetic. */
@@ -92,6 +95,10 @@ typedef struct {
   int32_t c_idx;
   int32_t _pad2;
   int64_t d_flops_lin, d_bytes_const, d_bytes_lin;
+  /* Batched verify (extension, 0 for one request): surrogate of the other requests
+   * of the pass; Algorithm 1 scores S_hat = (a_offset + a_hat) * l_ar / C_hat, the
+   * batch's accepted tokens per pass time with the others' trees held fixed.      */
+  double a_offset;
 } bst_plan_t;
 
 /* Output arrays (device), row 0 = root.  Capacity n_cap+1 rows. */
@@ -246,6 +253,17 @@ int bst_attention_keymajor(const void* q, int64_t q_tok_stride, void* out, int64
                            const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
                            bst_stream_t stream);
 
+/* Ragged batched K3 (config 3, per-request adaptive trees): request r's query rows are
+ * q/out rows [row_off[r], row_off[r] + row_cnt[r]) of a packed layout (device arrays,
+ * written by bst_ragged_rows earlier in the same stream); its ancestor-mask rows stay at
+ * anc[(r*s_max + i) * mask_words].  Same semantics as bst_attention_batch otherwise. */
+int bst_attention_ragged(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
+                         int n_layers, int n_pages_total, int layer, const int32_t* page_table, int req_pages, int n_q,
+                         int n_kv, int n_req, int s_max, const int32_t* row_off, const int32_t* row_cnt,
+                         int keys_after_c, int max_keys, const int32_t* state, int req_state, int c_idx, int mode,
+                         const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
+                         bst_stream_t stream);
+
 /* ------------------------------------------------------------------------
  * K5 — fused elementwise epilogues of the target/drafter forward.
  * ---------------------------------------------------------------------- */
@@ -267,11 +285,14 @@ int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* sched, int 
                        const void* q_norm, const void* k_norm, float eps, const float* inv_freq, const int32_t* pos,
                        const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride, void* kv,
                        int64_t layer_off_elems, const int32_t* page_table, int page_size, const int32_t* state,
-                       int state_c_idx, int req_rows, int req_span, int req_state, int req_slots, bst_stream_t stream);
+                       int state_c_idx, int req_rows, int req_span, int req_state, int req_slots,
+                       const int32_t* row_req /* ragged batch: request of each row, < 0 = padding; nullable */,
+                       bst_stream_t stream);
 int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act, int64_t lda,
                bst_stream_t stream);
+/* dst[r] = src[*row_base + idx[r]] for r < *count (row_base nullable: 0), zero rows after. */
 int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx, const int32_t* count, int max_rows, int cols,
-                    void* dst, int64_t ldd, bst_stream_t stream);
+                    void* dst, int64_t ldd, const int32_t* row_base, bst_stream_t stream);
 
 /* ------------------------------------------------------------------------
  * Decode-state plumbing of the on-device loop (no host round trip):
@@ -298,6 +319,30 @@ int bst_drafter_rows_batch(const int32_t* state, int req_state, int n_req, int g
 int bst_commit_state(int32_t* state, const int32_t* accept_meta, const int32_t* committed, int max_path,
                      int32_t* out_tokens, int out_cap, const int32_t* tree_meta, const double* surrogate,
                      int32_t* log_i32, double* log_f64, int log_cap, bst_stream_t stream);
+
+/* ------------------------------------------------------------------------
+ * Ragged batched verify (extension beyond the reference's batch-1 controller,
+ * PAPER.md:686).  Request r verifies s_r = N*_r + 1 rows, packed
+ * request after request.
+ * bst_ragged_rows: row_off/row_cnt [n_req], *total = sum s_r; tokens/pos/slot/row_req
+ *   for rows [0, rows_cap) (root token = state bonus, pos = depth, slot = row in the
+ *   tree; rows >= total: token 0, slot INT32_MIN, row_req -1).
+ * bst_ragged_unpack: dst[r*s_max + i] = src[row_off[r] + i] (i < row_cnt[r]), else -1.
+ * bst_batch_plan: out[r] = base[r] with the batch-aware verify cost: curve.flops_const /
+ *   bytes_const += the other requests' flops / KV + activation bytes at their last tree
+ *   sizes and contexts (weights counted once), a_offset = their surrogates (first != 0:
+ *   no trees yet, every other request counts as its root row, surrogate 1).  One request:
+ *   out == base, i.e. exactly run_cycle (controller.py:56-107).
+ * ---------------------------------------------------------------------- */
+int bst_ragged_rows(const bst_tree_t* trees_dev, const int32_t* state, int req_state, int n_req, int s_max,
+                    int rows_cap, int32_t* row_off, int32_t* row_cnt, int32_t* total, int32_t* tokens, int32_t* pos,
+                    int32_t* slot, int32_t* row_req, bst_stream_t stream);
+int bst_ragged_unpack(const int32_t* src, const int32_t* row_off, const int32_t* row_cnt, int n_req, int s_max,
+                      int32_t* dst, bst_stream_t stream);
+int bst_batch_plan(const bst_plan_t* base_dev, bst_plan_t* out_dev, const bst_tree_t* trees_dev,
+                   const int32_t* state, int req_state, int n_req, int first, bst_stream_t stream);
+/* sizeof of the ABI structs (0 curve, 1 plan, 2 tree, 3 GEMM schedule) for binding checks. */
+int bst_struct_size(int which);
 
 #ifdef __cplusplus
 }

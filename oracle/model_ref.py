@@ -157,6 +157,8 @@ class RefPlugin:
         self.ref, self.prompt = ref, [int(t) for t in prompt]
         self.gamma, self.mask_token, self.top_k, self.tol = gamma, mask_token, top_k, tol
         self.near_ties: list[tuple[str, int]] = []  # (kind, committed length)
+        self.target_gap: dict[int, float] = {}      # committed index -> top-2 gap / max|logit|
+        self.drafter_gap: dict[int, float] = {}     # committed length -> min K/K+1 gap / max|logit|
 
     def drafter_marginals(self, prefix):
         full = self.prompt + [int(t) for t in prefix]
@@ -165,6 +167,7 @@ class RefPlugin:
         lg = self.ref.drafter(feat, c, full[-1], self.gamma, self.mask_token)
         top = lg.topk(self.top_k + 1, dim=-1).values
         scale = lg.abs().amax(-1)
+        self.drafter_gap[len(prefix)] = float(((top[:, self.top_k - 1] - top[:, self.top_k]) / scale).min())
         if bool(((top[:, self.top_k - 1] - top[:, self.top_k]) < self.tol * scale).any()):
             self.near_ties.append(("drafter", len(prefix)))
         return torch.softmax(lg.double(), -1).cpu().numpy()
@@ -176,6 +179,7 @@ class RefPlugin:
         n = len(full)
         lg, _ = self.ref.target(full, list(range(n)), causal_mask(n))
         top = lg[-1].topk(2).values
+        self.target_gap[len(seq)] = float(top[0] - top[1]) / float(lg[-1].abs().max())
         if float(top[0] - top[1]) < self.tol * float(lg[-1].abs().max()):
             self.near_ties.append(("target", len(seq)))
         return int(torch.argmax(lg[-1]))  # first max on ties, as np.argmax (sp/verify_sim.py:107-109)

@@ -256,10 +256,11 @@ class Curve:
     slope: float
     intercept: float
     ratio: float
+    flops_const: int = 0  # batched verify: the other requests' flops (not in the reference)
 
     def latency(self, s: int) -> float:
         """sp/cost_model.py:305-309 — note the reciprocal multiply."""
-        compute = (self.flops_lin + self.flops_quad * s) * s * self.inv_peak
+        compute = (self.flops_const + (self.flops_lin + self.flops_quad * s) * s) * self.inv_peak
         memory = (self.bytes_const + (self.bytes_lin + self.bytes_quad * s) * s) * self.inv_bw
         raw = compute if compute > memory else memory
         return self.ratio * (self.slope * raw + self.intercept)
@@ -327,12 +328,13 @@ class Decision:
 
 
 def controller(tok: np.ndarray, prob: np.ndarray, n_max: int, curve: Curve,
-               t_draft: float, t_aux: float, l_ar: float) -> Decision:
+               t_draft: float, t_aux: float, l_ar: float, a_offset: float = 0.0) -> Decision:
     """Expand best-first and stop at the first strict decrease of S_hat.
 
     Arithmetic order follows sp/controller.py:73-98: fixed = t_draft + t_aux;
     a_hat += rho; c_hat = fixed + curve.latency(n + 1); s_hat = a_hat * l_ar / c_hat.
-    Equal S_hat keeps expanding without moving best_n.
+    Equal S_hat keeps expanding without moving best_n.  ``a_offset`` (batched verify,
+    not in the reference; 0 reproduces it exactly): s_hat = (a_hat + a_offset) * l_ar / c_hat.
     """
     if n_max < 1:
         raise ValueError(f"n_max must be >= 1, got {n_max}")
@@ -345,7 +347,7 @@ def controller(tok: np.ndarray, prob: np.ndarray, n_max: int, curve: Curve,
         rows.append(row)
         n = len(rows)
         a_hat += row[4]
-        s_hat = a_hat * l_ar / (fixed + curve.latency(n + 1))
+        s_hat = (a_hat + a_offset) * l_ar / (fixed + curve.latency(n + 1))
         trace.append(s_hat)
         if s_hat > best_s:
             best_s, best_n, best_a = s_hat, n, a_hat

@@ -24,14 +24,16 @@ class Curve(C.Structure):
 
     _fields_ = [("flops_lin", C.c_int64), ("flops_quad", C.c_int64), ("bytes_const", C.c_int64),
                 ("bytes_lin", C.c_int64), ("bytes_quad", C.c_int64), ("inv_peak", C.c_double),
-                ("inv_bw", C.c_double), ("slope", C.c_double), ("intercept", C.c_double), ("ratio", C.c_double)]
+                ("inv_bw", C.c_double), ("slope", C.c_double), ("intercept", C.c_double), ("ratio", C.c_double),
+                ("flops_const", C.c_int64)]
 
 
 class Plan(C.Structure):
     _fields_ = [("policy", C.c_int32), ("n_max", C.c_int32), ("width", C.c_int32), ("depth", C.c_int32),
                 ("algo", C.c_int32), ("_pad", C.c_int32), ("curve", Curve), ("fixed_cost", C.c_double),
                 ("l_ar", C.c_double), ("state", C.c_void_p), ("c_idx", C.c_int32), ("_pad2", C.c_int32),
-                ("d_flops_lin", C.c_int64), ("d_bytes_const", C.c_int64), ("d_bytes_lin", C.c_int64)]
+                ("d_flops_lin", C.c_int64), ("d_bytes_const", C.c_int64), ("d_bytes_lin", C.c_int64),
+                ("a_offset", C.c_double)]
 
 
 class Tree(C.Structure):
@@ -90,9 +92,15 @@ SIGNATURES = {
     "bst_qkv_rope": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64, _P, _I64,
                           _P, _I, _P, _I, _P]),
     "bst_qkv_rope_batch": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64,
-                                _P, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P]),
+                                _P, _I64, _P, _I, _P, _I, _I, _I, _I, _I, _P, _P]),
     "bst_swiglu": (_I, [_P, C.POINTER(GemmSched), _I, _I, _P, _I64, _P]),
-    "bst_gather_rows": (_I, [_P, _I64, _P, _P, _I, _I, _P, _I64, _P]),
+    "bst_gather_rows": (_I, [_P, _I64, _P, _P, _I, _I, _P, _I64, _P, _P]),
+    "bst_attention_ragged": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _P, _P, _I, _I, _P, _I,
+                                  _I, _I, _P, _I, _I, _P, _SZ, _P]),
+    "bst_ragged_rows": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bst_ragged_unpack": (_I, [_P, _P, _P, _I, _I, _P, _P]),
+    "bst_batch_plan": (_I, [_P, _P, _P, _P, _I, _I, _I, _P]),
+    "bst_struct_size": (_I, [_I]),
     "bst_verify_rows": (_I, [_P, _P, _P, _P, _I, _P, _P, _P, _P]),
     "bst_drafter_rows": (_I, [_P, _I, _I, _I, _P, _P, _P, _P, _P]),
     "bst_drafter_rows_batch": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
@@ -135,7 +143,8 @@ KERNELS_PER_CALL = {
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
     "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_keymajor": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,
-    "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1, "bst_gemm_argmax_keys": 2, "bst_argmax_from_keys": 1, "bst_gemm_sample": 2,
+    "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1, "bst_attention_ragged": 1, "bst_ragged_rows": 1,
+    "bst_ragged_unpack": 1, "bst_batch_plan": 1, "bst_gemm_argmax_keys": 2, "bst_argmax_from_keys": 1, "bst_gemm_sample": 2,
 }
 launch_count = 0
 

@@ -63,10 +63,22 @@ struct AttnArgs {
   // [req * s, req * s + s), page-table entries [req * req_pages, ...), state words
   // [req * req_state, ...) and ws partials [req][split][s * n_q]
   int n_req, req_pages, req_state;
+  // ragged batch (nullable): request req's query rows are q/out rows [row_off[req],
+  // row_off[req] + row_cnt[req]) of a packed layout; masks and partials keep the
+  // uniform [req][s] stride (s = the per-request row capacity)
+  const int32_t* row_off;
+  const int32_t* row_cnt;
   int rows_per_block;      // key-major kernel: query rows per CTA (row blocks balanced over R)
   bst_prefetch_t pf;       // next-GEMM weights to pull into L2 while we run
   int seq;                 // boundary-trace launch number (BST_TRACE builds)
 };
+
+// First packed q/out row of request req, and its query-row count (ragged batches).
+__device__ __forceinline__ int64_t req_row0(const AttnArgs& a, int req) {
+  return a.row_off ? (int64_t)a.row_off[req] : (int64_t)req * a.s;
+}
+__device__ __forceinline__ int req_rows(const AttnArgs& a, int req) { return a.row_cnt ? a.row_cnt[req] : a.s; }
+
 
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
@@ -283,7 +295,7 @@ __device__ void split_merge(const AttnArgs& a, const float* stg, int head, int s
     }
     if (t == 0) TRACE(30, 4);
     const float inv = L > 0.f ? 1.f / L : 0.f;
-    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + d0;
+    __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + d0;
     if constexpr (DI == 8) {
       *reinterpret_cast<uint4*>(op) = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
                                                  pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
@@ -359,7 +371,7 @@ __device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req,
     }
     const float inv = L > 0.f ? 1.f / L : 0.f;
     const int tok = rr / a.group, qh = head * a.group + rr % a.group;
-    __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
+    __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
     *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
   }
 }
@@ -435,7 +447,12 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
   const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
-  const int R = a.group * a.s;
+  int R = a.group * a.s;
+  if (a.row_cnt) {  // ragged batch: the row counts come from an earlier kernel of the graph
+    sm100::grid_dep_wait();
+    R = a.group * req_rows(a, req);
+    if (rb * 128 >= R) return;  // every split of this (head, row block) exits: no barrier waits on it
+  }
   int page0, n_tiles;
   split_pages(a, n_keys, split, page0, n_tiles);
 
@@ -543,7 +560,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     if (threadIdx.x == 64) BND(a.seq, 3);
     if (threadIdx.x == 64) TRACE_MAX(0);
     {  // stage Q row (256 B) into the swizzled K-major tile
-      const int4* src = reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D);
+      const int4* src = reinterpret_cast<const int4*>(a.q + (req_row0(a, req) + tok) * a.q_tok_stride + (int64_t)qh * A_D);
 #pragma unroll
       for (int q = 0; q < 16; ++q) {
         const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
@@ -676,7 +693,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D);
+        uint4* op = reinterpret_cast<uint4*>(a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D);
 #pragma unroll
         for (int q = 0; q < 16; ++q)
           op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
@@ -731,7 +748,12 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
   const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
-  const int R = a.group * a.s;
+  int R = a.group * a.s;
+  if (a.row_cnt) {  // ragged batch: the row counts come from an earlier kernel of the graph
+    sm100::grid_dep_wait();
+    R = a.group * req_rows(a, req);
+    if (rb * 128 >= R) return;  // every split of this (head, row block) exits: no barrier waits on it
+  }
   int page0, n_tiles;
   split_pages(a, n_keys, split, page0, n_tiles);
 
@@ -854,7 +876,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
     if (threadIdx.x == 64) TRACE(31, 2);
     if (threadIdx.x == 64) TRACE_MAX(0);
     {  // each group stages one 64-dim half of the row
-      const int4* src = reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
+      const int4* src = reinterpret_cast<const int4*>(a.q + (req_row0(a, req) + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * g;
 #pragma unroll
       for (int q = 0; q < 8; ++q) {
         const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
@@ -975,12 +997,13 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
     }
     if (a.n_splits > 1 && a.merge) {
+      const int Rws = a.group * a.s;  // the workspace keeps the uniform per-request row stride
       if (valid) {  // unnormalised partial straight to the L2 workspace, coalesced over rows
         const int64_t bse = kt_ws_base(a, req, split, head);
-        float4* op = reinterpret_cast<float4*>(a.ws_o) + (bse * 32 + 16 * g) * R + rg;
+        float4* op = reinterpret_cast<float4*>(a.ws_o) + (bse * 32 + 16 * g) * Rws + rg;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) __stcg(op + (int64_t)q * R, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
-        if (g == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + bse * R + rg, make_float2(M, L));
+        for (int q = 0; q < 16; ++q) __stcg(op + (int64_t)q * Rws, make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]));
+        if (g == 0) __stcg(reinterpret_cast<float2*>(a.ws_ml) + bse * Rws + rg, make_float2(M, L));
       }
       if (threadIdx.x == 64) TRACE(31, 5);
       if (threadIdx.x == 64) TRACE_MAX(1);
@@ -988,7 +1011,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
+        uint4* op = reinterpret_cast<uint4*>(a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * g);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
@@ -1154,7 +1177,12 @@ __global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_con
   const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
   const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
   const int n_keys = c_ctx + a.keys_after_c;
-  const int R = a.group * a.s;
+  int R = a.group * a.s;
+  if (a.row_cnt) {  // ragged batch: the row counts come from an earlier kernel of the graph
+    sm100::grid_dep_wait();
+    R = a.group * req_rows(a, req);
+    if (rb * 128 >= R) return;  // every split of this (head, row block) exits: no barrier waits on it
+  }
   const int row0 = rb * a.rows_per_block;
   const int Rb = min(a.rows_per_block, R - row0);
   int page0, n_pages;
@@ -1280,7 +1308,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_con
         const int rg = row0 + (valid ? row : 0);
         const int tok = rg / a.group, qh = head * a.group + rg % a.group;
         const int4* src =
-            reinterpret_cast<const int4*>(a.q + ((int64_t)req * a.s + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * hq;
+            reinterpret_cast<const int4*>(a.q + (req_row0(a, req) + tok) * a.q_tok_stride + (int64_t)qh * A_D) + 8 * hq;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const int4 v = valid ? src[q] : make_int4(0, 0, 0, 0);
@@ -1526,7 +1554,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_con
     } else if (valid) {
       if (a.n_splits == 1) {
         const float inv = L > 0.f ? 1.f / L : 0.f;
-        uint4* op = reinterpret_cast<uint4*>(a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * h);
+        uint4* op = reinterpret_cast<uint4*>(a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 64 * h);
 #pragma unroll
         for (int q = 0; q < 8; ++q)
           op[q] = make_uint4(pack_bf16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_bf16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
@@ -1583,7 +1611,7 @@ __global__ void __launch_bounds__(KT_THREADS, 1) attn_kt_kernel(const __grid_con
         }
         const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
         const int rg = row0 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
-        __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * cq;
+        __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * cq;
         *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
       }
     }
@@ -1612,6 +1640,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   const int lane = threadIdx.x & 31;
   const int rows = a.s * a.n_q;
   if (row >= rows) return;
+  if (a.row_cnt && row / a.n_q >= req_rows(a, req)) return;  // ragged: past this request's rows
   float M = -INFINITY, L = 0.f;
   float acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int sp0 = 0; sp0 < a.n_splits; sp0 += 4) {
@@ -1648,7 +1677,7 @@ __global__ void attn_combine_kernel(AttnArgs a) {
   }
   const float inv = L > 0.f ? 1.f / L : 0.f;
   const int tok = row / a.n_q, qh = row % a.n_q;
-  __nv_bfloat16* op = a.out + ((int64_t)req * a.s + tok) * a.o_tok_stride + (int64_t)qh * A_D + lane * 4;
+  __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + lane * 4;
   *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   if (blockIdx.x == 0 && threadIdx.x == 0) TRACE(30, 1);
 }
@@ -1693,7 +1722,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
                           int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
                           int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
                           const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes, int n_req,
-                          int req_pages, int req_state, bool keymajor, bst_stream_t stream) {
+                          int req_pages, int req_state, bool keymajor, const int32_t* row_off,
+                          const int32_t* row_cnt, bst_stream_t stream) {
   BST_REQUIRE(q && out && kv_cache && page_table, "null pointer argument");
   BST_REQUIRE(n_req >= 1 && (n_req == 1 || (req_pages >= 1 && (state == nullptr || req_state >= 1))),
               "batched attention needs per-request page and state strides");
@@ -1701,6 +1731,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   BST_REQUIRE(s >= 1 && c >= 0 && keys_after_c >= 0, "bad sizes");
   BST_REQUIRE(mode >= 0 && mode <= 2, "mode must be 0 (tree), 1 (causal) or 2 (full)");
   BST_REQUIRE(mode != 0 || (anc && mask_words * 32 >= keys_after_c), "tree mode needs the ancestor mask");
+  BST_REQUIRE(!row_off == !row_cnt, "ragged batches need both row offsets and row counts");
+  BST_REQUIRE(!row_off || (!keymajor && state), "ragged batches run on the row-major kernels with device contexts");
   if (max_keys < c + keys_after_c) max_keys = c + keys_after_c;
   const int group = n_q / n_kv;
   const int R = group * s;
@@ -1764,6 +1796,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   a.req_pages = req_pages;
   a.req_state = req_state;
   a.rows_per_block = 128;
+  a.row_off = row_off;
+  a.row_cnt = row_cnt;
   a.pf = take_prefetch();
   a.seq = bnd_next_seq();
   cudaStream_t st = as_stream(stream);
@@ -1928,7 +1962,7 @@ extern "C" int bst_attention(const void* q, int64_t q_tok_stride, void* out, int
                              bst_stream_t stream) {
   return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
                              n_q, n_kv, s, c, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
-                             ws, ws_bytes, 1, 0, 0, false, stream);
+                             ws, ws_bytes, 1, 0, 0, false, nullptr, nullptr, stream);
 }
 
 extern "C" int bst_attention_keymajor(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
@@ -1939,7 +1973,7 @@ extern "C" int bst_attention_keymajor(const void* q, int64_t q_tok_stride, void*
                                       bst_stream_t stream) {
   return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
                              n_q, n_kv, s, c, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
-                             ws, ws_bytes, 1, 0, 0, true, stream);
+                             ws, ws_bytes, 1, 0, 0, true, nullptr, nullptr, stream);
 }
 
 extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
@@ -1950,7 +1984,20 @@ extern "C" int bst_attention_batch(const void* q, int64_t q_tok_stride, void* ou
                                    size_t ws_bytes, bst_stream_t stream) {
   return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
                              n_q, n_kv, s, 0, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
-                             ws, ws_bytes, n_req, req_pages, req_state, false, stream);
+                             ws, ws_bytes, n_req, req_pages, req_state, false, nullptr, nullptr, stream);
+}
+
+extern "C" int bst_attention_ragged(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride,
+                                    const void* kv_cache, int n_layers, int n_pages_total, int layer,
+                                    const int32_t* page_table, int req_pages, int n_q, int n_kv, int n_req,
+                                    int s_max, const int32_t* row_off, const int32_t* row_cnt, int keys_after_c,
+                                    int max_keys, const int32_t* state, int req_state, int c_idx, int mode,
+                                    const uint32_t* anc, int mask_words, int n_splits, float* ws, size_t ws_bytes,
+                                    bst_stream_t stream) {
+  BST_REQUIRE(row_off && row_cnt, "null row offsets / counts");
+  return bst::attention_impl(q, q_tok_stride, out, o_tok_stride, kv_cache, n_layers, n_pages_total, layer, page_table,
+                             n_q, n_kv, s_max, 0, keys_after_c, max_keys, state, c_idx, mode, anc, mask_words, n_splits,
+                             ws, ws_bytes, n_req, req_pages, req_state, false, row_off, row_cnt, stream);
 }
 
 extern "C" size_t bst_attention_workspace(int n_q, int s, int n_splits) {  // two banks of partials

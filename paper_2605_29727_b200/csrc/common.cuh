@@ -50,7 +50,7 @@ __device__ __forceinline__ T warp_sum(T v) {
 // LatencyCurve.latency (cost_model.py:305-309) with round-to-nearest and no
 // contraction, matching Python's int->float conversion and float arithmetic.
 __host__ __device__ inline double curve_latency(const bst_curve_t& c, long long s) {
-  long long f = (c.flops_lin + c.flops_quad * s) * s;
+  long long f = c.flops_const + (c.flops_lin + c.flops_quad * s) * s;
   long long b = c.bytes_const + (c.bytes_lin + c.bytes_quad * s) * s;
 #ifdef __CUDA_ARCH__
   double compute = __dmul_rn(__ll2double_rn(f), c.inv_peak);

@@ -199,11 +199,12 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
 // ------------------------------------------------------------ gather rows
 __global__ void gather_rows_kernel(const __nv_bfloat16* __restrict__ src, int64_t lds, const int32_t* __restrict__ idx,
                                    const int32_t* __restrict__ count, int max_rows, int cols,
-                                   __nv_bfloat16* __restrict__ dst, int64_t ldd) {
+                                   __nv_bfloat16* __restrict__ dst, int64_t ldd, const int32_t* __restrict__ row_base) {
   pdl_enter();
   const int r = blockIdx.x;
   const int n = count ? *count : max_rows;
-  const int4* sp = reinterpret_cast<const int4*>(src + (int64_t)(r < n ? idx[r] : 0) * lds);
+  const int64_t base = row_base ? *row_base : 0;
+  const int4* sp = reinterpret_cast<const int4*>(src + (base + (r < n ? idx[r] : 0)) * lds);
   int4* dp = reinterpret_cast<int4*>(dst + (int64_t)r * ldd);
   for (int i = threadIdx.x; i < cols / 8; i += blockDim.x) dp[i] = r < n ? sp[i] : make_int4(0, 0, 0, 0);
 }
@@ -244,7 +245,7 @@ RopeArgs make_rope_args(int n_q, int n_kv, const void* q_norm, const void* k_nor
                         const int32_t* pos, const int32_t* slot, const int32_t* qrow, void* q_out, int64_t q_tok_stride,
                         void* kv, int64_t layer_off_elems, const int32_t* page_table, int page_size,
                         const int32_t* state, int state_c_idx, int req_rows, int req_span, int req_state,
-                        int req_slots) {
+                        int req_slots, const int32_t* row_req) {
   RopeArgs r;
   r.n_q = n_q;
   r.n_kv = n_kv;
@@ -267,6 +268,7 @@ RopeArgs make_rope_args(int n_q, int n_kv, const void* q_norm, const void* k_nor
   r.req_span = req_span > 0 ? req_span : 1;
   r.req_state = req_state;
   r.req_slots = req_slots;
+  r.row_req = row_req;
   return r;
 }
 }  // namespace bst
@@ -276,13 +278,13 @@ extern "C" int bst_qkv_rope_batch(const float* partial, const bst_gemm_sched_t* 
                                   const int32_t* pos, const int32_t* slot, const int32_t* qrow, void* q_out,
                                   int64_t q_tok_stride, void* kv, int64_t layer_off_elems, const int32_t* page_table,
                                   int page_size, const int32_t* state, int state_c_idx, int req_rows, int req_span,
-                                  int req_state, int req_slots, bst_stream_t stream) {
+                                  int req_state, int req_slots, const int32_t* row_req, bst_stream_t stream) {
   BST_REQUIRE(partial && sched && q_norm && k_norm && inv_freq && pos && slot && q_out && kv && page_table,
               "null pointer argument");
   BST_REQUIRE(sched->n_out == (n_q + 2 * n_kv) * 128, "qkv width mismatch (head_dim must be 128)");
   const RopeArgs ra = make_rope_args(n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, q_tok_stride,
                                      kv, layer_off_elems, page_table, page_size, state, state_c_idx, req_rows,
-                                     req_span, req_state, req_slots);
+                                     req_span, req_state, req_slots, row_req);
   bst_gemm_sched_t s = *sched;
   s.reserved = bnd_next_seq();
   BST_CUDA(launch_pdl(qkv_rope_kernel, dim3(rows, (n_q + 2 * n_kv + 15) / 16), dim3(512), 0, as_stream(stream),
@@ -298,7 +300,7 @@ extern "C" int bst_qkv_rope(const float* partial, const bst_gemm_sched_t* sched,
                             int state_c_idx, bst_stream_t stream) {
   return bst_qkv_rope_batch(partial, sched, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out,
                             q_tok_stride, kv, layer_off_elems, page_table, page_size, state, state_c_idx, 0, 1, 0, 0,
-                            stream);
+                            nullptr, stream);
 }
 
 extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, int rows, int ffn, void* act,
@@ -315,11 +317,12 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
 }
 
 extern "C" int bst_gather_rows(const void* src, int64_t lds, const int32_t* idx, const int32_t* count, int max_rows,
-                               int cols, void* dst, int64_t ldd, bst_stream_t stream) {
+                               int cols, void* dst, int64_t ldd, const int32_t* row_base, bst_stream_t stream) {
   BST_REQUIRE(src && idx && dst, "null pointer argument");
   BST_REQUIRE(cols % 8 == 0 && lds % 8 == 0 && ldd % 8 == 0, "rows must be 16-byte multiples");
   BST_CUDA(launch_pdl(gather_rows_kernel, dim3(max_rows), dim3(256), 0, as_stream(stream), static_cast<const __nv_bfloat16*>(src), lds, idx, count,
-                                                              max_rows, cols, static_cast<__nv_bfloat16*>(dst), ldd));
+                                                              max_rows, cols, static_cast<__nv_bfloat16*>(dst), ldd,
+                                                              row_base));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -496,7 +496,7 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
     double* shat = out.trace ? out.trace : ws.shat;
     for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
       double c_hat = __dadd_rn(plan.fixed_cost, curve_latency(plan.curve, (long long)i + 2));
-      shat[i] = __ddiv_rn(__dmul_rn(ws.ahat[i], plan.l_ar), c_hat);
+      shat[i] = __ddiv_rn(__dmul_rn(__dadd_rn(ws.ahat[i], plan.a_offset), plan.l_ar), c_hat);
     }
     if (threadIdx.x == 0) { sm.min_stop = 0x7fffffff; }
     __syncthreads();

@@ -26,11 +26,16 @@ struct RopeArgs {
   const int32_t* state;     // c = state[r * req_state + c_idx] (nullptr: c = 0)
   int c_idx;
   int req_rows, req_span, req_state, req_slots;  // batched requests (req_rows = 0: one request)
+  const int32_t* row_req;   // ragged batch: request of each row (< 0: padding row); overrides req_rows
 };
 
 // This warp's lane holds dims 4 lane .. 4 lane + 3 of head `hd` for token row t in v.
 __device__ __forceinline__ void rope_store_head(const RopeArgs& a, int t, int hd, float (&v)[4], int lane) {
-  const int r = a.req_rows > 0 ? (t % a.req_span) / a.req_rows : 0;
+  int r = a.req_rows > 0 ? (t % a.req_span) / a.req_rows : 0;
+  if (a.row_req) {
+    r = a.row_req[t];
+    if (r < 0) return;  // padding row of a ragged batch: no q, no K/V
+  }
   const int c0 = a.state ? a.state[r * a.req_state + a.c_idx] : 0;
   const bool is_q = hd < a.n_q, is_k = !is_q && hd < a.n_q + a.n_kv;
   const int qr = a.qrow ? a.qrow[t] : t;

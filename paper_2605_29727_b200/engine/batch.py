@@ -92,7 +92,8 @@ class BatchEngine:
         slots = n_req * self.req_pages * PAGE
         self.tw = TargetWeights.random(cfg, seed, dev)
         self.dw = DrafterWeights.random(cfg, self.dcfg, len(feat), seed, dev)
-        self.target = TargetModel(cfg, self.tw, slots, max(MAX_ROWS, self.chunk_v * self.S), feat, dev)
+        self.rows_cap = n_req * self.S  # ragged verify: every request's tree packed in one forward
+        self.target = TargetModel(cfg, self.tw, slots, max(MAX_ROWS, self.chunk_v * self.S, self.rows_cap), feat, dev)
         self.drafter = DrafterModel(cfg, self.dcfg, self.dw, self.tw, slots, len(feat), dev, n_req_max=self.chunk_d)
         i32 = dict(dtype=torch.int32, device=dev)
         self.state = torch.zeros(n_req, 8, **i32)
@@ -113,18 +114,37 @@ class BatchEngine:
         self.log_i32 = torch.zeros(n_req, max_cycles * 8, **i32)
         self.log_f64 = torch.zeros(n_req, max_cycles, dtype=torch.float64, device=dev)
         self.plan_dev = torch.zeros(n_req, C.sizeof(_lib.Plan), dtype=torch.uint8, device=dev)
+        self.plan_base = torch.zeros_like(self.plan_dev)  # adaptive: per-request plans before the batch shift
+        self.row_off = torch.zeros(n_req, **i32)
+        self.row_cnt = torch.zeros(n_req, **i32)
+        self.row_total = torch.zeros(1, **i32)
+        self.row_req = torch.zeros(self.rows_cap, **i32)
+        self.argmax_u = torch.zeros(n_req * self.S, **i32)  # per-request [S] argmax for the K6 walk
+        self.total_host = torch.zeros(1, dtype=torch.int32).pin_memory()
+        self.graph_d = None
+        self.graphs_v: dict[int, torch.cuda.CUDAGraph] = {}
         self.policy = _lib.POLICY_FIXED
         self.set_policy("fixed")
         self.stream = torch.cuda.Stream(dev)
         self.graph = None
         self.graph_kernels = 0
+        self.graph_nodes: dict[int, int] = {}
+        self.last_rows = 0
         self.use_graphs = True
         self._c_bound = 0
         torch.cuda.synchronize()
 
     def set_policy(self, kind: str, estimator=None, latencies=None) -> None:
-        """Per-request K2 plans: fixed-N (N = n_fixed) or adaptive Algorithm 1 with N_max = n_fixed,
-        each request reading its own context length from its state row (independent controllers)."""
+        """Per-request K2 plans: fixed-N (N = n_fixed), or adaptive Algorithm 1 with N_max = n_fixed
+        and a batch-aware verify cost (each request reads its own context from its state row).
+
+        Adaptive (the reference controller is batch-1): the
+        requests' trees are verified together in one ragged pass (rows packed, no padding),
+        whose cost is the weights once plus every request's rows.  Before each cycle
+        ``bst_batch_plan`` shifts request r's curve by the other requests' flops and bytes
+        at their last tree sizes and scores S_hat with the batch's surrogate (a_offset), so
+        each request's K2 is Algorithm 1 against the batch it is verified in — the best
+        response for the batch's tokens per pass; with one request it is run_cycle exactly."""
         if kind == "fixed":
             plans = [_lib.Plan(policy=_lib.POLICY_FIXED, n_max=self.N) for _ in range(self.n_req)]
             self.policy = _lib.POLICY_FIXED
@@ -143,7 +163,13 @@ class BatchEngine:
             raise ValueError(f"unsupported batch policy {kind!r}")
         raw = b"".join(bytes(pl) for pl in plans)
         self.plan_dev.copy_(torch.frombuffer(bytearray(raw), dtype=torch.uint8).view(self.n_req, -1))
-        self.graph = None  # the policy is a launch parameter of K2
+        self.plan_base.copy_(self.plan_dev)
+        if kind == "adaptive":
+            with torch.cuda.stream(self.stream):
+                ops.batch_plan(self.plan_base, self.plan_dev, self.trees_dev, self.state, self.n_req, first=True)
+            self.stream.synchronize()
+        self.graph = self.graph_d = None  # the policy is a launch parameter of K2
+        self.graphs_v = {}
 
     def set_attention_splits(self, n: int) -> None:
         """Pin the K3 split count of both models (0 = automatic); parity tests use 1."""
@@ -184,12 +210,16 @@ class BatchEngine:
                 st.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
         self.stream.synchronize()
         self._c_bound = int(self.contexts().max())
+        if self.policy == _lib.POLICY_ADAPTIVE:  # first plans against the new contexts
+            with torch.cuda.stream(self.stream):
+                ops.batch_plan(self.plan_base, self.plan_dev, self.trees_dev, self.state, self.n_req, first=True)
+            self.stream.synchronize()
 
     # ------------------------------------------------------------------ cycle
-    def _cycle_body(self) -> None:
-        G1, S, rp, n_req = self.G1, self.S, self.req_pages, self.n_req
-        t, d = self.target, self.drafter
-        # phase 1: draft every request (chunks of chunk_d), K1 over all block rows, K2 per request
+    def _draft_phase(self) -> None:
+        """Draft every request (chunks of chunk_d), K1 over all block rows, K2 per request."""
+        G1, rp, n_req = self.G1, self.req_pages, self.n_req
+        d = self.drafter
         for r0 in range(0, n_req, self.chunk_d):
             n = min(self.chunk_d, n_req - r0)
             logits = d.forward_batch(self.state[r0:r0 + n], n, self._dpt(r0), rp,
@@ -199,6 +229,24 @@ class BatchEngine:
         # block row 0 of each request is the bonus position: request r's lattice is rows r*G1+1 ..
         expand_device_plan_batch(self.lat_tok[1:], self.lat_prob[1:], G1 * self.top_k, self.gamma, self.plan_dev,
                                  self.policy, self.N, self.trees, self.trees_dev)
+
+    def _accept_commit(self, r: int, argmax: torch.Tensor, feat_rows: torch.Tensor, row_base=None) -> None:
+        """K6 walk, KV compaction, drafter feature gather and state update of request r."""
+        t, tr, G1 = self.target, self.trees[r], self.G1
+        accept_device(tr.token, tr.child_start, tr.child_list, argmax, G1, self.path[r], self.committed[r],
+                      self.acc_meta[r])
+        kv = t.kv
+        ops.kv_compact(kv.buf, self.cfg.L, self.cfg.n_kv, PAGE, kv.layer_stride, self._pt(r), self.state[r],
+                       self.path[r], self.acc_meta[r], G1)
+        ops.gather_rows(feat_rows, self.path[r], self.acc_meta[r], G1, self.feat[r * G1:(r + 1) * G1], row_base)
+        ops.commit_state(self.state[r], self.acc_meta[r], self.committed[r], G1, self.out_tokens[r], tr.meta,
+                         tr.surrogate, self.log_i32[r], self.log_f64[r])
+
+    def _cycle_body(self) -> None:
+        """Fixed budget: one static-shape cycle (every tree has N nodes)."""
+        S, rp, n_req = self.S, self.req_pages, self.n_req
+        t = self.target
+        self._draft_phase()
         # phase 2: verify every request (chunks of chunk_v), then accept / compact / gather / commit
         for r0 in range(0, n_req, self.chunk_v):
             n = min(self.chunk_v, n_req - r0)
@@ -209,31 +257,79 @@ class BatchEngine:
             t.forward(n * S, self.state[r0:r0 + n], MODE_TREE, keys_after_c=S, anc=self.anc[r0:r0 + n],
                       mask_words=self.mask_words, head="argmax", pt=self._pt(r0), batch=(n, S, rp))
             for i in range(n):
-                r = r0 + i
-                tr = self.trees[r]
-                accept_device(tr.token, tr.child_start, tr.child_list, t.argmax[i * S:(i + 1) * S], G1,
-                              self.path[r], self.committed[r], self.acc_meta[r])
-                kv = t.kv
-                ops.kv_compact(kv.buf, self.cfg.L, self.cfg.n_kv, PAGE, kv.layer_stride, self._pt(r), self.state[r],
-                               self.path[r], self.acc_meta[r], G1)
-                ops.gather_rows(t.feat[i * S:(i + 1) * S], self.path[r], self.acc_meta[r], G1,
-                                self.feat[r * G1:(r + 1) * G1])
-                ops.commit_state(self.state[r], self.acc_meta[r], self.committed[r], G1, self.out_tokens[r],
-                                 tr.meta, tr.surrogate, self.log_i32[r], self.log_f64[r])
+                self._accept_commit(r0 + i, t.argmax[i * S:(i + 1) * S], t.feat[i * S:(i + 1) * S])
+
+    # ------------------------------------------------ adaptive: ragged verify
+    def _draft_ragged(self) -> None:
+        """Draft + K2 (batch-aware plans), then the packed verify row layout of this cycle."""
+        t = self.target
+        self._draft_phase()
+        ops.ragged_rows(self.trees_dev, self.state, self.n_req, self.S, self.rows_cap, self.row_off, self.row_cnt,
+                        self.row_total, t.tokens, t.pos, t.slot, self.row_req)
+
+    def _verify_ragged(self, rows: int) -> None:
+        """One target pass over the packed trees of every request (rows = the 64-row bucket of
+        the total), per-request accept / compaction / commit, next cycle's batch-aware plans."""
+        t, S, n = self.target, self.S, self.n_req
+        t.forward(rows, self.state, MODE_TREE, keys_after_c=S, anc=self.anc, mask_words=self.mask_words,
+                  head="argmax", pt=self._pt(0),
+                  ragged=(n, S, self.req_pages, self.row_req, self.row_off, self.row_cnt))
+        ops.ragged_unpack(t.argmax, self.row_off, self.row_cnt, n, S, self.argmax_u)
+        for r in range(n):
+            self._accept_commit(r, self.argmax_u[r * S:(r + 1) * S], t.feat, self.row_off[r:r + 1])
+        ops.batch_plan(self.plan_base, self.plan_dev, self.trees_dev, self.state, n, first=False)
+
+    def _cycle_adaptive(self) -> int:
+        """Graph D (draft + K2 + row layout) -> one host read of the packed row total ->
+        graph V of its 64-row bucket.  Returns the total verified rows."""
+        st = self.stream
+        if not self.use_graphs:
+            with torch.cuda.stream(st):
+                self._draft_ragged()
+        else:
+            if self.graph_d is None:
+                self.graph_d = self._capture_fn(self._draft_ragged)
+            with torch.cuda.stream(st):
+                self.graph_d.replay()
+        with torch.cuda.stream(st):
+            self.total_host.copy_(self.row_total, non_blocking=True)
+        st.synchronize()
+        total = int(self.total_host[0])
+        rows = min(self.rows_cap, -(-total // 64) * 64)
+        if not self.use_graphs:
+            with torch.cuda.stream(st):
+                self._verify_ragged(rows)
+            return total
+        g = self.graphs_v.get(rows)
+        if g is None:
+            g = self.graphs_v[rows] = self._capture_fn(lambda: self._verify_ragged(rows))
+        with torch.cuda.stream(st):
+            g.replay()
+        return total
 
     def _capture(self) -> torch.cuda.CUDAGraph:
-        saved = self.state.clone()
+        g = self._capture_fn(self._cycle_body)
+        self.graph_kernels = self.graph_nodes[id(g)]
+        return g
+
+    def _capture_fn(self, fn) -> torch.cuda.CUDAGraph:
+        # warm-up run outside the graph (workspaces, tensor maps, kernel attributes), then
+        # capture; every mutable decode buffer is restored so the capture changes nothing
+        keep = [self.state, self.plan_dev, self.out_tokens, self.log_i32, self.log_f64, self.feat]
+        saved = [x.clone() for x in keep]
         with torch.cuda.stream(self.stream):
-            self._cycle_body()  # warm-up: workspaces, tensor maps, kernel attributes
+            fn()
         self.stream.synchronize()
-        self.state.copy_(saved)
+        for x, y in zip(keep, saved):
+            x.copy_(y)
         g = torch.cuda.CUDAGraph(keep_graph=True)
         with torch.cuda.graph(g, stream=self.stream):
-            self._cycle_body()
-        self.graph_kernels = graph_kernel_nodes(g)
+            fn()
+        self.graph_nodes[id(g)] = graph_kernel_nodes(g)
         g.instantiate()
         self.stream.synchronize()
-        self.state.copy_(saved)
+        for x, y in zip(keep, saved):
+            x.copy_(y)
         torch.cuda.synchronize()
         return g
 
@@ -249,6 +345,9 @@ class BatchEngine:
                 raise RuntimeError(f"KV cache full: a request's context {self._c_bound} + {self.S} verify rows "
                                    f"exceeds max_ctx={self.max_ctx}")
         self._c_bound += self.G1
+        if self.policy == _lib.POLICY_ADAPTIVE:
+            self.last_rows = self._cycle_adaptive()
+            return
         if not self.use_graphs:
             with torch.cuda.stream(self.stream):
                 self._cycle_body()

@@ -353,6 +353,7 @@ class B200Engine:
         return out
 
     def tokens(self) -> list[int]:
+        self.stream.synchronize()  # the last verify graph runs asynchronously on the engine stream
         n = int(self.state[ST_COMMITTED].item())
         return self.out_tokens[:n].cpu().tolist()
 

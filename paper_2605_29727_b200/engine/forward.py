@@ -147,15 +147,17 @@ class TargetModel:
 
     def forward(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None, mask_words: int = 0,
                 head: str | None = "argmax", c_host: int = 0, pt: torch.Tensor | None = None,
-                batch: tuple[int, int, int] | None = None) -> None:
+                batch: tuple[int, int, int] | None = None, ragged: tuple | None = None) -> None:
         """Run `rows` query rows (tokens/pos/slot buffers already filled, relative to c = state[0]).
 
         pt: page-table view (a request's page range in a shared pool; default the whole table).
         batch = (n_req, S, req_pages): rows are n_req requests of S rows each; request r's
-        state is state[r] (8 words), its pages pt[r*req_pages:], its mask rows anc[r*S:]."""
+        state is state[r] (8 words), its pages pt[r*req_pages:], its mask rows anc[r*S:].
+        ragged = (n_req, S, req_pages, row_req, row_off, row_cnt): packed rows of variable
+        per-request counts (device arrays from bst_ragged_rows); masks keep the S stride."""
         cfg, w, kv = self.cfg, self.w, self.kv
         n, eps = rows, cfg.eps
-        if head == "sample" and batch is not None:
+        if head == "sample" and (batch is not None or ragged is not None):
             # bst_gemm_sample keys every row by one state's context c (ADVICE r1)
             raise ValueError("sampled verification is per request: the batched head supports argmax only")
         pt = kv.page_table if pt is None else pt
@@ -170,14 +172,22 @@ class TargetModel:
                 if "rope" in _ABLATE:
                     ops.gemm_partial(x[r0:r1], lw.qkv, out=self.partial)
                     continue
-                req = (0, 1, 0, 0) if batch is None else (batch[1], batch[0] * batch[1], state.stride(0),
-                                                          batch[2] * PAGE)
+                req, row_req = (0, 1, 0, 0), None
+                if batch is not None:
+                    req = (batch[1], batch[0] * batch[1], state.stride(0), batch[2] * PAGE)
+                elif ragged is not None:
+                    req, row_req = (0, 1, state.stride(0), ragged[2] * PAGE), ragged[3][r0:]
                 ops.gemm_qkv_rope(x[r0:r1], lw.qkv, self.partial, cfg.n_q, cfg.n_kv, lw.q_norm, lw.k_norm,
                                   eps, self.inv_freq, self.pos[r0:], self.slot[r0:], None, self.q[r0:], kv.buf,
-                                  li * kv.layer_stride, pt, PAGE, state, req)
+                                  li * kv.layer_stride, pt, PAGE, state, req, row_req)
             if "attn" not in _ABLATE:
                 _pf("o", (lw.o, lw.o.numel() * 2), (lw.gate_up, 32 * MB) if "gate_up" in _PREFETCH else None)
-                if batch is None:
+                if ragged is not None:
+                    nr, S, rp, _, off, cnt = ragged
+                    ops.attention_ragged(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, rp, cfg.n_q,
+                                         cfg.n_kv, nr, S, off, cnt, S, rp * PAGE, state, state.stride(0), mode, anc,
+                                         mask_words, self.attn_ws, n_splits=self.attn_splits)
+                elif batch is None:
                     ops.attention(self.q[:n], self.attn[:n], kv.buf, cfg.L, kv.n_pages, li, pt, cfg.n_q,
                                   cfg.n_kv, n, c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words,
                                   self.attn_ws, n_splits=self.attn_splits)

@@ -134,14 +134,14 @@ def residual_rmsnorm(p: PartialOut | None, resid, rows, h, w, eps, x=None, feat=
 
 
 def gemm_qkv_rope(x, w, out, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv,
-                  layer_off, page_table, page_size, state, req=(0, 1, 0, 0)) -> None:
+                  layer_off, page_table, page_size, state, req=(0, 1, 0, 0), row_req=None) -> None:
     """q/k/v projection (K4) then q/k RMSNorm + RoPE + q and paged-KV stores (K5 qkv_rope)
     of the m = x.shape[0] rows.  (A variant fusing the epilogue into the GEMM's stream-K
     tile fixup was measured slower: it raised the GEMM to 168 registers, which blocks the
     PDL co-residency of the epilogue kernels, and serialised one head x all rows per CTA.)"""
     p = gemm_partial(x, w, out=out)
     qkv_rope_batch(p, x.shape[0], n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv, layer_off,
-                   page_table, page_size, state, *req)
+                   page_table, page_size, state, *req, row_req=row_req)
 
 
 def qkv_rope(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv, layer_off,
@@ -153,11 +153,11 @@ def qkv_rope(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos,
 
 
 def qkv_rope_batch(p: PartialOut, rows, n_q, n_kv, q_norm, k_norm, eps, inv_freq, pos, slot, qrow, q_out, kv,
-                   layer_off, page_table, page_size, state, req_rows, req_span, req_state, req_slots):
+                   layer_off, page_table, page_size, state, req_rows, req_span, req_state, req_slots, row_req=None):
     _lib.call("bst_qkv_rope_batch", p.buf.data_ptr(), C.byref(p.sched), rows, n_q, n_kv, q_norm.data_ptr(),
               k_norm.data_ptr(), C.c_float(eps), inv_freq.data_ptr(), pos.data_ptr(), slot.data_ptr(), _p(qrow),
               q_out.data_ptr(), q_out.stride(0), kv.data_ptr(), layer_off, page_table.data_ptr(), page_size,
-              _p(state), 0, req_rows, req_span, req_state, req_slots, stream_ptr())
+              _p(state), 0, req_rows, req_span, req_state, req_slots, _p(row_req), stream_ptr())
 
 
 def swiglu(p: PartialOut, rows, ffn, act):
@@ -165,9 +165,35 @@ def swiglu(p: PartialOut, rows, ffn, act):
               stream_ptr())
 
 
-def gather_rows(src, idx, count, max_rows, dst):
+def gather_rows(src, idx, count, max_rows, dst, row_base=None):
+    """dst[r] = src[row_base + idx[r]] for r < count (row_base: a device int32, default 0)."""
     _lib.call("bst_gather_rows", src.data_ptr(), src.stride(0), idx.data_ptr(), _p(count), max_rows, src.shape[1],
-              dst.data_ptr(), dst.stride(0), stream_ptr())
+              dst.data_ptr(), dst.stride(0), _p(row_base), stream_ptr())
+
+
+def attention_ragged(q, out, kv, n_layers, n_pages, layer, page_table, req_pages, n_q, n_kv, n_req, s_max, row_off,
+                     row_cnt, keys_after_c, max_keys, state, req_state, mode, anc, mask_words, ws=None, n_splits=0):
+    """Ragged batched K3: request r's rows are q/out rows [row_off[r], row_off[r] + row_cnt[r])."""
+    _lib.call("bst_attention_ragged", q.data_ptr(), q.stride(0), out.data_ptr(), out.stride(0), kv.data_ptr(),
+              n_layers, n_pages, layer, page_table.data_ptr(), req_pages, n_q, n_kv, n_req, s_max, row_off.data_ptr(),
+              row_cnt.data_ptr(), keys_after_c, max_keys, state.data_ptr(), req_state, 0, mode, _p(anc), mask_words,
+              n_splits, _p(ws), 0 if ws is None else ws.numel() * 4, stream_ptr())
+
+
+def ragged_rows(trees_dev, state, n_req, s_max, rows_cap, row_off, row_cnt, total, tokens, pos, slot, row_req):
+    _lib.call("bst_ragged_rows", trees_dev.data_ptr(), state.data_ptr(), state.stride(0), n_req, s_max, rows_cap,
+              row_off.data_ptr(), row_cnt.data_ptr(), total.data_ptr(), tokens.data_ptr(), pos.data_ptr(),
+              slot.data_ptr(), row_req.data_ptr(), stream_ptr())
+
+
+def ragged_unpack(src, row_off, row_cnt, n_req, s_max, dst):
+    _lib.call("bst_ragged_unpack", src.data_ptr(), row_off.data_ptr(), row_cnt.data_ptr(), n_req, s_max,
+              dst.data_ptr(), stream_ptr())
+
+
+def batch_plan(base, out, trees_dev, state, n_req, first):
+    _lib.call("bst_batch_plan", base.data_ptr(), out.data_ptr(), trees_dev.data_ptr(), state.data_ptr(),
+              state.stride(0), n_req, int(first), stream_ptr())
 
 
 def kv_compact(kv, n_layers, n_kv, page_size, layer_stride, page_table, state, path, meta, max_path):

@@ -27,6 +27,14 @@ def test_library_exports_every_declared_symbol():
     assert lib.bst_abi_version() == 1
 
 
+def test_ctypes_struct_layouts_match_the_library():
+    import ctypes as C
+
+    from paper_2605_29727_b200 import _lib
+    for which, struct in enumerate((_lib.Curve, _lib.Plan, _lib.Tree, _lib.GemmSched)):
+        assert _lib.lib().bst_struct_size(which) == C.sizeof(struct), struct.__name__
+
+
 def test_host_curve_matches_reference_golden():
     from paper_2605_29727_b200 import _lib
     g = load("cost_model")
