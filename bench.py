@@ -33,6 +33,14 @@ WORKLOAD = ("config2: Qwen3-8B-shape target + DFlash-style 5-layer block drafter
             "per GPU, 2048-token context, gamma 16, top-K 8, adaptive budget (Algorithm 1, N_max 1024)")
 
 
+_T0 = time.time()
+
+
+def _log(msg: str) -> None:
+    """Phase progress on stderr (the JSON line stays alone on stdout)."""
+    print(f"[bench {time.time() - _T0:7.1f}s] {msg}", file=sys.stderr, flush=True)
+
+
 def load_peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -360,6 +368,7 @@ def run_ours(args) -> None:
         torch.cuda.cudart().cudaProfilerStop()
         return
     # ---- K7: measure l_ar / t_draft, static calibration of the verify roofline
+    _log('K7')
     l_ar = eng.measure_ar_step()
     calib = []
     for n in (15, 47, 95, 159, 255, 511):
@@ -387,6 +396,7 @@ def run_ours(args) -> None:
             eng.set_policy("fixed", n=int(args.policy.split("-")[1]))
 
     # ---- device-timed decode (inputs resident, graphs)
+    _log('device-timed decode')
     eng.reset(prompt)
     set_policy()
     for _ in range(args.warmup):
@@ -424,6 +434,7 @@ def run_ours(args) -> None:
     gpu_launches = sum(kd + kv[b] for b in buckets)  # exact: nodes of the graphs replayed in the timed region
 
     # ---- step-level and decode-level rooflines of the timed cycles
+    _log('step-level and decode-level rooflines of the timed cycles')
     bw, pk = peaks["hbm_gbs"] * 1e9, peaks["bf16_tflops"] * 1e12
     v_roof = [max(step_bytes(pdict, st.tree_size + 1, st.context) / bw,
                   step_flops(pdict, st.tree_size + 1, st.context) / pk) for st in stats]
@@ -443,6 +454,7 @@ def run_ours(args) -> None:
                                   "activations, no score matrix; time roof = max(bytes/BW, flops/peak)"}
 
     # ---- cycles exported for the CPU reference replay (same inputs as the GPU)
+    _log('cycles exported for the CPU reference replay')
     exported = []
     if rank == 0 and world == 1 and not args.no_cpu:
         eng.reset(prompt)
@@ -456,6 +468,7 @@ def run_ours(args) -> None:
         eng.exported = []
 
     # ---- e2e: the public API, same estimator as the timed region; prompt upload + prefill inside
+    _log('e2e')
     sim = P.SimConfig(controller=P.ControllerConfig(n_max=1024, latencies=lat, variant="static",
                                                     context_len=args.context), run_length=args.e2e_cycles,
                       top_k=8)
@@ -470,6 +483,7 @@ def run_ours(args) -> None:
     e2e_val = reduce_throughput(e2e_time, float(e2e_tokens))[2]
 
     # ---- dominant kernel (K4) and K3 probes
+    _log('dominant kernel')
     s_med = int(statistics.median(buckets))
     gemm = gemm_replay_roofline(eng, cfg, peaks, s_med)
     attn = attn2k = None
@@ -478,6 +492,7 @@ def run_ours(args) -> None:
         attn = attention_roofline(peaks, 32768, 17)
 
     # ---- CPU baseline (rank 0, N=1 only): the reference decode over the GPU's own cycles
+    _log('CPU baseline')
     cpu = cpu3 = None
     if exported:
         from oracle import ref_replay as R
@@ -493,6 +508,7 @@ def run_ours(args) -> None:
                "trees_match_gpu": True, **R.host_info()}
         del exported
         if not args.no_cpu3:
+            _log("config 3 CPU process-pool leg")
             c3 = R.process_pool_streams(args.c3_requests, 2, pdict, latd, args.context, 1024)
             cpu3 = {"value": c3["tokens_per_s_wall"], "unit": "tokens/s", "cores": c3["workers"], "kind": c3["kind"],
                     "sample": f"config 3: {c3['streams']} reference decode streams x {c3['cycles_per_stream']} cycles, "
@@ -500,6 +516,7 @@ def run_ours(args) -> None:
 
     c3 = None
     if not args.no_config3:
+        _log("config 3 GPU leg")
         del eng
         torch.cuda.empty_cache()
         c3 = run_config3(args, world, rank, local, cfg, peaks)

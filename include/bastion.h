@@ -269,6 +269,10 @@ int bst_attention_ragged(const void* q, int64_t q_tok_stride, void* out, int64_t
  * ---------------------------------------------------------------------- */
 int bst_embed_rmsnorm(const int32_t* tokens, int rows, const void* emb, int h, const void* w, float eps, float* resid,
                       void* x, int64_t ldx, bst_stream_t stream);
+/* Residual update from a dense y (the tensor-parallel all-reduced row-parallel output, fp32
+ * or bf16 when y_bf16; NULL: normalise only): resid += y; x = RMSNorm(resid) * w. */
+int bst_residual_dense(const void* y, int y_bf16, int64_t ldy, float* resid, int rows, int h, const void* w, float eps,
+                       void* x, int64_t ldx, void* feat, int64_t ldf, bst_stream_t stream);
 int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t* sched, float* resid, int rows, int h,
                          const void* w, float eps, void* x, int64_t ldx, void* feat, int64_t ldf, bst_stream_t stream);
 /* pos/slot are relative to c = state[c_idx]; slot == INT32_MIN skips the KV write,

@@ -88,6 +88,7 @@ SIGNATURES = {
     "bst_attention_keymajor": (_I, [_P, _I64, _P, _I64, _P, _I, _I, _I, _P, _I, _I, _I, _I, _I, _I, _P, _I, _I, _P,
                                     _I, _I, _P, _SZ, _P]),
     "bst_embed_rmsnorm": (_I, [_P, _I, _P, _I, _P, C.c_float, _P, _P, _I64, _P]),
+    "bst_residual_dense": (_I, [_P, _I, _I64, _P, _I, _I, _P, C.c_float, _P, _I64, _P, _I64, _P]),
     "bst_residual_rmsnorm": (_I, [_P, _P, _P, _I, _I, _P, C.c_float, _P, _I64, _P, _I64, _P]),
     "bst_qkv_rope": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, C.c_float, _P, _P, _P, _P, _P, _I64, _P, _I64,
                           _P, _I, _P, _I, _P]),
@@ -141,7 +142,7 @@ def check(rc: int) -> None:
 KERNELS_PER_CALL = {
     "bst_topk_logits": 3, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_expand_dev_batch": 1, "bst_linearize_mask": 1,
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
-    "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_keymajor": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_qkv_rope": 1,
+    "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_keymajor": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_residual_dense": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,
     "bst_qkv_rope_batch": 1, "bst_drafter_rows_batch": 1, "bst_attention_ragged": 1, "bst_ragged_rows": 1,
     "bst_ragged_unpack": 1, "bst_batch_plan": 1, "bst_gemm_argmax_keys": 2, "bst_argmax_from_keys": 1, "bst_gemm_sample": 2,

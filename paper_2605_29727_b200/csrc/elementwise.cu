@@ -146,6 +146,46 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
 #endif
 }
 
+
+// Residual update from a DENSE y (the tensor-parallel all-reduced row-parallel output,
+// fp32 or bf16): resid += y; x = RMSNorm(resid) * w; optional bf16 copy of the residual.
+// Same arithmetic as residual_rmsnorm_kernel with y in place of the partial slots.
+template <typename YT>
+__global__ void __launch_bounds__(R_THREADS) residual_dense_kernel(
+    const YT* __restrict__ y, int64_t ldy, float* resid, int h, const __nv_bfloat16* __restrict__ w, float eps,
+    __nv_bfloat16* x, int64_t ldx, __nv_bfloat16* feat, int64_t ldf) {
+  pdl_enter();
+  __shared__ float sh[32];
+  __shared__ float4 vals[2048];
+  const int t = blockIdx.x;
+  const int ng = h >> 2;
+  float ss = 0.f;
+  for (int g = threadIdx.x; g < ng; g += R_THREADS) {
+    float4 v = reinterpret_cast<const float4*>(resid + (int64_t)t * h)[g];
+    if (y) {
+      const YT* yp = y + (int64_t)t * ldy + g * 4;
+      v.x += (float)yp[0]; v.y += (float)yp[1]; v.z += (float)yp[2]; v.w += (float)yp[3];
+    }
+    reinterpret_cast<float4*>(resid + (int64_t)t * h)[g] = v;
+    if (feat) {
+      __nv_bfloat162* f = reinterpret_cast<__nv_bfloat162*>(feat + (int64_t)t * ldf + g * 4);
+      f[0] = __floats2bfloat162_rn(v.x, v.y);
+      f[1] = __floats2bfloat162_rn(v.z, v.w);
+    }
+    vals[g] = v;
+    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+  }
+  const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
+  for (int g = threadIdx.x; g < ng; g += R_THREADS) {
+    const float4 v = vals[g];
+    const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w + g * 4);
+    const float2 w01 = __bfloat1622float2(wp[0]), w23 = __bfloat1622float2(wp[1]);
+    __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(x + (int64_t)t * ldx + g * 4);
+    xp[0] = __floats2bfloat162_rn(v.x * inv * w01.x, v.y * inv * w01.y);
+    xp[1] = __floats2bfloat162_rn(v.z * inv * w23.x, v.w * inv * w23.y);
+  }
+}
+
 // ------------------------------------------------------------- q/k/v + rope
 // One CTA per (token row, group of 16 heads); one warp per head (d = 128, 4 values per lane).
 __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, RopeArgs ra, bst_prefetch_t pf) {
@@ -236,6 +276,24 @@ extern "C" int bst_residual_rmsnorm(const float* partial, const bst_gemm_sched_t
   BST_CUDA(launch_pdl(residual_rmsnorm_kernel, dim3(rows), dim3(R_THREADS), 0, as_stream(stream), partial, s, resid, h,
                       static_cast<const __nv_bfloat16*>(w), eps, static_cast<__nv_bfloat16*>(x), ldx,
                       static_cast<__nv_bfloat16*>(feat), ldf, rows, take_prefetch()));
+  BST_LAUNCH_CHECK();
+  return BST_OK;
+}
+
+
+extern "C" int bst_residual_dense(const void* y, int y_bf16, int64_t ldy, float* resid, int rows, int h, const void* w,
+                                  float eps, void* x, int64_t ldx, void* feat, int64_t ldf, bst_stream_t stream) {
+  BST_REQUIRE(resid && w && x, "null pointer argument");
+  BST_REQUIRE(h <= 8192 && h % 4 == 0, "hidden size must be a multiple of 4 and <= 8192");
+  if (rows <= 0) return BST_OK;
+  if (y_bf16)
+    BST_CUDA(launch_pdl(residual_dense_kernel<__nv_bfloat16>, dim3(rows), dim3(R_THREADS), 0, as_stream(stream),
+                        static_cast<const __nv_bfloat16*>(y), ldy, resid, h, static_cast<const __nv_bfloat16*>(w), eps,
+                        static_cast<__nv_bfloat16*>(x), ldx, static_cast<__nv_bfloat16*>(feat), ldf));
+  else
+    BST_CUDA(launch_pdl(residual_dense_kernel<float>, dim3(rows), dim3(R_THREADS), 0, as_stream(stream),
+                        static_cast<const float*>(y), ldy, resid, h, static_cast<const __nv_bfloat16*>(w), eps,
+                        static_cast<__nv_bfloat16*>(x), ldx, static_cast<__nv_bfloat16*>(feat), ldf));
   BST_LAUNCH_CHECK();
   return BST_OK;
 }

@@ -5,7 +5,8 @@ Rank r of a tp-way group holds
   * q/k/v (column-parallel): query heads [r n_q/tp, (r+1) n_q/tp) and KV heads
     [r n_kv/tp, ...), so attention and the paged KV cache are head-local;
   * o_proj, down_proj (row-parallel): the matching input columns; their outputs are
-    partial sums of the residual stream, all-reduced (SUM, fp32) before RMSNorm;
+    partial sums of the residual stream, all-reduced (SUM, bf16 by default: half the
+    NVLink bytes of fp32, ``set_allreduce_dtype``) before the residual update + RMSNorm;
   * gate/up (column-parallel): FFN columns [r h_ffn/tp, ...) of gate and of up;
   * the LM head (vocab-parallel): vocabulary rows [r V/tp, ...); the per-row argmax
     is reduced as one signed 64-bit key (order-preserving fp32 bits | ~global index,
@@ -18,10 +19,11 @@ the same lattice, so no broadcast is needed.
 The collective points are exposed by ``forward_steps`` (a generator yielding
 ``(op, tensor)``), so the same code runs under NCCL (``dist_collective``) and in a
 single-process lock-step simulation of tp shards (``run_lockstep``, the parity test).
-Residual protocol at each row-parallel output: rank 0 adds its partial into the
-residual (residual_rmsnorm with the partial), the other ranks overwrite their copy
-of the residual with their partial (gemm_reduce), then SUM all-reduce → every rank
-holds residual + sum of partials; RMSNorm of the reduced residual follows.
+Residual protocol at each row-parallel output: every rank reduces its partial output
+y_r into a dense bf16 (or fp32) buffer (bst_gemm_reduce), the SUM all-reduce leaves
+sum_r y_r on every rank, and bst_residual_dense adds it to the replicated fp32
+residual and writes RMSNorm(residual) for the next column-parallel GEMM.  NCCL picks
+NVLS (in-switch reduction) for this all-reduce on NVSwitch systems when available.
 """
 
 from __future__ import annotations
@@ -91,16 +93,21 @@ class TPTargetModel(TargetModel):
         self.full_cfg, self.tp, self.rank = cfg, tp, rank
         super().__init__(local_config(cfg, tp), w, max_slots, max_rows, (), dev)
         self.keys = torch.zeros(max_rows, dtype=torch.int64, device=dev)
+        self.y_ar = torch.zeros(max_rows, cfg.h, dtype=torch.bfloat16, device=dev)  # all-reduce payload
 
-    def _row_parallel_out(self, p: ops.PartialOut, n: int):
-        """Residual protocol of a row-parallel GEMM output; yields the SUM all-reduce."""
+    def set_allreduce_dtype(self, dtype: torch.dtype) -> None:
+        """bf16 (default) or fp32 payload of the row-parallel output all-reduce."""
+        if dtype not in (torch.bfloat16, torch.float32):
+            raise ValueError("all-reduce dtype must be bf16 or fp32")
+        self.y_ar = torch.zeros(self.y_ar.shape, dtype=dtype, device=self.dev)
+
+    def _row_parallel_out(self, p: ops.PartialOut, n: int, norm_w: torch.Tensor):
+        """Row-parallel output: dense y_r, SUM all-reduce (yielded), residual += sum, RMSNorm."""
         cfg = self.cfg
-        resid = self.resid[:n]
-        if self.rank == 0:
-            ops.residual_rmsnorm(p, resid, n, cfg.h, self.w.final_norm, cfg.eps, x=self.x[:n])  # resid += Y_0
-        else:
-            ops.gemm_reduce_into(p, resid)  # resid = Y_r
-        yield "sum", resid
+        y = self.y_ar[:n]
+        ops.gemm_reduce_into(p, y)
+        yield "sum", y
+        ops.residual_dense(y, self.resid[:n], n, norm_w, cfg.eps, self.x[:n])
 
     def forward_steps(self, rows: int, state: torch.Tensor, mode: int, keys_after_c: int, anc=None,
                       mask_words: int = 0, head: str | None = "argmax", c_host: int = 0):
@@ -118,14 +125,12 @@ class TPTargetModel(TargetModel):
                           c_host, keys_after_c, kv.max_slots, state, mode, anc, mask_words, self.attn_ws,
                           n_splits=self.attn_splits)
             p = ops.gemm_partial(self.attn[:n], lw.o, out=self.partial)
-            yield from self._row_parallel_out(p, n)
-            ops.residual_rmsnorm(None, resid, n, cfg.h, lw.post_norm, eps, x=x)
+            yield from self._row_parallel_out(p, n, lw.post_norm)
             p = ops.gemm_partial(x, lw.gate_up, out=self.partial)
             ops.swiglu(p, n, cfg.h_ffn, self.act[:n])
             p = ops.gemm_partial(self.act[:n], lw.down, out=self.partial)
-            yield from self._row_parallel_out(p, n)
             nxt = w.layers[li + 1].in_norm if li + 1 < cfg.L else w.final_norm
-            ops.residual_rmsnorm(None, resid, n, cfg.h, nxt, eps, x=x)
+            yield from self._row_parallel_out(p, n, nxt)
         if head == "argmax":
             p = ops.gemm_partial(x, w.lm_head, out=self.partial)
             ops.gemm_argmax_keys(p, self.keys[:n], self.rank * cfg.V)

@@ -59,10 +59,13 @@ def linear(x: torch.Tensor, w: torch.Tensor, dtype=torch.float32) -> torch.Tenso
 
 
 def gemm_reduce_into(p: PartialOut, y: torch.Tensor) -> torch.Tensor:
-    """Dense fp32 Y[m, n_out] (row stride y.stride(0)) from the partial slots."""
+    """Dense Y[m, n_out] (fp32 or bf16, row stride y.stride(0)) from the partial slots."""
     s = p.sched
-    assert y.dtype == torch.float32 and y.stride(1) == 1 and y.shape[0] >= s.m and y.shape[1] >= s.n_out
-    _lib.call("bst_gemm_reduce", p.buf.data_ptr(), C.byref(s), y.data_ptr(), None, y.stride(0), stream_ptr())
+    assert y.dtype in (torch.float32, torch.bfloat16) and y.stride(1) == 1
+    assert y.shape[0] >= s.m and y.shape[1] >= s.n_out
+    f32 = y.data_ptr() if y.dtype == torch.float32 else None
+    b16 = y.data_ptr() if y.dtype == torch.bfloat16 else None
+    _lib.call("bst_gemm_reduce", p.buf.data_ptr(), C.byref(s), f32, b16, y.stride(0), stream_ptr())
     return y
 
 
@@ -130,6 +133,15 @@ def residual_rmsnorm(p: PartialOut | None, resid, rows, h, w, eps, x=None, feat=
     sched = C.byref(p.sched) if p is not None else None
     _lib.call("bst_residual_rmsnorm", None if p is None else p.buf.data_ptr(), sched, _p(resid), rows, h,
               w.data_ptr(), C.c_float(eps), _p(x), 0 if x is None else x.stride(0), _p(feat),
+              0 if feat is None else feat.stride(0), stream_ptr())
+
+
+def residual_dense(y, resid, rows, w, eps, x, feat=None) -> None:
+    """resid += y (dense fp32 / bf16 [rows, h], e.g. an all-reduced row-parallel output; None:
+    normalise only); x = RMSNorm(resid) * w (bf16); feat = bf16(resid)."""
+    yb = y is not None and y.dtype == torch.bfloat16
+    _lib.call("bst_residual_dense", _p(y), int(yb), 0 if y is None else y.stride(0), resid.data_ptr(), rows,
+              resid.shape[1], w.data_ptr(), C.c_float(eps), x.data_ptr(), x.stride(0), _p(feat),
               0 if feat is None else feat.stride(0), stream_ptr())
 
 

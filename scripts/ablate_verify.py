@@ -34,3 +34,5 @@ for _ in range(12):
     ts_v.append(b.elapsed_time(c))
 print(f"ablate={os.environ.get('BST_ABLATE', '-'):14s} rows={rows} draft_ms={statistics.median(ts_d[2:]):.3f} "
       f"verify_ms={statistics.median(ts_v[2:]):.3f}")
+if os.environ.get("AR"):
+    print(f"ar_step_ms={1e3 * eng.measure_ar_step():.3f}")

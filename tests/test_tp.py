@@ -89,8 +89,9 @@ def test_argmax_keys_kernel_matches_host_packing():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tp", [2])
-def test_tp_lockstep_matches_unsharded_target(tp):
+@pytest.mark.parametrize("tp,ar_dtype", [(2, "bf16"), (2, "fp32")])
+def test_tp_lockstep_matches_unsharded_target(tp, ar_dtype):
+    """bf16 (default) and fp32 all-reduce payloads of the row-parallel outputs."""
     from oracle import specplan_port as O
     from paper_2605_29727_b200.engine.config import TINY
     from paper_2605_29727_b200.engine.forward import MODE_CAUSAL, MODE_TREE, TargetModel
@@ -102,6 +103,8 @@ def test_tp_lockstep_matches_unsharded_target(tp):
     slots, R = 512, 64
     ref = TargetModel(cfg, full, slots, R, (), dev)
     shards = [TPTargetModel(cfg, tp, r, shard_weights(full, cfg, tp, r), slots, R, dev) for r in range(tp)]
+    for sh in shards:
+        sh.set_allreduce_dtype(torch.bfloat16 if ar_dtype == "bf16" else torch.float32)
     streams = [torch.cuda.Stream() for _ in range(tp)]
     rng = np.random.default_rng(0)
     P = 200
