@@ -723,7 +723,13 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 // K and V pages stream through separate rings: a K stage is released when its S
 // MMA completes, a V stage when its PV MMA completes, so K runs further ahead of
 // the softmax than a joint K+V ring of the same size allows.
-constexpr int T2_KS = 5, T2_VS = 4;
+#ifndef BST_T2_KS  // ring depths (measurement builds may override: BST_NVCC_EXTRA=-DBST_T2_KS=..)
+#define BST_T2_KS 5
+#endif
+#ifndef BST_T2_VS
+#define BST_T2_VS 4
+#endif
+constexpr int T2_KS = BST_T2_KS, T2_VS = BST_T2_VS;
 constexpr int T2_MIN_PAGES = 8;  // per-CTA page run from which the two-group kernel is used
 constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
 constexpr int T2_THREADS = 384;  // warps 0-1 K TMA / S issuer, 2-9 softmax groups, 10 V TMA, 11 PV issuer
