@@ -724,7 +724,11 @@ extern "C" int bst_gemm(const void* w, const void* x, int64_t ld_x, const bst_ge
     cfg2.attrs = at2;
     cfg2.numAttrs = 1;
     static int trig2 = -1;
-    if (trig2 < 0) trig2 = getenv("BST_GEMM_TRIGGER") ? atoi(getenv("BST_GEMM_TRIGGER")) : 1;
+    // No PDL trigger at CTA entry for the CTA-pair kernel: with it, a batched draft phase
+    // (CTA-pair GEMMs at 144-256 rows, back to back with their epilogues) deadlocked the
+    // GPU within a few cycles (scripts/c3_probe.py, 64 requests); dependents launch when
+    // the grid retires.  BST_GEMM2_TRIGGER=1 re-enables it (measurement only).
+    if (trig2 < 0) trig2 = getenv("BST_GEMM2_TRIGGER") ? atoi(getenv("BST_GEMM2_TRIGGER")) : 0;
     BST_CUDA(cudaLaunchKernelEx(&cfg2, gemm_bf16_2cta_kernel, tw2, tx2, s, partial, (int)s.stages, trig2));
     return BST_OK;
   }

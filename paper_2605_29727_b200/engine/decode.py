@@ -220,11 +220,12 @@ class B200Engine:
         ops.commit_state(self.state, self.acc_meta, self.committed, self.gamma + 1, self.out_tokens, tr.meta,
                          tr.surrogate, self.log_i32, self.log_f64)
 
-    @staticmethod
-    def _bucket(n_nodes: int) -> int:
+    def _bucket(self, n_nodes: int) -> int:
+        """Verify rows of an n-node tree: padded to its row bucket, never past the engine's
+        n_cap + 1 rows (the ancestor mask and tree buffers hold n_cap + 1 rows)."""
         rows = n_nodes + 1
         b = BUCKET if rows <= 256 else WIDE_BUCKET
-        return ((rows + b - 1) // b) * b
+        return min(((rows + b - 1) // b) * b, self.n_cap + 1)
 
     def _capture(self, fn) -> torch.cuda.CUDAGraph:
         # warm-up run outside the graph (kernel attributes, tensor maps, workspaces), then capture
@@ -252,6 +253,24 @@ class B200Engine:
             self.graph_d = self.graphs_d[self.policy] = self._capture(self._draft_body)
         with torch.cuda.stream(self.stream):
             self.graph_d.replay()
+
+    def precapture(self, max_rows: int | None = None) -> int:
+        """Capture the verify graph of every row bucket up to ``max_rows`` (default: the
+        engine's capacity) now, so no capture lands inside a timed decode loop (a bucket
+        first seen mid-run otherwise pays its eager warm-up run + capture + instantiate in
+        that cycle).  KV slots at and beyond c written by the warm-up runs are overwritten
+        by the next real verify; the decode state is restored.  Returns the graph count."""
+        if not self.use_graphs:
+            return 0
+        top = self.max_rows if max_rows is None else min(self._bucket(max_rows - 1), self.max_rows)
+        self._check_room(self._c_host, top)
+        for n in range(self.n_cap + 1):
+            b = self._bucket(n)
+            if b > top:
+                break
+            if b not in self.graphs_v:
+                self.graphs_v[b] = self._capture(lambda rows=b: self._verify_body(rows))
+        return len(self.graphs_v)
 
     def _run_verify(self, rows: int) -> None:
         if not self.use_graphs or self.export:
