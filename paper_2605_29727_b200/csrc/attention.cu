@@ -404,6 +404,11 @@ __device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
   asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ float ld_dsmem_f1(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
   float2 v;
   asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
@@ -411,6 +416,61 @@ __device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Cluster split merge (a.merge == 2): the n_splits (<= 16) CTAs of one (head, row block)
+// form a thread-block cluster (rank = split).  Each has staged its unnormalised partial
+// rows (fp32 [128][128], 16-byte chunks swizzled by row % 8) at shared address `stg` and
+// (m, l) per row in ms / ls; after a cluster barrier CTA `split` merges rows
+// [split * per, split * per + per) from every rank over DSMEM in rank order (the same
+// arithmetic and order as split_merge: deterministic) and stores bf16; a second barrier
+// keeps the staging alive until every remote read is done.  This replaces the L2 merge's
+// partial stores, arrival atomic, poll and partial loads (three dependent gpu-scope round
+// trips, ~3 us per launch at c = 2K) by two cluster barriers and DSMEM loads.
+constexpr int T2_CLUSTER_MAX = 16;
+template <int NT>
+__device__ void cluster_split_merge(const AttnArgs& a, const float* ms, const float* ls, uint32_t stg, int head,
+                                    int split, int req, int rb, int R) {
+  cluster_sync_all();
+  if (threadIdx.x >= 64 && threadIdx.x < 64 + NT) {
+    const int t = threadIdx.x - 64, ns = a.n_splits;
+    const int Rb = min(128, R - rb * 128);
+    const int per = (Rb + ns - 1) / ns, r0 = split * per, r1 = min(r0 + per, Rb);
+    const uint32_t ms_u = sm100::smem_u32(ms), ls_u = sm100::smem_u32(ls);
+    for (int it = t; it < (r1 - r0) * 32; it += NT) {
+      const int r = r0 + (it >> 5), cq = it & 31;
+      const uint32_t off = (uint32_t)(r * A_D + ((cq ^ (r & 7)) << 2)) * 4u;
+      float m[T2_CLUSTER_MAX], l[T2_CLUSTER_MAX];
+      float4 v[T2_CLUSTER_MAX];
+#pragma unroll
+      for (int q = 0; q < T2_CLUSTER_MAX; ++q) {
+        if (q < ns) {
+          m[q] = ld_dsmem_f1(mapa_shared(ms_u + r * 4, q));
+          l[q] = ld_dsmem_f1(mapa_shared(ls_u + r * 4, q));
+          v[q] = ld_dsmem_f4(mapa_shared(stg + off, q));
+        }
+      }
+      float M = -INFINITY;
+#pragma unroll
+      for (int q = 0; q < T2_CLUSTER_MAX; ++q)
+        if (q < ns) M = fmaxf(M, m[q]);
+      float Lsum = 0.f;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int q = 0; q < T2_CLUSTER_MAX; ++q) {
+        if (q < ns && m[q] != -INFINITY) {
+          const float w = ex2(m[q] - M);
+          Lsum += w * l[q];
+          acc.x += w * v[q].x; acc.y += w * v[q].y; acc.z += w * v[q].z; acc.w += w * v[q].w;
+        }
+      }
+      const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
+      const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
+      __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * cq;
+      *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+    }
+  }
+  cluster_sync_all();
 }
 
 // ===========================================================================
@@ -432,6 +492,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
+  __shared__ float cm[128], cl[128];  // cluster merge: (m, l) per row
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) TRACE(31, 0);
   if (threadIdx.x == 0) BND(a.seq, 0);
@@ -676,7 +737,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 #pragma unroll
       for (int e = 0; e < 128; ++e) o[e] = 0.f;
     }
-    if (a.n_splits > 1 && a.merge) {
+    if (a.n_splits > 1 && a.merge == 2) {
+      float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
+#pragma unroll
+      for (int q = 0; q < 32; ++q)
+        *reinterpret_cast<float4*>(stg + row * A_D + ((q ^ (row & 7)) << 2)) =
+            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      cm[row] = m_run;
+      cl[row] = l_run;
+    } else if (a.n_splits > 1 && a.merge) {
       float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
 #pragma unroll
       for (int q = 0; q < 32; ++q)
@@ -710,6 +779,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     if (threadIdx.x == 64) TRACE(31, 6);
     if (threadIdx.x == 64) TRACE_MAX(2);
   }
+  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<128>(a, cm, cl, sm100::smem_u32(gKV), head, split, req, rb, R);
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -730,7 +800,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
 #define BST_T2_VS 4
 #endif
 constexpr int T2_KS = BST_T2_KS, T2_VS = BST_T2_VS;
-constexpr int T2_MIN_PAGES = 8;  // per-CTA page run from which the two-group kernel is used
+#ifndef BST_T2_MIN_PAGES  // measurement builds may override
+#define BST_T2_MIN_PAGES 4
+#endif
+constexpr int T2_MIN_PAGES = BST_T2_MIN_PAGES;  // per-CTA page run from which the two-group kernel is used
 constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
 constexpr int T2_THREADS = 384;  // warps 0-1 K TMA / S issuer, 2-9 softmax groups, 10 V TMA, 11 PV issuer
 
@@ -739,7 +812,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   __shared__ __align__(8) uint64_t fullK[T2_KS], emptyK[T2_KS], fullV[T2_VS], emptyV[T2_VS], s_full[2], s_free[2],
       p_full[2], o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
-  __shared__ float xm[2][128], xl[2][128];
+  __shared__ float xm[2][128], xl[2][128], cm[128], cl[128];
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) TRACE(31, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1002,7 +1075,14 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
 #pragma unroll
       for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
     }
-    if (a.n_splits > 1 && a.merge) {
+    if (a.n_splits > 1 && a.merge == 2) {
+      float* stg = reinterpret_cast<float*>(gKV);
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
+            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      if (g == 0) { cm[row] = M; cl[row] = L; }
+    } else if (a.n_splits > 1 && a.merge) {
       const int Rws = a.group * a.s;  // the workspace keeps the uniform per-request row stride
       if (valid) {  // unnormalised partial straight to the L2 workspace, coalesced over rows
         const int64_t bse = kt_ws_base(a, req, split, head);
@@ -1034,6 +1114,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       }
     }
   }
+  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<256>(a, cm, cl, sm100::smem_u32(gKV), head, split, req, rb, R);
   if (threadIdx.x == 64) TRACE_MAX(2);
   if (threadIdx.x == 0) TRACE(31, 0);
   sm100::tc_fence_before();
@@ -1724,6 +1805,41 @@ static int kt_cluster_occupancy(int nch, int cs) {
 }
 
 
+// resident clusters of `cs` row-major attention CTAs (cudaOccupancyMaxActiveClusters), per kernel
+static int rm_cluster_fits(bool two_groups, int cs, int smem) {
+  static int occ[2][T2_CLUSTER_MAX + 1];
+  static bool init = false;
+  if (!init) {
+    for (int k = 0; k < 2; ++k)
+      for (int i = 0; i <= T2_CLUSTER_MAX; ++i) occ[k][i] = -1;
+    init = true;
+  }
+  if (cs < 2 || cs > T2_CLUSTER_MAX) return 0;
+  int& o = occ[two_groups ? 1 : 0][cs];
+  if (o >= 0) return o;
+  auto kern = two_groups ? attn_tc2_kernel : attn_tc_kernel;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1, cs, 1);
+  cfg.blockDim = dim3(two_groups ? T2_THREADS : T_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 1;
+  at[0].val.clusterDim.y = cs;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, kern, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  o = n;
+  return n;
+}
+
 static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_t o_tok_stride, const void* kv_cache,
                           int n_layers, int n_pages_total, int layer, const int32_t* page_table, int n_q, int n_kv, int s,
                           int c, int keys_after_c, int max_keys, const int32_t* state, int c_idx, int mode,
@@ -1932,20 +2048,49 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   // row-major kernels, chosen by shape: the single-group kernel for short per-CTA page
   // runs, two alternating softmax groups once a CTA walks >= T2_MIN_PAGES pages (long
   // context; the tc2 kernel on short runs broke the tiny-config exactness)
-  const bool two_groups = pps >= T2_MIN_PAGES;
+  bool two_groups = pps >= T2_MIN_PAGES;
   a.merge = (n_splits > 1 && n_kv * n_splits * row_blocks * n_req <= n_sm &&
              n_kv * row_blocks * n_req * sizeof(unsigned long long) <= A_WS_CNT_BYTES / 2) ? 1 : 0;
+  // Split merge inside a thread-block cluster over DSMEM when every cluster is co-resident
+  // (the largest cluster <= the one-wave split count that fits); taken when it lengthens
+  // each CTA's page run by at most 4 pages (~0.65 us each) against the ~3 us it saves.
+  // BST_ATTN_CLUSTER=0 disables it (measurement).
+  static int cl_on = -1;
+  if (cl_on < 0) cl_on = getenv("BST_ATTN_CLUSTER") ? atoi(getenv("BST_ATTN_CLUSTER")) : 1;
+  if (cl_on && a.merge && n_splits_arg <= 0) {
+    const int groups_total = n_kv * row_blocks * n_req;
+    for (int ncl = n_splits > T2_CLUSTER_MAX ? T2_CLUSTER_MAX : n_splits; ncl >= 2; --ncl) {
+      int pk = (pages + ncl - 1) / ncl;
+      pk += pk & 1;
+      const int nsc = (pages + pk - 1) / pk;
+      const bool tg = pk >= T2_MIN_PAGES;
+      if (nsc < 2 || rm_cluster_fits(tg, nsc, tg ? smem_tc2 : smem_tc) < groups_total) continue;
+      if (pk - pps <= 4) {
+        n_splits = nsc;
+        pps = pk;
+        two_groups = tg;
+        a.n_splits = n_splits;
+        a.pages_per_split = pps;
+        a.merge = 2;
+      }
+      break;
+    }
+  }
   {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(n_kv, n_splits, row_blocks * n_req);
     cfg.blockDim = dim3(two_groups ? T2_THREADS : T_THREADS);
     cfg.dynamicSmemBytes = two_groups ? smem_tc2 : smem_tc;
     cfg.stream = st;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = 1;
+    attr[1].val.clusterDim.y = a.merge == 2 ? n_splits : 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = a.merge == 2 ? 2 : 1;
     if (two_groups)
       BST_CUDA(cudaLaunchKernelEx(&cfg, attn_tc2_kernel, tm, a));
     else
@@ -2075,4 +2220,11 @@ extern "C" int bst_debug_bnd_trace_attn(void* buf) {  // BST_TRACE builds only
   (void)buf;
   return BST_EINVAL;
 #endif
+}
+
+// debug: resident clusters of `cs` two-group attention CTAs at the kernel's shared memory
+extern "C" int bst_debug_tc2_cluster_fits(int cs) {
+  using namespace bst;
+  const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
+  return rm_cluster_fits(true, cs, smem_tc2);
 }
