@@ -47,7 +47,7 @@ from .forward import _gemm_rows
 
 # rows per batched verify launch (K4 CTA-pair kernel takes up to 512); BST_VERIFY_ROWS: measurement
 VERIFY_ROWS = min(512, int(os.environ.get("BST_VERIFY_ROWS", "512")))
-from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
+from .forward import MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel, drafter_prefill
 from .weights import DrafterWeights, TargetWeights
 
 
@@ -203,10 +203,7 @@ class BatchEngine:
                     t.pos[:n].copy_(ar)
                     t.slot[:n].copy_(ar)
                     t.forward(n, st, MODE_CAUSAL, keys_after_c=n, head=None, c_host=start, pt=self._pt(r))
-                    d.feat_in[:n].copy_(t.feat[:n])
-                    d.pos[:n].copy_(ar)
-                    d.slot[:n].copy_(ar)
-                    d.prefill_ctx(n, st, pt=self._dpt(r))
+                    drafter_prefill(d, t.feat, n, st, start, pt=self._dpt(r))
                 st.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
         self.stream.synchronize()
         self._c_bound = int(self.contexts().max())

@@ -36,7 +36,7 @@ from ..device import graph_kernel_nodes
 from ..draft_tree import DeviceTree, expand_device_plan
 from ..lattice import MarginalBlock, topk_logits_into
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
-from .forward import _ABLATE, MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel
+from .forward import _ABLATE, MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel, drafter_prefill
 from .weights import DrafterWeights, TargetWeights
 
 ST_C, ST_NNEW, ST_BONUS, ST_COMMITTED, ST_CYCLE = 0, 1, 2, 3, 4
@@ -44,7 +44,7 @@ MAX_TREE = 1024      # reference default n_max (sp/harness.py:62, fixed grid up 
 BUCKET = 16          # verify rows are padded to 16-row buckets up to 256 rows ...
 WIDE_BUCKET = 64     # ... and to 64-row buckets above (one captured verify graph per bucket)
 MAX_ROWS = 1088      # verify rows of the largest tree (1025) rounded up to its bucket
-PREFILL_ROWS = 256   # causal prefill chunk
+PREFILL_ROWS = 512   # causal prefill chunk (one CTA-pair GEMM launch per weight: the weights stream once per 512 rows)
 
 
 @dataclass
@@ -137,10 +137,7 @@ class B200Engine:
                 t.pos[:n].copy_(ar)
                 t.slot[:n].copy_(ar)
                 t.forward(n, self.state, MODE_CAUSAL, keys_after_c=n, head=None, c_host=start)
-                d.feat_in[:n].copy_(t.feat[:n])
-                d.pos[:n].copy_(ar)
-                d.slot[:n].copy_(ar)
-                d.prefill_ctx(n, self.state)
+                drafter_prefill(d, t.feat, n, self.state, start)
             self.state.copy_(torch.tensor([P - 1, 0, prompt[-1], 0, 0, 0, 0, 0], dtype=torch.int32))
         self.stream.synchronize()
         self.exported = []

@@ -349,6 +349,25 @@ class DrafterModel:
         return self.logits_b[:QB]
 
 
+DRAFT_PREFILL_ROWS = 256  # drafter context rows per prefill launch (its GEMM partials hold 256 rows)
+
+
+def drafter_prefill(d: "DrafterModel", feat: torch.Tensor, n: int, state: torch.Tensor, start: int,
+                    pt: torch.Tensor | None = None) -> None:
+    """Drafter context K/V for prompt rows [start, start + n) from the target's feature rows
+    feat[:n], in launches of <= DRAFT_PREFILL_ROWS rows; state[0] (c) is set to each piece's
+    first absolute position (the rows' slots are relative to c)."""
+    for d0 in range(0, n, DRAFT_PREFILL_ROWS):
+        dn = min(DRAFT_PREFILL_ROWS, n - d0)
+        if d0:
+            state[0:1].fill_(start + d0)
+        d.feat_in[:dn].copy_(feat[d0:d0 + dn])
+        ar = torch.arange(dn, dtype=torch.int32, device=feat.device)
+        d.pos[:dn].copy_(ar)
+        d.slot[:dn].copy_(ar)
+        d.prefill_ctx(dn, state, pt=pt)
+
+
 def _reduce_into(p: ops.PartialOut, y: torch.Tensor) -> None:
     import ctypes as C
 
