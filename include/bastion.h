@@ -199,6 +199,12 @@ int bst_gemm_argmax(const float* partial, const bst_gemm_sched_t* sched, void* s
 int bst_gemm_sample(const float* partial, const bst_gemm_sched_t* sched, void* scratch_u64, int32_t* out,
                     const int32_t* pos, const int32_t* state, int c_idx, float temperature, uint64_t seed,
                     bst_stream_t stream);
+/* K1 on the GEMM output (replaces the drafter plugin's softmax + top_k_truncate, lattice.py:24-55,
+ * 128-142, like bst_topk_logits): the drafter LM head's partial slots are read directly,
+ * summed as bst_gemm_reduce sums them, so the lattice is bit-identical to reducing first;
+ * rows 0..gamma-1 of the GEMM, sched->n_out == vocab.  No full-row export. */
+int bst_topk_gemm_partial(const float* partial, const bst_gemm_sched_t* sched, int gamma, int vocab, int k,
+                          int32_t* tok, double* prob, void* ws, size_t ws_bytes, bst_stream_t stream);
 /* Vocab-parallel LM head (tensor-parallel target): per-row argmax keys of
  * this shard, key = (order-preserving fp32 bits << 32 | 0xFFFFFFFF - global index),
  * global index = vocab_offset + column, top bit flipped so a signed int64 MAX

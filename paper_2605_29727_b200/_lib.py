@@ -67,6 +67,7 @@ SIGNATURES = {
     "bst_topk_workspace": (_SZ, [_I, _I, _I]),
     "bst_topk_logits": (_I, [_P, _I, _I, _I, _I64, _I, _P, _P, _P, _P, _SZ, _P]),
     "bst_topk_probs": (_I, [_P, _I, _I, _I, _P, _P, _P, _SZ, _P]),
+    "bst_topk_gemm_partial": (_I, [_P, C.POINTER(GemmSched), _I, _I, _I, _P, _P, _P, _SZ, _P]),
     "bst_expand_workspace": (_SZ, [_I, _I, _I]),
     "bst_expand": (_I, [_P, _P, _I, _I, C.POINTER(Plan), _I, C.POINTER(Tree), _P, _SZ, _P]),
     "bst_linearize_mask": (_I, [_P, _I, _I, _I, _P, _P]),
@@ -140,7 +141,7 @@ def check(rc: int) -> None:
 
 # kernels launched by one call of each C-ABI entry point (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
-    "bst_topk_logits": 3, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_expand_dev_batch": 1, "bst_linearize_mask": 1,
+    "bst_topk_logits": 2, "bst_topk_gemm_partial": 2, "bst_topk_probs": 2, "bst_expand": 1, "bst_expand_dev": 1, "bst_expand_dev_batch": 1, "bst_linearize_mask": 1,
     "bst_ancestor_mask": 1, "bst_accept": 1, "bst_kv_compact": 1, "bst_gemm": 1, "bst_gemm_reduce": 1,
     "bst_gemm_argmax": 2, "bst_attention": 1, "bst_attention_keymajor": 1, "bst_attention_batch": 1, "bst_embed_rmsnorm": 1, "bst_residual_rmsnorm": 1, "bst_residual_dense": 1, "bst_qkv_rope": 1,
     "bst_swiglu": 1, "bst_gather_rows": 1, "bst_verify_rows": 1, "bst_drafter_rows": 1, "bst_commit_state": 1,

@@ -8,7 +8,7 @@
 //
 // Logits (hot path): k1_fast_chunk (per chunk: max, fp64 sum, top-(K+1) by
 // logit) -> k1_fast_finalize (per row: m, Z, exact fp64 probs of the K
-// survivors, (prob desc, token asc) order, boundary check) -> k1_fast_fallback
+// survivors, (prob desc, token asc) order, boundary check; in-CTA fallback)
 // (exact full-row selection, only for rows whose K/K+1 boundary logits are
 // distinct but < 1e-12 apart).  fp64 MarginalBlock rows are probs_full.
 // fp64 probability input (top_k_truncate): exact chunked selection on the
@@ -18,6 +18,7 @@
 #include <cuda_bf16.h>
 
 #include "common.cuh"
+#include "gemm.cuh"
 
 namespace bst {
 
@@ -63,6 +64,29 @@ static TopkWs carve(void* ws, int gamma, int chunks, int k, size_t* total) {
 __device__ __forceinline__ float load_logit(const void* base, int dtype, int64_t idx) {
   if (dtype == 0) return __ldg(static_cast<const float*>(base) + idx);
   return __bfloat162float(static_cast<const __nv_bfloat16*>(base)[idx]);
+}
+
+// Logit source of the fast path: an fp32/bf16 [gamma, stride] matrix, or the LM head's
+// stream-K partial slots (the K4 GEMM output, summed here in the order gemm_reduce uses:
+// slot 0, then the higher k ranges), so K1 reads the GEMM output without a reduce pass.
+struct LogitSrc {
+  const void* logits;
+  int dtype;
+  int64_t stride;
+  const float* partial;  // non-null: partial slots of sched
+  bst_gemm_sched_t sched;
+};
+__device__ __forceinline__ float src_logit(const LogitSrc& src, int row, int v) {
+  if (src.partial) {
+    const bst_gemm_sched_t& s = src.sched;
+    const int tile = v >> 7;
+    const int nslot = tile_nslot(s, tile);
+    const float* p = src.partial + ((int64_t)tile * s.s_max * s.bn + row) * 128 + (v & 127);
+    float acc = __ldg(p);
+    for (int k = 1; k < nslot; ++k) acc += __ldg(p + (int64_t)k * s.bn * 128);
+    return acc;
+  }
+  return load_logit(src.logits, src.dtype, (int64_t)row * src.stride + v);
 }
 
 __device__ __forceinline__ bool better(double pa, int ta, double pb, int tb) {
@@ -315,12 +339,10 @@ __device__ void block_top_keys(unsigned long long (&c)[TK_PER_THREAD], int n, un
 }
 
 // A: per (chunk, row): fp32 max m_c, fp64 S_c = sum exp(l - m_c), top-(K+1) keys
-__global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(const void* logits, int dtype, int vocab, int64_t stride,
-                                                            int kp, float* pmax, double* psum,
+__global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(LogitSrc src, int vocab, int kp, float* pmax, double* psum,
                                                             unsigned long long* ckeys) {
   pdl_enter();
   const int row = blockIdx.y, chunk = blockIdx.x, chunks = gridDim.x;
-  const int64_t base = (int64_t)row * stride;
   float l[TK_PER_THREAD];
   unsigned long long key[TK_PER_THREAD];
   float m = -INFINITY;
@@ -328,7 +350,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(const void* logits, 
   for (int i = 0; i < TK_PER_THREAD; ++i) {
     const int v = chunk * TK_CHUNK + i * TK_THREADS + threadIdx.x;
     if (v < vocab) {
-      l[i] = load_logit(logits, dtype, base + v);
+      l[i] = src_logit(src, row, v);
       key[i] = logit_key(l[i], v);
       m = fmaxf(m, l[i]);
     } else {
@@ -366,12 +388,18 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_chunk(const void* logits, 
   block_top_keys(key, kp, ckeys + ((int64_t)row * chunks + chunk) * kp);
 }
 
-// B: per row: m, Z (fixed order), global top-(K+1), exact fp64 probs, boundary check
+__device__ void k1_fallback_row(const LogitSrc& src, int vocab, int row, double m, double z, int k, int32_t* tok_out,
+                                double* prob_out);
+
+// B: per row: m, Z (fixed order), global top-(K+1), exact fp64 probs, boundary check; a
+// row whose K-th / (K+1)-th logits are distinct but < 1e-12 apart redoes the selection on
+// the exact fp64 probabilities of the whole row in the same CTA (k1_fallback_row)
 __global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax, const double* psum,
                                                                const unsigned long long* ckeys, int chunks, int kp,
                                                                int k, int32_t* tok_out, double* prob_out,
-                                                               double* stats, int* fallback) {
+                                                               double* stats, int* fallback, LogitSrc src, int vocab) {
   pdl_enter();
+  __shared__ int fb_sh;
   const int row = blockIdx.x;
   const int n = chunks * kp;
   unsigned long long c[TK_PER_THREAD];
@@ -398,6 +426,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax
       if (gap > 0.0 && gap < 1e-12) fb = 1;
     }
     fallback[row] = fb;
+    fb_sh = fb;
     // exact probabilities, then (prob desc, token asc) insertion sort of the K survivors
     double p[TK_KP_MAX];
     int t[TK_KP_MAX];
@@ -422,6 +451,8 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_finalize(const float* pmax
       prob_out[row * k + j] = p[j];
     }
   }
+  __syncthreads();
+  if (fb_sh) k1_fallback_row(src, vocab, row, stats[row * 2], stats[row * 2 + 1], k, tok_out, prob_out);
 }
 
 // Full fp64 rows (MarginalBlock export) with the same m and Z.
@@ -437,13 +468,8 @@ __global__ void __launch_bounds__(TK_THREADS) k1_full_rows(const void* logits, i
 
 // Exact fallback: rows flagged by the boundary check redo the selection on the
 // fp64 probabilities of the whole row (single CTA per flagged row).
-__global__ void __launch_bounds__(TK_THREADS) k1_fast_fallback(const void* logits, int dtype, int vocab,
-                                                               int64_t stride, const double* stats, const int* fallback,
-                                                               int k, int32_t* tok_out, double* prob_out) {
-  pdl_enter();
-  const int row = blockIdx.x;
-  if (!fallback[row]) return;
-  const double m = stats[row * 2], z = stats[row * 2 + 1];
+__device__ void k1_fallback_row(const LogitSrc& src, int vocab, int row, double m, double z, int k, int32_t* tok_out,
+                                double* prob_out) {
   // running top-k over the row: per 4096-element block, merge the block's top-k with the current list
   __shared__ double cur_p[TK_MAX_K];
   __shared__ int cur_t[TK_MAX_K];
@@ -458,7 +484,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_fallback(const void* logit
     for (int i = 0; i < TK_PER_THREAD; ++i) {
       const int v = b0 + i * TK_THREADS + threadIdx.x;
       if (v < vocab) {
-        p[i] = __ddiv_rn(exp((double)load_logit(logits, dtype, (int64_t)row * stride + v) - m), z);
+        p[i] = __ddiv_rn(exp((double)src_logit(src, row, v) - m), z);
         t[i] = v;
       } else {
         p[i] = -1.0;
@@ -488,7 +514,7 @@ __global__ void __launch_bounds__(TK_THREADS) k1_fast_fallback(const void* logit
 
 static int run_topk(const void* logits, int dtype, const double* probs_in, int gamma, int vocab, int64_t stride,
                     int k, int32_t* tok, double* prob, double* probs_full, void* ws, size_t ws_bytes,
-                    cudaStream_t st) {
+                    cudaStream_t st, const float* partial = nullptr, const bst_gemm_sched_t* sched = nullptr) {
   BST_REQUIRE(gamma >= 1, "gamma must be >= 1, got %d", gamma);
   BST_REQUIRE(vocab >= 2, "vocab_size must be >= 2, got %d", vocab);
   BST_REQUIRE(k >= 1 && k <= vocab, "k must be in [1, %d], got %d", vocab, k);
@@ -501,11 +527,14 @@ static int run_topk(const void* logits, int dtype, const double* probs_in, int g
   BST_REQUIRE(ws != nullptr && ws_bytes >= need, "workspace too small: %zu < %zu", ws_bytes, need);
   dim3 grid(chunks, gamma);
   const int kp = k + 1 <= vocab ? k + 1 : k;
+  LogitSrc src{logits, dtype, stride, partial, sched ? *sched : bst_gemm_sched_t{}};
+  BST_REQUIRE(!partial || (probs_in == nullptr && probs_full == nullptr && kp < TK_KP_MAX &&
+                           (int64_t)chunks * kp <= TK_CHUNK),
+              "K1 over GEMM partials: fast path only, no full-row export");
   if (probs_in == nullptr && kp < TK_KP_MAX && (int64_t)chunks * kp <= TK_CHUNK) {
-    BST_CUDA(launch_pdl(k1_fast_chunk, dim3(grid), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, kp, w.pmax, w.psum, w.ckeys));
-    BST_CUDA(launch_pdl(k1_fast_finalize, dim3(gamma), dim3(TK_THREADS), 0, st, w.pmax, w.psum, w.ckeys, chunks, kp, k, tok, prob, w.stats,
-                                                   w.fallback));
-    BST_CUDA(launch_pdl(k1_fast_fallback, dim3(gamma), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.stats, w.fallback, k, tok, prob));
+    BST_CUDA(launch_pdl(k1_fast_chunk, dim3(grid), dim3(TK_THREADS), 0, st, src, vocab, kp, w.pmax, w.psum, w.ckeys));
+    BST_CUDA(launch_pdl(k1_fast_finalize, dim3(gamma), dim3(TK_THREADS), 0, st, w.pmax, w.psum, w.ckeys, chunks, kp, k, tok,
+                        prob, w.stats, w.fallback, src, vocab));
     if (probs_full) BST_CUDA(launch_pdl(k1_full_rows, dim3(dim3(chunks, gamma)), dim3(TK_THREADS), 0, st, logits, dtype, vocab, stride, w.stats,
                                                                             probs_full));
     BST_LAUNCH_CHECK();
@@ -539,6 +568,15 @@ extern "C" int bst_topk_logits(const void* logits, int dtype, int gamma, int voc
   BST_REQUIRE(logits && tok && prob, "null pointer argument");
   return bst::run_topk(logits, dtype, nullptr, gamma, vocab, row_stride, k, tok, prob, probs_full, ws, ws_bytes,
                        bst::as_stream(stream));
+}
+
+extern "C" int bst_topk_gemm_partial(const float* partial, const bst_gemm_sched_t* sched, int gamma, int vocab, int k,
+                                     int32_t* tok, double* prob, void* ws, size_t ws_bytes, bst_stream_t stream) {
+  BST_REQUIRE(partial && sched && tok && prob, "null pointer argument");
+  BST_REQUIRE(sched->n_out == vocab && sched->m >= gamma, "schedule (n_out=%d, m=%d) does not cover %d x %d logits",
+              sched->n_out, sched->m, gamma, vocab);
+  return bst::run_topk(nullptr, 0, nullptr, gamma, vocab, vocab, k, tok, prob, nullptr, ws, ws_bytes,
+                       bst::as_stream(stream), partial, sched);
 }
 
 extern "C" int bst_topk_probs(const double* probs, int gamma, int vocab, int k, int32_t* tok, double* prob,

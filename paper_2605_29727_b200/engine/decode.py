@@ -34,7 +34,7 @@ from ..controller import STOP_BUDGET_CAP
 from ..cost_model import CycleLatencies, VerifyLatencyEstimator
 from ..device import graph_kernel_nodes
 from ..draft_tree import DeviceTree, expand_device_plan
-from ..lattice import MarginalBlock, topk_logits_into
+from ..lattice import MarginalBlock, topk_logits_into, topk_partial_into
 from .config import QWEN3_8B, DrafterConfig, ModelConfig, default_feat_layers
 from .forward import _ABLATE, MODE_CAUSAL, MODE_TREE, PAGE, DrafterModel, TargetModel, drafter_prefill
 from .weights import DrafterWeights, TargetWeights
@@ -183,9 +183,14 @@ class B200Engine:
     def _draft_body(self) -> None:
         if self.draft_override is not None:  # test hook: externally supplied drafter logits [gamma, V]
             logits = self.draft_override(self)
+        elif self.probs_full is None:  # hot path: K1 reads the LM head's partial slots (no reduce pass)
+            p = self.drafter.forward(self.state, reduce=False)
+            if "k1" not in _ABLATE:
+                topk_partial_into(p, self.gamma, self.top_k, self.lat_tok, self.lat_prob)
+            logits = None
         else:
             logits = self.drafter.forward(self.state)
-        if "k1" not in _ABLATE:
+        if logits is not None and "k1" not in _ABLATE:
             topk_logits_into(logits, self.top_k, self.lat_tok, self.lat_prob, self.probs_full)
         if "k2" not in _ABLATE:
             expand_device_plan(self.lat_tok, self.lat_prob, self.plan_dev, self.policy[0], self.policy[1], self.tree)

@@ -284,8 +284,9 @@ class DrafterModel:
                               cfg.eps, self.inv_freq, self.pos, self.slot, self.qrow, self.q, self.kv.buf,
                               li * self.kv.layer_stride, pt, PAGE, state)
 
-    def forward(self, state: torch.Tensor) -> torch.Tensor:
-        """Draft one block: returns logits [gamma, V] fp32 for future positions c+1..c+gamma."""
+    def forward(self, state: torch.Tensor, reduce: bool = True):
+        """Draft one block: returns logits [gamma, V] fp32 for future positions c+1..c+gamma
+        (reduce=False: the LM head's ``ops.PartialOut`` for K1 to read directly)."""
         cfg, w, B, CR = self.cfg, self.w, self.B, self.CR
         eps, M = cfg.eps, B + CR
         ops.drafter_rows(state, self.dcfg.gamma, self.mask_token, CR, self.tokens, self.pos, self.slot, self.qrow)
@@ -307,6 +308,8 @@ class DrafterModel:
             nxt = w.layers[li + 1].in_norm if li + 1 < len(w.layers) else w.final_norm
             ops.residual_rmsnorm(p, resid, B, cfg.h, nxt, eps, x=xb)
         p = ops.gemm_partial(self.X[1:B], self.tw.lm_head, out=self.partial)
+        if not reduce:
+            return p
         _reduce_into(p, self.logits)
         return self.logits
 

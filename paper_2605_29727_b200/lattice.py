@@ -199,6 +199,17 @@ def block_from_rows(rows: Sequence[Sequence[float]]) -> MarginalBlock:
     return MarginalBlock(gamma=probs.shape[0], vocab_size=probs.shape[1], probs=probs)
 
 
+def topk_partial_into(p, gamma: int, k: int, tok: torch.Tensor, prob: torch.Tensor) -> None:
+    """K1 on the drafter LM head's GEMM output (``ops.PartialOut``, rows 0..gamma-1) without a
+    reduce pass: bit-identical to ``topk_logits_into`` on the reduced fp32 logits."""
+    import ctypes as _C
+    vocab = int(p.sched.n_out)
+    need = _lib.lib().bst_topk_workspace(gamma, vocab, k)
+    ws = workspace("topk", need)
+    _lib.call("bst_topk_gemm_partial", p.buf.data_ptr(), _C.byref(p.sched), gamma, vocab, k, tok.data_ptr(),
+              prob.data_ptr(), ws.data_ptr(), ws.numel(), stream_ptr())
+
+
 def topk_logits_into(logits: torch.Tensor, k: int, tok: torch.Tensor, prob: torch.Tensor,
                      full: torch.Tensor | None = None) -> None:
     """K1 into caller-owned buffers (graph-capturable; workspace must already be sized)."""

@@ -58,8 +58,8 @@ def _engine_logits(eng, prompt, n_fixed):
     eng.set_policy("fixed", n=n_fixed)
     t, tr = eng.target, eng.tree
     with torch.cuda.stream(eng.stream):
-        eng._draft_body()
-        dl = eng.drafter.logits.clone()
+        eng._draft_body()  # K1 reads the LM head's partial slots here; the logits themselves:
+        dl = eng.drafter.forward(eng.state).clone()
     eng.stream.synchronize()
     n = int(tr.meta[0].item())
     rows = eng._bucket(n)
@@ -94,7 +94,7 @@ def test_tiny_drafter_and_verify_logits(gamma):
     from paper_2605_29727_b200.engine.config import TINY
     eng = _engine(TINY, gamma, 2, 128, 640)
     ref = _ref(eng)
-    prompt = _prompt(300, TINY.V, seed=21)  # > 256: chunked prefill
+    prompt = _prompt(560, TINY.V, seed=21)  # > 512: chunked prefill
     dg, vg, tree = _engine_logits(eng, prompt, 96)
     dw, vw = _oracle_logits(ref, eng, prompt, tree)
     ed, ev = _rel_err(dg, dw), _rel_err(vg, vw)

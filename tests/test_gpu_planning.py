@@ -73,6 +73,30 @@ def test_k1_logits_full_vocab_matches_oracle(P, dtype, scale):
     np.testing.assert_allclose(full_h, ref, rtol=1e-12, atol=1e-300)
 
 
+@pytest.mark.parametrize("vocab,scale", [(151936, 6.0), (151936, 30.0), (1024, 6.0)])
+def test_k1_on_gemm_partials_equals_reduced_logits(P, vocab, scale):
+    """bst_topk_gemm_partial (K1 reading the LM head's stream-K partial slots, the engine's
+    draft path) is bit-identical to K1 on the reduced fp32 logits (the export path)."""
+    from paper_2605_29727_b200 import ops
+    from paper_2605_29727_b200.lattice import topk_logits_into, topk_partial_into
+    g = torch.Generator(device="cuda").manual_seed(vocab + int(scale))
+    w = (torch.randn(vocab, 4096, device="cuda", generator=g) * 0.02).to(torch.bfloat16)
+    x = (torch.randn(16, 4096, device="cuda", generator=g) * scale).to(torch.bfloat16)
+    part = torch.empty(64 << 20, dtype=torch.float32, device="cuda")
+    p = ops.gemm_partial(x, w, out=part)
+    logits = torch.empty(16, vocab, device="cuda")
+    from paper_2605_29727_b200.engine.forward import _reduce_into
+    _reduce_into(p, logits)
+    tok_a = torch.empty(16, 8, dtype=torch.int32, device="cuda")
+    prob_a = torch.empty(16, 8, dtype=torch.float64, device="cuda")
+    tok_b, prob_b = torch.empty_like(tok_a), torch.empty_like(prob_a)
+    topk_logits_into(logits, 8, tok_a, prob_a)
+    topk_partial_into(p, 16, 8, tok_b, prob_b)
+    torch.cuda.synchronize()
+    assert torch.equal(tok_a, tok_b)
+    assert prob_a.cpu().numpy().tobytes() == prob_b.cpu().numpy().tobytes()
+
+
 def test_k1_bf16_ties_token_order(P):
     from paper_2605_29727_b200.lattice import lattice_from_logits
     # many exactly equal logits: order must be token ascending among ties
