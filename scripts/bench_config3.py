@@ -30,6 +30,8 @@ ap.add_argument("--n", type=int, default=64, help="fixed tree budget")
 ap.add_argument("--context", type=int, default=2048)
 ap.add_argument("--tokens", type=int, default=64, help="new tokens per request in the timed region")
 ap.add_argument("--warmup-cycles", type=int, default=3)
+ap.add_argument("--policy", default="fixed", choices=["fixed", "adaptive"],
+                help="adaptive: batch-aware Algorithm 1 per request with N_max = --n (ragged verify)")
 a = ap.parse_args()
 
 world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -47,6 +49,13 @@ max_ctx = a.context + 1 + (a.warmup_cycles + a.tokens + 16) * 17 + 64
 t0 = time.time()
 be = BatchEngine(cfg, DrafterConfig(layers=5, gamma=16, logit_scale=6.0), n_req=len(shard), n_fixed=a.n,
                  max_ctx=max_ctx, seed=0)
+if a.policy == "adaptive":
+    import paper_2605_29727_b200 as P
+    pk = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {}
+    params = cfg.cost_params(pk.get("bf16_tflops", 1590.0) * 1e12, pk.get("hbm_gbs", 6650.0) * 1e9)
+    est = P.VerifyLatencyEstimator(params, variant="static")  # uncalibrated roofline curve
+    lat = P.CycleLatencies(t_draft=est.estimate(17, a.context), t_aux=0.0, l_ar=est.estimate(1, a.context))
+    be.set_policy("adaptive", estimator=est, latencies=lat)
 be.reset(prompts)
 for _ in range(a.warmup_cycles):
     be.cycle()
@@ -78,9 +87,10 @@ if world > 1:
 if rank == 0:
     print(json.dumps({
         "config": "config3", "requests": a.requests, "n_gpus": world, "requests_per_gpu": len(shard),
-        "fixed_budget": a.n, "context": a.context, "value": tokens / t, "unit": "tokens/s",
+        "fixed_budget": a.n, "policy": a.policy, "context": a.context, "value": tokens / t, "unit": "tokens/s",
         "tokens": tokens, "seconds": t, "cycles": cycles, "ms_per_cycle": t / cycles * 1e3,
         "mean_accept_len": tokens / (cycles * a.requests), "graph_kernels_per_cycle": be.graph_kernels,
+        "mean_rows_per_cycle": getattr(be, "last_rows", None) if a.policy == "adaptive" else a.requests * (a.n + 1),
         "setup_s": round(t_setup, 1), "scaling": "weak-per-request (64 requests sharded)",
         "data": "synthetic (random-init bf16 weights, uniform random prompts, seeds 0..63)"}), flush=True)
 if world > 1:
