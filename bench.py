@@ -274,14 +274,17 @@ def gemm_replay_roofline(eng, cfg, peaks: dict, s_med: int) -> dict:
     g_time = statistics.median(reps[1:])
     g_bytes = sum(w.numel() * 2 + x.shape[0] * w.shape[1] * 2 for w, x in seq)
     achieved = g_bytes / g_time / 1e9
-    traffic = None
-    prof = ROOT / "profiles" / "gemm_dram_bytes.json"
-    if prof.exists():
-        traffic = json.loads(prof.read_text()).get("dram_bytes_per_launch")
+    # ncu --set full DRAM bytes per launch of the same 145-launch sequence, from the capture
+    # (profiles/gemm_dram_bytes*.json) whose row count is nearest to this step's
+    traffic, traffic_m = None, None
+    for prof in sorted((ROOT / "profiles").glob("gemm_dram_bytes*.json")):
+        d = json.loads(prof.read_text())
+        if traffic_m is None or abs(d.get("m", 0) - s_med) < abs(traffic_m - s_med):
+            traffic, traffic_m = d.get("dram_bytes_per_launch"), d.get("m")
     del gg
     return {"bound": "hbm", "kernel": "gemm_bf16_kernel (K4, tcgen05 weight streaming)", "achieved": achieved,
             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-            "peak_src": peaks["src"], "avg_launch_us": 1e6 * g_time / len(seq),
+            "peak_src": peaks["src"], "avg_launch_us": 1e6 * g_time / len(seq), "traffic_m": traffic_m,
             "algorithmic_bytes": f"bf16 weights + X rows per launch, 36x(qkv,o,gate_up,down)+lm_head at m={s_med}",
             "timing": "CUDA events around a graph of the step's 145 GEMM launches (back to back, PDL)"}
 

@@ -5,6 +5,7 @@ import subprocess
 import sys
 
 rep, out = sys.argv[1], sys.argv[2]
+m = int(sys.argv[3]) if len(sys.argv) > 3 else 32  # token rows of the captured launches (gemm_one.py m)
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(raw.splitlines()))
 hdr, units = rows[0], rows[1]
@@ -19,7 +20,6 @@ def val(r, k):
 names = ["qkv", "o", "gate_up", "down", "lm_head"]
 shapes = {"qkv": (6144, 4096), "o": (4096, 4096), "gate_up": (24576, 4096), "down": (4096, 12288),
           "lm_head": (151936, 4096)}
-m = 32
 per = {}
 for i, n in enumerate(names):
     sub = rows[2 + 3 * i: 5 + 3 * i]
