@@ -344,11 +344,18 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # BST_BENCH_DEVICE / BST_DIST_BACKEND=gloo: exercise the N > 1 code path with several ranks
+    # on one GPU (the 1-GPU test pool); the driver's runs use one GPU per rank and NCCL
+    local = int(os.environ.get("BST_BENCH_DEVICE", local))
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BST_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     peaks = load_peaks()
     cfg = MODELS[args.model]
     pdict = cost_params_dict(peaks)
