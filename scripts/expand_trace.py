@@ -14,14 +14,14 @@ lib.bst_debug_expand_trace.argtypes = [C.c_void_p]
 tr = torch.zeros(16, dtype=torch.int64, device="cuda")
 logits = (torch.randn(16, 151936, device="cuda") * 6).to(torch.bfloat16)
 tok, prob = lattice_from_logits(logits, 8)
-for n in (31, 255):
-    dt = DeviceTree(255)
-    expand_device(tok, prob, _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n), 255, dt)
+for n, cap in ((31, 255), (111, 1024), (255, 255), (255, 1024)):
+    dt = DeviceTree(cap)
+    expand_device(tok, prob, _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n), cap, dt)
     torch.cuda.synchronize()
     lib.bst_debug_expand_trace(tr.data_ptr())
-    expand_device(tok, prob, _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n), 255, dt)
+    expand_device(tok, prob, _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n), cap, dt)
     torch.cuda.synchronize()
     lib.bst_debug_expand_trace(None)
     t = tr.cpu().tolist()
     names = ["dp", "enumerate", "sort", "ties", "output", "finish"]
-    print(n, "enum", int(dt.meta[4].item()), " ".join(f"{nm}={(t[i + 1] - t[i]) / 1000:.1f}us" for i, nm in enumerate(names)))
+    print(n, "cap", cap, "enum", int(dt.meta[4].item()), " ".join(f"{nm}={(t[i + 1] - t[i]) / 1000:.1f}us" for i, nm in enumerate(names)))
