@@ -259,8 +259,15 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
 
 // ------------------------------------------------------------- enumeration
 // Enumerate every node with rho >= tau (rho > 0).  Returns false on overflow.
+// Level d's candidates are the (parent at level d-1, lattice rank) pairs; a row's
+// probabilities are sorted descending, so the kept children of a parent are a prefix
+// (the reference's break at the first child below tau).  Slots inside a level come from
+// warp-aggregated atomics: the enumeration order inside a level is arbitrary, which is
+// safe because the final order is the sort by (rho, depth, token) with exact ties
+// repaired by the parent's sorted position (fix_ties), never by enumeration index.
 __device__ bool enumerate_nodes(const int32_t* tok, const double* prob, int gamma, int k, double tau,
                                 ExSmem& sm) {
+  const int lane = threadIdx.x & 31;
   if (threadIdx.x == 0) { sm.n_enum = 0; sm.overflow = 0; sm.lvl_start[1] = 0; sm.max_depth = 0; }
   __syncthreads();
   int prev_lo = 0, prev_hi = 0;  // enumeration range of the previous level (root for d=1)
@@ -268,53 +275,49 @@ __device__ bool enumerate_nodes(const int32_t* tok, const double* prob, int gamm
     const double* pr = prob + (size_t)(d - 1) * k;
     const int32_t* tr = tok + (size_t)(d - 1) * k;
     const int n_par = d == 1 ? 1 : prev_hi - prev_lo;
-    const int per = (n_par + EX_THREADS - 1) / EX_THREADS;
-    const int p0 = threadIdx.x * per;
-    int cnt = 0;
-    for (int q = 0; q < per; ++q) {
-      int pi = p0 + q;
-      if (pi >= n_par) break;
-      double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
-      for (int r = 0; r < k; ++r) {
-        double v = __dmul_rn(prho, pr[r]);
-        if (!(v > 0.0) || v < tau) break;
-        ++cnt;
+    const int base = sm.lvl_start[d];
+    const int n_items = n_par * k;
+    for (int i0 = 0; i0 < n_items; i0 += EX_THREADS) {
+      const int item = i0 + threadIdx.x;
+      int pi = 0, r = 0;
+      double v = 0.0;
+      bool take = false;
+      if (item < n_items) {
+        pi = item / k;
+        r = item - pi * k;
+        const double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
+        v = __dmul_rn(prho, pr[r]);
+        take = v > 0.0 && !(v < tau);
       }
-    }
-    int total;
-    int off = block_excl_scan(cnt, sm.scan, &total);
-    const int base = sm.n_enum;
-    if (base + total > EX_CAP) {
-      if (threadIdx.x == 0) sm.overflow = 1;
-      __syncthreads();
-      return false;
-    }
-    int w = base + off;
-    for (int q = 0; q < per; ++q) {
-      int pi = p0 + q;
-      if (pi >= n_par) break;
-      double prho = d == 1 ? 1.0 : bitsd(~sm.hi[prev_lo + pi]);
-      for (int r = 0; r < k; ++r) {
-        double v = __dmul_rn(prho, pr[r]);
-        if (!(v > 0.0) || v < tau) break;
-        sm.hi[w] = ~dbits(v);
-        sm.lo[w] = ((unsigned long long)d << 40) | ((unsigned long long)(unsigned)tr[r] << 16) |
-                   (unsigned long long)w;
-        sm.par[w] = d == 1 ? NO_PARENT : (unsigned short)(prev_lo + pi);
-        sm.rnk[w] = (unsigned char)r;
-        ++w;
+      const unsigned bal = __ballot_sync(0xffffffffu, take);
+      int slot0 = 0;
+      if (lane == 0 && bal) slot0 = atomicAdd(&sm.n_enum, __popc(bal));
+      slot0 = __shfl_sync(0xffffffffu, slot0, 0);
+      if (take) {
+        const int w = slot0 + __popc(bal & ((1u << lane) - 1u));
+        if (w < EX_CAP) {
+          sm.hi[w] = ~dbits(v);
+          sm.lo[w] = ((unsigned long long)d << 40) | ((unsigned long long)(unsigned)tr[r] << 16) |
+                     (unsigned long long)w;
+          sm.par[w] = d == 1 ? NO_PARENT : (unsigned short)(prev_lo + pi);
+          sm.rnk[w] = (unsigned char)r;
+        } else {
+          sm.overflow = 1;
+        }
       }
     }
     __syncthreads();
+    const int top = sm.n_enum;
+    if (sm.overflow || top > EX_CAP) return false;
+    const int total = top - base;
     if (threadIdx.x == 0) {
-      sm.n_enum = base + total;
-      sm.lvl_start[d + 1] = base + total;
+      sm.lvl_start[d + 1] = top;
       if (total > 0) sm.max_depth = d;
     }
     __syncthreads();
     if (total == 0) break;
     prev_lo = base;
-    prev_hi = base + total;
+    prev_hi = top;
   }
   return true;
 }
@@ -324,28 +327,73 @@ __device__ __forceinline__ bool key_gt(unsigned long long ah, unsigned long long
   return ah > bh || (ah == bh && al > bl);
 }
 
+// Compare-exchange helpers of the register stages: 128-bit keys (hi, lo), unique except
+// the ~0 padding (equal keys never swap).
+__device__ __forceinline__ void reg_cas(unsigned long long& ah, unsigned long long& al, unsigned long long& bh,
+                                        unsigned long long& bl, bool asc) {
+  if (key_gt(ah, al, bh, bl) == asc) {
+    unsigned long long th = ah, tl = al;
+    ah = bh; al = bl; bh = th; bl = tl;
+  }
+}
+__device__ __forceinline__ void reg_xchg(unsigned long long& h, unsigned long long& l, int j, bool lower, bool asc) {
+  const unsigned long long oh = __shfl_xor_sync(0xffffffffu, h, j), ol = __shfl_xor_sync(0xffffffffu, l, j);
+  // the lower position keeps the smaller key when ascending, the larger when descending
+  const bool other_smaller = key_gt(h, l, oh, ol);
+  if (lower == asc ? other_smaller : !other_smaller && !(oh == h && ol == l)) { h = oh; l = ol; }
+}
+
+// Bitonic sort of (hi, lo) over p2 = next power of two >= max(n, 64) keys.  Stages with
+// j >= 64 compare across warp blocks through shared memory (block / named barrier per
+// stage); each run of stages with j <= 32 touches only one aligned block of 64 keys per
+// warp and runs in registers (2 keys per lane: block positions lane and lane + 32; j = 32
+// inside the lane, j <= 16 by shuffles), so shared memory is read and written once per run.
 __device__ void bitonic_sort(ExSmem& sm, int n) {
-  int p2 = 1;
+  int p2 = 64;
   while (p2 < n) p2 <<= 1;
   for (int i = n + threadIdx.x; i < p2; i += EX_THREADS) { sm.hi[i] = ~0ull; sm.lo[i] = ~0ull; }
   __syncthreads();
-  // only as many warps as there are compare-exchange pairs take part (named barrier)
-  const int active = min(EX_THREADS, max(32, p2 >> 1));
+  const int active = min(EX_THREADS, p2 >> 1);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = active >> 5;
+  auto bar = [&]() {
+    if (active == EX_THREADS) __syncthreads();
+    else asm volatile("bar.sync 2, %0;" ::"r"(active));
+  };
   if (threadIdx.x < active) {
     for (int kk = 2; kk <= p2; kk <<= 1) {
-      for (int j = kk >> 1; j > 0; j >>= 1) {
+      int j = kk >> 1;
+      for (; j >= 64; j >>= 1) {  // cross-block stages
         for (int i = threadIdx.x; i < (p2 >> 1); i += active) {
-          int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
-          int b = a + j;
-          bool asc = (a & kk) == 0;
+          const int a = ((i & ~(j - 1)) << 1) | (i & (j - 1));
+          const int b = a + j;
+          const bool asc = (a & kk) == 0;
           unsigned long long ah = sm.hi[a], al = sm.lo[a], bh = sm.hi[b], bl = sm.lo[b];
           if (key_gt(ah, al, bh, bl) == asc) {
             sm.hi[a] = bh; sm.lo[a] = bl; sm.hi[b] = ah; sm.lo[b] = al;
           }
         }
-        if (active == EX_THREADS) __syncthreads();
-        else asm volatile("bar.sync 2, %0;" ::"r"(active));
+        bar();
       }
+      // register run: stages j .. 1 (j <= 32); for kk <= 64 the runs of kk = 2 .. 64 merge
+      if (kk < 64 && kk < p2) continue;  // handled by the kk = 64 run below
+      for (int blk = warp; blk < (p2 >> 6); blk += nwarps) {
+        const int base = blk << 6;
+        const int p0 = base + lane, p1 = p0 + 32;
+        unsigned long long h0 = sm.hi[p0], l0 = sm.lo[p0], h1 = sm.hi[p1], l1 = sm.lo[p1];
+        const int k_lo = kk <= 64 ? 2 : kk;  // first stage group of this run
+        for (int kq = k_lo; kq <= kk; kq <<= 1) {
+          for (int jj = (kq == kk ? min(j, 32) : (kq >> 1)); jj > 0; jj >>= 1) {
+            if (jj == 32) {
+              reg_cas(h0, l0, h1, l1, (p0 & kq) == 0);
+            } else {
+              reg_xchg(h0, l0, jj, (p0 & jj) == 0, (p0 & kq) == 0);
+              reg_xchg(h1, l1, jj, (p1 & jj) == 0, (p1 & kq) == 0);
+            }
+          }
+        }
+        sm.hi[p0] = h0; sm.lo[p0] = l0; sm.hi[p1] = h1; sm.lo[p1] = l1;
+      }
+      bar();
     }
   }
   __syncthreads();
@@ -464,6 +512,11 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
     }
   }
   __syncthreads();
+  // a_hat / S_hat scratch in shared memory when they fit (the staged lattice is dead now)
+  const bool ah_smem = in_smem && n_eval <= 2048;
+  double* ahat = ah_smem ? sm.lat_p : ws.ahat;
+  const bool sh_smem = in_smem && n_eval <= 1024;
+  double* shat_s = sh_smem ? reinterpret_cast<double*>(sm.lat_t) : (out.trace ? out.trace : ws.shat);
   if (threadIdx.x == 0) {
     // controller.py:85 / draft_tree.py:153 addition order; 8 loads in flight per step
     double a = 1.0;
@@ -476,27 +529,28 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           a = __dadd_rn(a, r[k]);
-          ws.ahat[i + k] = a;
+          ahat[i + k] = a;
         }
       }
       for (; i < n_eval; ++i) {
         a = __dadd_rn(a, rho_s[i + 1]);
-        ws.ahat[i] = a;
+        ahat[i] = a;
       }
     } else {
       for (; i < n_eval; ++i) {
         a = __dadd_rn(a, out.rho[i + 1]);
-        ws.ahat[i] = a;
+        ahat[i] = a;
       }
     }
   }
   __syncthreads();
   int n_nodes = n_eval, n_expanded = n_eval, stop = -1;
   if (adaptive && n_eval > 0) {
-    double* shat = out.trace ? out.trace : ws.shat;
+    double* shat = shat_s;
     for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
       double c_hat = __dadd_rn(plan.fixed_cost, curve_latency(plan.curve, (long long)i + 2));
-      shat[i] = __ddiv_rn(__dmul_rn(__dadd_rn(ws.ahat[i], plan.a_offset), plan.l_ar), c_hat);
+      shat[i] = __ddiv_rn(__dmul_rn(__dadd_rn(ahat[i], plan.a_offset), plan.l_ar), c_hat);
+      if (sh_smem && out.trace) out.trace[i] = shat[i];
     }
     if (threadIdx.x == 0) { sm.min_stop = 0x7fffffff; }
     __syncthreads();
@@ -553,19 +607,32 @@ __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive
     out.meta[2] = stop;
     out.meta[3] = algo_used;
     out.meta[4] = enumerated;
-    out.surrogate[0] = n_nodes > 0 ? ws.ahat[n_nodes - 1] : 1.0;
+    out.surrogate[0] = n_nodes > 0 ? ahat[n_nodes - 1] : 1.0;
   }
   // ancestor-or-self bitmask rows 0..n_nodes (walks parents in smem)
   if (out.anc_mask) {
     const int W = out.mask_words;
+    // ancestors are visited in decreasing index order, so each word of the row is
+    // complete when the walk leaves it: every word is stored once, zeros included
     for (int i = threadIdx.x; i <= n_nodes; i += EX_THREADS) {
       uint32_t* row = out.anc_mask + (size_t)i * W;
-      for (int w = 0; w < W; ++w) row[w] = 0u;
+      int w_hi = W - 1, cur_w = i >> 5;
+      uint32_t bits = 0u;
       int j = i;
-      while (j >= 0) {
-        row[j >> 5] |= 1u << (j & 31);
+      while (true) {
+        const int jw = j >= 0 ? (j >> 5) : -1;
+        if (jw != cur_w) {
+          for (; w_hi > cur_w; --w_hi) row[w_hi] = 0u;
+          row[cur_w] = bits;
+          w_hi = cur_w - 1;
+          bits = 0u;
+          cur_w = jw;
+          if (j < 0) break;
+        }
+        bits |= 1u << (j & 31);
         j = j == 0 ? -1 : (in_smem ? par_s[j] : out.parent[j]);
       }
+      for (; w_hi >= 0; --w_hi) row[w_hi] = 0u;
     }
   }
   // children CSR: counts in smem, block exclusive scan, stable fill by child id

@@ -12,9 +12,9 @@ from paper_2605_29727_b200.lattice import lattice_from_logits  # noqa: E402
 lib = _lib.lib()
 lib.bst_debug_expand_trace.argtypes = [C.c_void_p]
 tr = torch.zeros(16, dtype=torch.int64, device="cuda")
-logits = (torch.randn(16, 151936, device="cuda") * 6).to(torch.bfloat16)
+logits = torch.randn(16, 151936, device="cuda") * 6  # fp32, as the engine's LM head
 tok, prob = lattice_from_logits(logits, 8)
-for n, cap in ((31, 255), (111, 1024), (255, 255), (255, 1024)):
+for n, cap in ((31, 255), (111, 1024), (255, 1024), (1024, 1024)):
     dt = DeviceTree(cap)
     expand_device(tok, prob, _lib.Plan(policy=_lib.POLICY_FIXED, n_max=n), cap, dt)
     torch.cuda.synchronize()
