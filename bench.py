@@ -289,13 +289,16 @@ def gemm_replay_roofline(eng, cfg, peaks: dict, s_med: int) -> dict:
             "timing": "CUDA events around a graph of the step's 145 GEMM launches (back to back, PDL)"}
 
 
-def run_config3(args, world: int, rank: int, local: int, cfg, peaks: dict) -> dict | None:
+def run_config3(args, world: int, rank: int, local: int, cfg, peaks: dict, policy: str = "adaptive") -> dict | None:
     """BASELINE config 3 at N GPUs: 64 requests (prompt seeds 0..63) sharded contiguously,
-    each rank decodes its shard batched in one BatchEngine (fixed N = 64), no collective on
-    the data path; tokens/s = all committed tokens / max over ranks of the device time."""
+    each rank decodes its shard batched in one BatchEngine, no collective on the data path;
+    tokens/s = all committed tokens / max over ranks of the device time.  policy "adaptive":
+    per-request Algorithm 1 with the batch-aware verify curve (N_max = --c3-budget, ragged
+    verify), "fixed": every tree has N = --c3-budget nodes."""
     import numpy as np
     import torch
 
+    import paper_2605_29727_b200 as P
     from paper_2605_29727_b200.dist import reduce_throughput, shard
     from paper_2605_29727_b200.engine.batch import BatchEngine
     from paper_2605_29727_b200.engine.config import DrafterConfig
@@ -304,7 +307,13 @@ def run_config3(args, world: int, rank: int, local: int, cfg, peaks: dict) -> di
     cycles = args.c3_cycles
     be = BatchEngine(cfg, DrafterConfig(layers=5, gamma=16, logit_scale=args.logit_scale), n_req=len(mine),
                      n_fixed=args.c3_budget, max_ctx=args.context + 17 * (cycles + 8) + 64, seed=0)
+    if policy == "adaptive":
+        params = cfg.cost_params(peaks["bf16_tflops"] * 1e12, peaks["hbm_gbs"] * 1e9)
+        est = P.VerifyLatencyEstimator(params, variant="static")  # roofline curve (batch shift on device)
+        lat = P.CycleLatencies(t_draft=est.estimate(17, args.context), t_aux=0.0, l_ar=est.estimate(1, args.context))
+        be.set_policy("adaptive", estimator=est, latencies=lat)
     be.reset(prompts)
+    be.precapture()  # adaptive: every 64-row verify bucket's graph before anything is timed
     for _ in range(3):
         be.cycle()
     base = be.committed_counts().copy()
@@ -314,18 +323,24 @@ def run_config3(args, world: int, rank: int, local: int, cfg, peaks: dict) -> di
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(be.stream)
+    rows = []
     for _ in range(cycles):
         be.cycle()
+        rows.append(be.last_rows if policy == "adaptive" else len(mine) * (args.c3_budget + 1))
     e1.record(be.stream)
     e1.synchronize()
     t = e0.elapsed_time(e1) * 1e-3
     tokens = float((be.committed_counts() - base).sum())
     t_max, tok_all, value = reduce_throughput(t, tokens)
+    desc = (f"adaptive (batch-aware Algorithm 1 per request, N_max={args.c3_budget}, ragged verify)"
+            if policy == "adaptive" else f"fixed N={args.c3_budget}")
     out = {"workload": f"config3: {args.c3_requests} requests (Qwen3-8B shape, 2048-token prompts) sharded "
-                       f"data-parallel over {world} GPU(s), batched per GPU, fixed N={args.c3_budget}",
+                       f"data-parallel over {world} GPU(s), batched per GPU, {desc}",
            "value": value, "unit": "tokens/s", "n_gpus": world, "requests_per_gpu": len(mine),
            "cycles": cycles, "ms_per_cycle": 1e3 * t_max / cycles, "scaling": "strong (64 requests in total)",
-           "graph_kernels_per_cycle": be.graph_kernels, "mean_accept_len": tok_all / (cycles * args.c3_requests)}
+           "verify_rows_per_cycle_mean": statistics.mean(rows), "mean_accept_len": tok_all / (cycles * args.c3_requests)}
+    if policy == "fixed":
+        out["graph_kernels_per_cycle"] = be.graph_kernels
     del be
     torch.cuda.empty_cache()
     return out
@@ -529,12 +544,13 @@ def run_ours(args) -> None:
                     "sample": f"config 3: {c3['streams']} reference decode streams x {c3['cycles_per_stream']} cycles, "
                               f"a process pool of {c3['workers']} workers (sp/harness.py:249-252), wall clock"}
 
-    c3 = None
+    c3 = c3f = None
     if not args.no_config3:
         _log("config 3 GPU leg")
         del eng
         torch.cuda.empty_cache()
-        c3 = run_config3(args, world, rank, local, cfg, peaks)
+        c3 = run_config3(args, world, rank, local, cfg, peaks, "adaptive")
+        c3f = run_config3(args, world, rank, local, cfg, peaks, "fixed")
 
     if rank != 0:
         if dist:
@@ -575,6 +591,8 @@ def run_ours(args) -> None:
         line["cpu_baseline_config3"] = cpu3
     if c3:
         line["config3"] = c3
+    if c3f:
+        line["config3_fixed"] = c3f
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()

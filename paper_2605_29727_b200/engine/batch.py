@@ -304,6 +304,21 @@ class BatchEngine:
             g.replay()
         return total
 
+    def precapture(self, max_rows: int | None = None) -> int:
+        """Adaptive policy: capture the verify graph of every 64-row bucket up to max_rows
+        (default rows_cap) and the draft graph now, so no capture lands inside a timed
+        loop.  The decode state is restored by each capture.  Returns the graph count."""
+        if self.policy != _lib.POLICY_ADAPTIVE or not self.use_graphs:
+            return 0
+        top = min(self.rows_cap, max_rows or self.rows_cap)
+        if self.graph_d is None:
+            self.graph_d = self._capture_fn(self._draft_ragged)
+        for rows in range(64, -(-top // 64) * 64 + 1, 64):
+            rows = min(rows, self.rows_cap)
+            if rows not in self.graphs_v:
+                self.graphs_v[rows] = self._capture_fn(lambda r=rows: self._verify_ragged(r))
+        return len(self.graphs_v)
+
     def _capture(self) -> torch.cuda.CUDAGraph:
         g = self._capture_fn(self._cycle_body)
         self.graph_kernels = self.graph_nodes[id(g)]

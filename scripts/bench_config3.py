@@ -57,6 +57,7 @@ if a.policy == "adaptive":
     lat = P.CycleLatencies(t_draft=est.estimate(17, a.context), t_aux=0.0, l_ar=est.estimate(1, a.context))
     be.set_policy("adaptive", estimator=est, latencies=lat)
 be.reset(prompts)
+be.precapture()  # adaptive: capture every verify bucket before timing
 for _ in range(a.warmup_cycles):
     be.cycle()
 base = be.committed_counts().copy()
