@@ -183,3 +183,28 @@ def test_ragged_adaptive_batch_trees_follow_the_batch_plan():
         eng.reset(prompts[r])
         toks = be.tokens(r)
         assert toks == eng.ar_decode(len(toks)), r
+
+
+def test_ragged_adaptive_precapture_changes_nothing():
+    """BatchEngine.precapture (every 64-row verify bucket captured before timing) leaves the
+    decode untouched: the same committed streams and per-cycle logs as capturing lazily."""
+    from paper_2605_29727_b200.engine.batch import BatchEngine
+    from paper_2605_29727_b200.engine.config import TINY, DrafterConfig
+    dcfg = DrafterConfig(layers=2, gamma=8, logit_scale=4.0)
+    _, est, lat = _adaptive(48)
+    prompts = _prompts(3, 100, TINY.V)
+    out = []
+    for pre in (False, True):
+        be = BatchEngine(TINY, dcfg, n_req=3, n_fixed=48, max_ctx=640, seed=0)
+        be.set_attention_splits(1)
+        be.set_policy("adaptive", estimator=est, latencies=lat)
+        be.reset(prompts)
+        if pre:
+            assert be.precapture() == -(-be.rows_cap // 64)
+        for _ in range(6):
+            be.cycle()
+        out.append(([be.tokens(r) for r in range(3)], be.log_i32[:, :48].cpu().numpy().copy()))
+        del be
+        torch.cuda.empty_cache()
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
