@@ -479,13 +479,15 @@ __device__ void cluster_split_merge(const AttnArgs& a, const float* ms, const fl
 // warp 0: TMA producer (K/V pages, 4-stage ring); warp 1: TMEM owner + single
 // issuing thread; warps 2-5: one thread per query row — Q staging, tcgen05.ld of
 // S, mask + online softmax (lazy O rescale when the row max grows by > 2^8),
-// P -> smem (K-major, 128B swizzle), epilogue.  TMEM: S double buffer (2 x 64
-// columns) + O (128 columns).  V is consumed as an MN-major UMMA operand.
+// bf16 P -> tensor memory (tcgen05.st), epilogue.  TMEM: S double buffer (2 x 64
+// columns), O (128 columns), P double buffer (2 x 32 columns, 2 bf16 per column).
+// O += P V reads P from TMEM as the A operand (TS-mode tcgen05.mma: no shared-memory
+// P, no async-proxy fence per tile) and V from shared memory as an MN-major operand.
 // ===========================================================================
 constexpr int T_THREADS = 192;
 constexpr int T_STAGES = 4;
 constexpr int T_Q_BYTES = 128 * A_D * 2;   // 32 KiB: two [128 rows][64] SW128 halves
-constexpr int T_P_BYTES = 2 * 128 * A_PAGE * 2; // 2 x 16 KiB: double-buffered [128 rows][64 keys]
+constexpr int T_PCOL = 256;  // TMEM: S 0-127 (double buffer), O 128-255, bf16 P 256-319 (double buffer, 32 each)
 constexpr float T_RESCALE = 8.f;            // log2 units
 
 __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
@@ -500,10 +502,9 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-  const uint32_t sQ = base, sP = base + T_Q_BYTES, sKV = sP + T_P_BYTES;
+  const uint32_t sQ = base, sKV = base + T_Q_BYTES;
   uint8_t* gQ = smem;
-  uint8_t* gP = smem + T_Q_BYTES;
-  uint8_t* gKV = gP + T_P_BYTES;
+  uint8_t* gKV = smem + T_Q_BYTES;
 
   const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
   const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
@@ -527,7 +528,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     sm100::mbar_init(&q_ready, 4);
     sm100::fence_mbar_init();
   }
-  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 256);
+  if (warp == 1) sm100::tmem_alloc(&tmem_sh, 512);  // S, O and P: 320 columns
   sm100::tc_fence_before();
   __syncthreads();
   sm100::tc_fence_after();
@@ -593,9 +594,8 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
           const uint32_t vb = sKV + stj * A_STAGE_BYTES + A_TILE_BYTES;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk) {
-            const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
             const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
-            sm100::umma_f16(tmem + 128, ad, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
+            sm100::umma_f16_ts(tmem + 128, tmem + T_PCOL + 32 * (j & 1) + 8 * kk, bd, idO, (j > 0 || kk > 0) ? 1u : 0u);
           }
           sm100::umma_commit(&o_done[j & 1]);
           sm100::umma_commit(&empty[stj]);
@@ -710,11 +710,10 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       }
       l_run = rescale ? l_run * alpha + rs : l_run + rs;
       m_run = m_ref;
-#pragma unroll
-      for (int cq = 0; cq < 8; ++cq)
-        *reinterpret_cast<uint4*>(gP + (i & 1) * (128 * 128) + row * 128 + ((cq ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
-      sm100::fence_async_shared();
+      // bf16 P into tensor memory (A operand of the PV MMA), buffer i & 1
+      sm100::tmem_st16u(lane_base + T_PCOL + 32 * (i & 1), pk);
+      sm100::tmem_st16u(lane_base + T_PCOL + 32 * (i & 1) + 16, pk + 16);
+      sm100::tmem_st_wait();
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&p_full);
@@ -784,7 +783,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   __syncthreads();
   if (warp == 1) {
     sm100::tc_fence_after();
-    sm100::tmem_dealloc(tmem, 256);
+    sm100::tmem_dealloc(tmem, 512);
   }
   if (threadIdx.x == 0) BND(a.seq, 1);
 }
@@ -805,6 +804,7 @@ constexpr int T2_KS = BST_T2_KS, T2_VS = BST_T2_VS;
 #endif
 constexpr int T2_MIN_PAGES = BST_T2_MIN_PAGES;  // per-CTA page run from which the two-group kernel is used
 constexpr int T2_LCOL = 384;  // TMEM: S 0-127, O 128-383, row sums 384-415 (16 columns per group)
+constexpr int T2_PCOL = 416;  // bf16 P of group g in columns 416 + 32 g .. + 32 (A operand of PV / row sums)
 constexpr int T2_THREADS = 384;  // warps 0-1 K TMA / S issuer, 2-9 softmax groups, 10 V TMA, 11 PV issuer
 
 __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_constant__ CUtensorMap tmKV, AttnArgs a) {
@@ -818,11 +818,10 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t base = (sm100::smem_u32(smem_raw) + 1023) & ~1023u;
   uint8_t* smem = smem_raw + (base - sm100::smem_u32(smem_raw));
-  const uint32_t sQ = base, sP = base + T_Q_BYTES, sK = sP + T_P_BYTES, sV = sK + T2_KS * A_TILE_BYTES;
+  const uint32_t sQ = base, sK = base + T_Q_BYTES, sV = sK + T2_KS * A_TILE_BYTES;
   const uint32_t sOnes = sV + T2_VS * A_TILE_BYTES;  // [16][64] bf16 ones: B operand of the row-sum MMA
   uint8_t* gQ = smem;
-  uint8_t* gP = smem + T_Q_BYTES;
-  uint8_t* gKV = gP + T_P_BYTES;  // K ring, then V ring; reused as the merge staging buffer
+  uint8_t* gKV = smem + T_Q_BYTES;  // K ring, then V ring; reused as the merge staging buffer
 
   const int head = blockIdx.x, split = blockIdx.y, req = blockIdx.z / a.row_blocks, rb = blockIdx.z % a.row_blocks;
   const int c_ctx = a.state ? a.state[req * a.req_state + a.c_idx] : a.c;
@@ -923,15 +922,15 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
         const uint32_t vb = sV + stj * A_TILE_BYTES;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {
-          const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
           const uint64_t bd = sm100::desc_mn_sw128(vb + kk * 2048, A_PAGE * 128);
-          sm100::umma_f16(tmem + 128 + (j & 1) * A_D, ad, bd, idO, (j > 1 || kk > 0) ? 1u : 0u);
+          sm100::umma_f16_ts(tmem + 128 + (j & 1) * A_D, tmem + T2_PCOL + 32 * (j & 1) + 8 * kk, bd, idO,
+                             (j > 1 || kk > 0) ? 1u : 0u);
         }
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk) {  // row sums of P: l += P x ones (the same bf16 P as the numerator)
-          const uint64_t ad = sm100::desc_k_sw128(sP + (j & 1) * (128 * 128) + kk * 32);
           const uint64_t bd = sm100::desc_k_sw128(sOnes + kk * 32);
-          sm100::umma_f16(tmem + T2_LCOL + (j & 1) * 16, ad, bd, idL, (j > 1 || kk > 0) ? 1u : 0u);
+          sm100::umma_f16_ts(tmem + T2_LCOL + (j & 1) * 16, tmem + T2_PCOL + 32 * (j & 1) + 8 * kk, bd, idL,
+                             (j > 1 || kk > 0) ? 1u : 0u);
         }
         sm100::umma_commit(&o_done[j & 1]);
         sm100::umma_commit(&emptyV[stj]);
@@ -1039,11 +1038,11 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
         sm100::tmem_st_wait();
       }
       m_run = m_ref;
-#pragma unroll
-      for (int cq = 0; cq < 8; ++cq)
-        *reinterpret_cast<uint4*>(gP + g * (128 * 128) + row * 128 + ((cq ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * cq], pk[4 * cq + 1], pk[4 * cq + 2], pk[4 * cq + 3]);
-      sm100::fence_async_shared();
+      // bf16 P straight into tensor memory: the PV / row-sum MMAs read it as their A
+      // operand (no shared-memory round trip, no proxy fence)
+      sm100::tmem_st16u(lane_base + T2_PCOL + 32 * g, pk);
+      sm100::tmem_st16u(lane_base + T2_PCOL + 32 * g + 16, pk + 16);
+      sm100::tmem_st_wait();
       sm100::tc_fence_before();
       __syncwarp();
       if (lane == 0) sm100::mbar_arrive(&p_full[g]);
@@ -2029,8 +2028,8 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     return BST_OK;
   }
   static bool attr = false;
-  const int smem_tc = T_Q_BYTES + T_P_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
-  const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
+  const int smem_tc = T_Q_BYTES + T_STAGES * A_STAGE_BYTES + 1024;
+  const int smem_tc2 = T_Q_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
   if (!attr) {
     BST_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc));
     BST_CUDA(cudaFuncSetAttribute(attn_tc2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_tc2));
@@ -2225,6 +2224,6 @@ extern "C" int bst_debug_bnd_trace_attn(void* buf) {  // BST_TRACE builds only
 // debug: resident clusters of `cs` two-group attention CTAs at the kernel's shared memory
 extern "C" int bst_debug_tc2_cluster_fits(int cs) {
   using namespace bst;
-  const int smem_tc2 = T_Q_BYTES + T_P_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
+  const int smem_tc2 = T_Q_BYTES + (T2_KS + T2_VS) * A_TILE_BYTES + 2048 + 1024;
   return rm_cluster_fits(true, cs, smem_tc2);
 }
