@@ -336,17 +336,24 @@ __device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req,
   const int per = (Rb + ns - 1) / ns, r0 = split * per, nr = min(r0 + per, Rb) - r0;
   const float2* ml_all = reinterpret_cast<const float2*>(a.ws_ml);
   const float4* o_all = reinterpret_cast<const float4*>(a.ws_o);
-  for (int it = t; it < nr * 32; it += 256) {
+  // two lanes per (row, 16-byte chunk) item: lane h merges the splits h, h + 2, ... (one
+  // batch of loads for up to 20 splits), then the pair combines over a shuffle; fixed
+  // assignment and combine order: deterministic
+  constexpr int MH = 10;
+  for (int it2 = t; it2 < nr * 64; it2 += 256) {
+    const unsigned am = __activemask();  // pairs (2i, 2i+1) are always active together
+    const int it = it2 >> 1, h = it2 & 1;
     const int rr = row0 + r0 + it % nr, d4 = it / nr;  // lanes walk rows: coalesced
     float M = -INFINITY, L = 0.f;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int j0 = 0; j0 < ns; j0 += 16) {
-      float2 ml[16];
-      float4 v[16];
+    for (int j0 = h; j0 < ns; j0 += 2 * MH) {
+      float2 ml[MH];
+      float4 v[MH];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        if (j0 + u < ns) {
-          const int64_t b = kt_ws_base(a, req, j0 + u, head);
+      for (int u = 0; u < MH; ++u) {
+        const int q = j0 + 2 * u;
+        if (q < ns) {
+          const int64_t b = kt_ws_base(a, req, q, head);
           ml[u] = __ldcg(ml_all + b * R + rr);
           v[u] = __ldcg(o_all + (b * 32 + d4) * R + rr);
         } else {
@@ -356,23 +363,34 @@ __device__ void kt_global_merge(const AttnArgs& a, int head, int split, int req,
       }
       float Mn = M;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) Mn = fmaxf(Mn, ml[u].x);
+      for (int u = 0; u < MH; ++u) Mn = fmaxf(Mn, ml[u].x);
       if (Mn == -INFINITY) continue;
       const float sc = M == -INFINITY ? 0.f : ex2(M - Mn);
       L *= sc;
       acc.x *= sc; acc.y *= sc; acc.z *= sc; acc.w *= sc;
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
+      for (int u = 0; u < MH; ++u) {
         const float w = ml[u].x == -INFINITY ? 0.f : ex2(ml[u].x - Mn);
         L += w * ml[u].y;
         acc.x += w * v[u].x; acc.y += w * v[u].y; acc.z += w * v[u].z; acc.w += w * v[u].w;
       }
       M = Mn;
     }
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    const int tok = rr / a.group, qh = head * a.group + rr % a.group;
-    __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
-    *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+    // combine the pair: half 0's terms first, then half 1's
+    const float Mo = __shfl_xor_sync(am, M, 1), Lo = __shfl_xor_sync(am, L, 1);
+    const float4 ao = make_float4(__shfl_xor_sync(am, acc.x, 1), __shfl_xor_sync(am, acc.y, 1),
+                                  __shfl_xor_sync(am, acc.z, 1), __shfl_xor_sync(am, acc.w, 1));
+    if (h == 0) {
+      const float Mt = fmaxf(M, Mo);
+      const float w0 = M == -INFINITY ? 0.f : ex2(M - Mt), w1 = Mo == -INFINITY ? 0.f : ex2(Mo - Mt);
+      const float Lt = w0 * L + w1 * Lo;
+      const float4 at = make_float4(w0 * acc.x + w1 * ao.x, w0 * acc.y + w1 * ao.y, w0 * acc.z + w1 * ao.z,
+                                    w0 * acc.w + w1 * ao.w);
+      const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
+      const int tok = rr / a.group, qh = head * a.group + rr % a.group;
+      __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * d4;
+      *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(at.x * inv, at.y * inv), pack_bf16(at.z * inv, at.w * inv));
+    }
   }
 }
 
