@@ -658,12 +658,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       if (threadIdx.x == 64) TRACE(i, 3);
       sm100::tc_fence_after();
       float sv[64];
+      {  // the tile's 64 score columns: four loads in flight, one wait
+        uint32_t r[4][16];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float t16[16];
-        sm100::tmem_ld16(lane_base + b * A_PAGE + 16 * k, t16);
+        for (int k = 0; k < 4; ++k) sm100::tmem_ld16_nw(lane_base + b * A_PAGE + 16 * k, r[k]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sv[16 * k + e] = t16[e];
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sv[16 * k + e] = __uint_as_float(r[k][e]);
       }
       sm100::tc_fence_before();
       __syncwarp();
@@ -743,12 +746,15 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       sm100::mbar_wait(&o_done[(n_tiles - 1) & 1], ((n_tiles - 1) >> 1) & 1);
       if (threadIdx.x == 64) TRACE(31, 4);
       sm100::tc_fence_after();
+      {
+        uint32_t r[8][16];
 #pragma unroll
-      for (int cc = 0; cc < 8; ++cc) {
-        float t16[16];
-        sm100::tmem_ld16(lane_base + 128 + 16 * cc, t16);
+        for (int cc = 0; cc < 8; ++cc) sm100::tmem_ld16_nw(lane_base + 128 + 16 * cc, r[cc]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) o[16 * cc + e] = t16[e];
+        for (int cc = 0; cc < 8; ++cc)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[16 * cc + e] = __uint_as_float(r[cc][e]);
       }
     } else {
 #pragma unroll
@@ -994,12 +1000,15 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       if (threadIdx.x == 64 || threadIdx.x == 192) TRACE(i, 3);
       sm100::tc_fence_after();
       float sv[64];
+      {  // the tile's 64 score columns: four loads in flight, one wait
+        uint32_t r[4][16];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float t16[16];
-        sm100::tmem_ld16(lane_base + g * A_PAGE + 16 * k, t16);
+        for (int k = 0; k < 4; ++k) sm100::tmem_ld16_nw(lane_base + g * A_PAGE + 16 * k, r[k]);
+        sm100::tmem_ld_wait();
 #pragma unroll
-        for (int e = 0; e < 16; ++e) sv[16 * k + e] = t16[e];
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) sv[16 * k + e] = __uint_as_float(r[k][e]);
       }
       sm100::tc_fence_before();
       __syncwarp();
