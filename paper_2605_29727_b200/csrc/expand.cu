@@ -33,6 +33,7 @@ constexpr int EX_CAP = 8192;   // enumerated-node capacity of the sort path
 constexpr int EX_BINS = 4096;  // histogram bins of the threshold DP
 constexpr int EX_MAXG = 127;
 constexpr int EX_MAXK = 128;
+constexpr int EX_PASS1 = 256;  // adaptive: nodes planned by the first pass
 constexpr unsigned short NO_PARENT = 0xFFFF;
 
 __device__ long long* g_ex_trace = nullptr;
@@ -494,6 +495,43 @@ __device__ int heap_expand(const int32_t* tok, const double* prob, int gamma, in
 // -------------------------------------------------------- post-processing
 // Writes the root row, Algorithm-1 stop logic (adaptive), surrogate, meta,
 // ancestor bitmask and children CSR for the first n_nodes rows.
+// Algorithm 1's stop test over the first n_eval nodes of the tree (rho from out.rho): true
+// when S_hat strictly decreases inside them (controller.py:85-98; the same a_hat order and
+// S_hat arithmetic as finish_tree).  Scratch: the staged lattice in shared memory.
+__device__ bool first_decrease_within(int n_eval, const bst_plan_t& plan, const bst_tree_t& out, ExSmem& sm) {
+  double* ahat = sm.lat_p;                              // [2048]
+  double* shat = reinterpret_cast<double*>(sm.lat_t);   // [1024]
+  if (n_eval < 1 || n_eval > 1024) return false;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 1.0;
+    for (int i = 0; i < n_eval; ++i) {
+      a = __dadd_rn(a, out.rho[i + 1]);
+      ahat[i] = a;
+    }
+    sm.min_stop = 0x7fffffff;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n_eval; i += EX_THREADS) {
+    double c_hat = __dadd_rn(plan.fixed_cost, curve_latency(plan.curve, (long long)i + 2));
+    shat[i] = __ddiv_rn(__dmul_rn(__dadd_rn(ahat[i], plan.a_offset), plan.l_ar), c_hat);
+  }
+  __syncthreads();
+  const int per = (n_eval + EX_THREADS - 1) / EX_THREADS;
+  const int s0 = threadIdx.x * per;
+  double local = -INFINITY;
+  for (int i = s0; i < min(s0 + per, n_eval); ++i) local = fmax(local, shat[i]);
+  double run = block_excl_max(local, sm.dscan);
+  for (int i = s0; i < min(s0 + per, n_eval); ++i) {
+    if (shat[i] < run) { atomicMin(&sm.min_stop, i); break; }
+    run = fmax(run, shat[i]);
+  }
+  __syncthreads();
+  const bool found = sm.min_stop != 0x7fffffff;
+  __syncthreads();
+  return found;
+}
+
 __device__ void finish_tree(int n_eval, bool adaptive, bool is_fixed_or_adaptive, int n_max, const bst_plan_t& plan,
                             const bst_tree_t& out, const ExWs& ws, int algo_used, int enumerated, ExSmem& sm) {
   // Stage rho / parent of rows 0..n_eval in shared memory (the sort arrays are free
@@ -729,12 +767,23 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
   const bst_plan_t plan = resolve_plan(plan_in, plan_dev);
   const bool adaptive = plan.policy == BST_POLICY_ADAPTIVE;
   const int n_max = plan.n_max;
-  const int limit = min(n_max, n_cap);
+  const int limit_full = min(n_max, n_cap);
+  // Adaptive plans usually stop far below n_max (S_hat's first strict decrease), so a first
+  // pass plans only the best EX_PASS1 nodes; the full limit is enumerated only when the
+  // frontier reaches EX_PASS1 nodes without a decrease.  The first EX_PASS1 nodes of both
+  // passes are the same exact pop order, so the result is identical either way.
+  const int limit1 = adaptive ? min(limit_full, EX_PASS1) : limit_full;
   int n_eval = 0;
   int algo_used = BST_ALGO_SORT;
   bool ok = false;
   int enumerated = 0;
   ex_trace(0);
+  for (int pass = 0;; ++pass) {
+  const int limit = pass == 0 ? limit1 : limit_full;
+  n_eval = 0;
+  algo_used = BST_ALGO_SORT;
+  ok = false;
+  enumerated = 0;
   if (plan.algo != BST_ALGO_HEAP) {
     double tau = estimate_tau(prob, gamma, k, limit, sm);
     const bool staged = gamma * k <= 2048;
@@ -775,6 +824,10 @@ __global__ void __launch_bounds__(EX_THREADS, 1)
     }
     __syncthreads();
     n_eval = s_n;
+  }
+  __syncthreads();
+  if (pass > 0 || limit1 == limit_full || n_eval < limit1) break;
+  if (first_decrease_within(n_eval, plan, out, sm)) break;
   }
   __syncthreads();
   ex_trace(5);

@@ -202,6 +202,42 @@ def test_k2_sort_and_heap_paths_match_oracle_full_shape(P, algo, seed):
         assert dt.surrogate.item() == want.tree.surrogate
 
 
+@pytest.mark.parametrize("fixed_cost", [3e-4, 3e-3, 3e-2, 1.0, 1e3])
+def test_k2_adaptive_stop_beyond_first_pass(P, fixed_cost):
+    """Adaptive K2 plans the best 256 nodes first and enumerates up to n_max only when S_hat
+    has not decreased by then; large fixed costs push the stop past 256 nodes (or to the
+    budget cap), and the tree, trace and stop must still equal the oracle's Algorithm 1."""
+    from paper_2605_29727_b200 import _lib
+    from paper_2605_29727_b200.draft_tree import expand_device
+    from paper_2605_29727_b200.lattice import lattice_from_logits
+    g = torch.Generator(device="cuda").manual_seed(7)
+    logits = torch.randn(16, 151936, device="cuda", generator=g) * 0.1
+    for r in range(16):  # three dominant candidates per position: rho decays slowly, trees grow large
+        logits[r, 1000 + 7 * r: 1003 + 7 * r] = torch.tensor([10.0, 9.9, 9.8], device="cuda")
+    tok, prob = lattice_from_logits(logits, 8)
+    tok_h, prob_h = tok.cpu().numpy(), prob.cpu().numpy()
+    dims = O.Dims(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=151936, bp=2, peak_flops=1649.1e12,
+                  bandwidth=6457.7e9)
+    cv = O.curve_for(dims, 2048)
+    l_ar = O.roofline(dims, 1, 2048)
+    want = O.controller(tok_h, prob_h, 1024, cv, fixed_cost, 0.0, l_ar)
+    plan = _lib.Plan(policy=_lib.POLICY_ADAPTIVE, n_max=1024,
+                     curve=_lib.Curve(cv.flops_lin, cv.flops_quad, cv.bytes_const, cv.bytes_lin, cv.bytes_quad,
+                                      cv.inv_peak, cv.inv_bw, cv.slope, cv.intercept, cv.ratio),
+                     fixed_cost=fixed_cost, l_ar=l_ar)
+    dt = expand_device(tok, prob, plan, 1024)
+    meta = dt.meta.cpu().numpy()
+    n = int(meta[0])
+    assert n == want.budget
+    assert int(meta[2]) == want.stop
+    assert dt.trace[: int(meta[1])].cpu().numpy().tobytes() == np.array(want.trace).tobytes()
+    assert dt.parent[: n + 1].cpu().numpy().tolist() == want.tree.parent.tolist()
+    assert dt.token[: n + 1].cpu().numpy().tolist() == want.tree.token.tolist()
+    assert dt.surrogate.item() == want.tree.surrogate
+    _report_budget = (fixed_cost, n, int(meta[1]), int(meta[2]))
+    print("adaptive budget", _report_budget)
+
+
 def test_k2_ancestor_mask_and_csr(P):
     from paper_2605_29727_b200 import _lib
     from paper_2605_29727_b200.draft_tree import expand_device
