@@ -183,3 +183,57 @@ def test_tp_nccl_world_one_runs():
         assert agree >= 0.9
     finally:
         dist.destroy_process_group()
+
+
+def _tp_process_worker(rank, world, port, out_dir):
+    """One TP rank as its own process on cuda:0 (the 1-GPU pool): the real
+    TPTargetModel.forward with torch.distributed collectives (gloo over CUDA tensors)."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+    from paper_2605_29727_b200.engine.config import TINY
+    from paper_2605_29727_b200.engine.forward import MODE_CAUSAL
+    from paper_2605_29727_b200.engine.tp import TPTargetModel, shard_weights
+    from paper_2605_29727_b200.engine.weights import TargetWeights
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        dev = torch.device("cuda", 0)
+        full = TargetWeights.random(TINY, 5, dev)
+        m = TPTargetModel(TINY, world, rank, shard_weights(full, TINY, world, rank), 256, 64, dev)
+        state = torch.zeros(8, dtype=torch.int32, device=dev)
+        toks = np.random.default_rng(9).integers(0, TINY.V, 48).tolist()
+        _fill(m, toks, list(range(48)), list(range(48)))
+        m.forward(48, state, MODE_CAUSAL, keys_after_c=48, head="argmax")
+        torch.cuda.synchronize()
+        np.save(os.path.join(out_dir, f"am{rank}.npy"), m.argmax[:48].cpu().numpy())
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_tp2_processes_match_unsharded_target(tmp_path):
+    """TP = 2 as two processes with a real process group (row-parallel bf16 SUM and
+    argmax-key MAX all-reduces through torch.distributed) reproduces the unsharded target's
+    argmax on every clear row; both ranks agree."""
+    import torch.multiprocessing as mp
+    from paper_2605_29727_b200.engine.config import TINY
+    from paper_2605_29727_b200.engine.forward import MODE_CAUSAL, TargetModel
+    from paper_2605_29727_b200.engine.weights import TargetWeights
+    mp.spawn(_tp_process_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
+    dev = torch.device("cuda", 0)
+    full = TargetWeights.random(TINY, 5, dev)
+    ref = TargetModel(TINY, full, 256, 64, (), dev)
+    state = torch.zeros(8, dtype=torch.int32, device=dev)
+    toks = np.random.default_rng(9).integers(0, TINY.V, 48).tolist()
+    _fill(ref, toks, list(range(48)), list(range(48)))
+    ref.forward(48, state, MODE_CAUSAL, keys_after_c=48, head="logits")
+    logits = ref.logits[:48].clone()
+    ref.forward(48, state, MODE_CAUSAL, keys_after_c=48, head="argmax")
+    torch.cuda.synchronize()
+    want = ref.argmax[:48].cpu().numpy()
+    a0, a1 = (np.load(tmp_path / f"am{r}.npy") for r in range(2))
+    assert np.array_equal(a0, a1)
+    top2 = torch.topk(logits, 2, dim=1).values
+    clear = ((top2[:, 0] - top2[:, 1]) > 1e-2).cpu().numpy()
+    assert clear.sum() >= 24
+    assert np.array_equal(want[clear], a0[clear])
