@@ -652,7 +652,9 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   }
   // pair mode loses TMEM double buffering at bn > 128 and doubles each CTA's partial
   // tile, so it only pays when every CTA streams at least one full tile (n_mt >= grid)
-  s.pair = (pair_min_bn > 0 && s.bn >= pair_min_bn && s.n_mt >= grid) ? 2 : 1;
+  // (very wide outputs, e.g. the LM head's 1187 tiles, already pay from bn = 96)
+  s.pair = (pair_min_bn > 0 && ((s.bn >= pair_min_bn && s.n_mt >= grid) ||
+                                (s.bn >= 96 && s.bn >= pair_min_bn / 2 && s.n_mt >= 4 * grid))) ? 2 : 1;
   // CTA-pair mode (cta_group::2) for m > 128 on even tile counts (BST_GEMM_2CTA=0/1)
   static int cta2_on = -1;
   if (cta2_on < 0) cta2_on = getenv("BST_GEMM_2CTA") ? atoi(getenv("BST_GEMM_2CTA")) : 1;
