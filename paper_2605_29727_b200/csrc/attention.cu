@@ -1093,13 +1093,28 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       L = (hasA ? wA * la[0] : 0.f) + (hasB ? wB * lb[0] : 0.f);
     }
     float o[64];
+    {  // group A's 64 columns in flight together (one wait), then group B's (register budget)
+      uint32_t r[4][16];
 #pragma unroll
-    for (int cc = 0; cc < 4; ++cc) {
-      float ta[16], tb[16];
-      if (hasA) sm100::tmem_ld16(lane_base + 128 + 64 * g + 16 * cc, ta);
-      if (hasB) sm100::tmem_ld16(lane_base + 128 + A_D + 64 * g + 16 * cc, tb);
+      for (int e = 0; e < 64; ++e) o[e] = 0.f;
+      if (hasA) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? wA * ta[e] : 0.f) + (hasB ? wB * tb[e] : 0.f);
+        for (int cc = 0; cc < 4; ++cc) sm100::tmem_ld16_nw(lane_base + 128 + 64 * g + 16 * cc, r[cc]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[16 * cc + e] = wA * __uint_as_float(r[cc][e]);
+      }
+      if (hasB) {
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc) sm100::tmem_ld16_nw(lane_base + 128 + A_D + 64 * g + 16 * cc, r[cc]);
+        sm100::tmem_ld_wait();
+#pragma unroll
+        for (int cc = 0; cc < 4; ++cc)
+#pragma unroll
+          for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? o[16 * cc + e] : 0.f) + wB * __uint_as_float(r[cc][e]);
+      }
     }
     if (a.n_splits > 1 && a.merge == 2) {
       float* stg = reinterpret_cast<float*>(gKV);
