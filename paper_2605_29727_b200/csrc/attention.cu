@@ -447,14 +447,14 @@ __device__ __forceinline__ void cluster_sync_all() {
 // trips, ~3 us per launch at c = 2K) by two cluster barriers and DSMEM loads.
 constexpr int T2_CLUSTER_MAX = 16;
 template <int NT>
-__device__ void cluster_split_merge(const AttnArgs& a, const float* ms, const float* ls, uint32_t stg, int head,
+__device__ void cluster_split_merge(const AttnArgs& a, const float2* ml, uint32_t stg, int head,
                                     int split, int req, int rb, int R) {
   cluster_sync_all();
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NT) {
     const int t = threadIdx.x - 64, ns = a.n_splits;
     const int Rb = min(128, R - rb * 128);
     const int per = (Rb + ns - 1) / ns, r0 = split * per, r1 = min(r0 + per, Rb);
-    const uint32_t ms_u = sm100::smem_u32(ms), ls_u = sm100::smem_u32(ls);
+    const uint32_t ml_u = sm100::smem_u32(ml);
     for (int it = t; it < (r1 - r0) * 32; it += NT) {
       const int r = r0 + (it >> 5), cq = it & 31;
       const uint32_t off = (uint32_t)(r * A_D + ((cq ^ (r & 7)) << 2)) * 4u;
@@ -463,8 +463,9 @@ __device__ void cluster_split_merge(const AttnArgs& a, const float* ms, const fl
 #pragma unroll
       for (int q = 0; q < T2_CLUSTER_MAX; ++q) {
         if (q < ns) {
-          m[q] = ld_dsmem_f1(mapa_shared(ms_u + r * 4, q));
-          l[q] = ld_dsmem_f1(mapa_shared(ls_u + r * 4, q));
+          const float2 v2 = ld_dsmem_f2(mapa_shared(ml_u + r * 8, q));  // (m, l) in one request
+          m[q] = v2.x;
+          l[q] = v2.y;
           v[q] = ld_dsmem_f4(mapa_shared(stg + off, q));
         }
       }
@@ -512,7 +513,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   __shared__ __align__(8) uint64_t full[T_STAGES], empty[T_STAGES], s_full[2], s_free[2], p_full, o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
-  __shared__ float cm[128], cl[128];  // cluster merge: (m, l) per row
+  __shared__ float2 cml[128];  // cluster merge: (m, l) per row
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) TRACE(31, 0);
   if (threadIdx.x == 0) BND(a.seq, 0);
@@ -766,8 +767,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       for (int q = 0; q < 32; ++q)
         *reinterpret_cast<float4*>(stg + row * A_D + ((q ^ (row & 7)) << 2)) =
             make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-      cm[row] = m_run;
-      cl[row] = l_run;
+      cml[row] = make_float2(m_run, l_run);
     } else if (a.n_splits > 1 && a.merge) {
       float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
 #pragma unroll
@@ -802,7 +802,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
     if (threadIdx.x == 64) TRACE(31, 6);
     if (threadIdx.x == 64) TRACE_MAX(2);
   }
-  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<128>(a, cm, cl, sm100::smem_u32(gKV), head, split, req, rb, R);
+  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<128>(a, cml, sm100::smem_u32(gKV), head, split, req, rb, R);
   sm100::tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -836,7 +836,8 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
   __shared__ __align__(8) uint64_t fullK[T2_KS], emptyK[T2_KS], fullV[T2_VS], emptyV[T2_VS], s_full[2], s_free[2],
       p_full[2], o_done[2], q_ready;
   __shared__ uint32_t tmem_sh;
-  __shared__ float xm[2][128], xl[2][128], cm[128], cl[128];
+  __shared__ float xm[2][128], xl[2][128];
+  __shared__ float2 cml[128];
   sm100::grid_dep_launch();
   if (threadIdx.x == 0) TRACE(31, 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1122,7 +1123,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       for (int q = 0; q < 16; ++q)
         *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
             make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
-      if (g == 0) { cm[row] = M; cl[row] = L; }
+      if (g == 0) cml[row] = make_float2(M, L);
     } else if (a.n_splits > 1 && a.merge) {
       const int Rws = a.group * a.s;  // the workspace keeps the uniform per-request row stride
       if (valid) {  // unnormalised partial straight to the L2 workspace, coalesced over rows
@@ -1155,7 +1156,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       }
     }
   }
-  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<256>(a, cm, cl, sm100::smem_u32(gKV), head, split, req, rb, R);
+  if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<256>(a, cml, sm100::smem_u32(gKV), head, split, req, rb, R);
   if (threadIdx.x == 64) TRACE_MAX(2);
   if (threadIdx.x == 0) TRACE(31, 0);
   sm100::tc_fence_before();
