@@ -608,7 +608,8 @@ def main() -> None:
     ap.add_argument("--context", type=int, default=2048)
     ap.add_argument("--policy", default="adaptive")
     ap.add_argument("--logit-scale", type=float, default=6.0)
-    ap.add_argument("--e2e-cycles", type=int, default=64)
+    ap.add_argument("--e2e-cycles", type=int, default=256,
+                    help="decode_full run_length of the e2e leg (the reference harness default, sp/harness.py:57)")
     ap.add_argument("--cpu-cycles", type=int, default=24)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cpu3", action="store_true", help="skip the config-3 process-pool CPU leg")
