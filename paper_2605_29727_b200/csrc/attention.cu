@@ -733,8 +733,7 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       l_run = rescale ? l_run * alpha + rs : l_run + rs;
       m_run = m_ref;
       // bf16 P into tensor memory (A operand of the PV MMA), buffer i & 1
-      sm100::tmem_st16u(lane_base + T_PCOL + 32 * (i & 1), pk);
-      sm100::tmem_st16u(lane_base + T_PCOL + 32 * (i & 1) + 16, pk + 16);
+      sm100::tmem_st32u(lane_base + T_PCOL + 32 * (i & 1), pk);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       __syncwarp();
@@ -1068,8 +1067,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       m_run = m_ref;
       // bf16 P straight into tensor memory: the PV / row-sum MMAs read it as their A
       // operand (no shared-memory round trip, no proxy fence)
-      sm100::tmem_st16u(lane_base + T2_PCOL + 32 * g, pk);
-      sm100::tmem_st16u(lane_base + T2_PCOL + 32 * g + 16, pk + 16);
+      sm100::tmem_st32u(lane_base + T2_PCOL + 32 * g, pk);
       sm100::tmem_st_wait();
       sm100::tc_fence_before();
       __syncwarp();
