@@ -15,6 +15,7 @@
 // tcgen05 with TMEM accumulators; softmax is the online exp2 form in fp32.
 // Splits merge in-kernel (last-arriving CTA) or in attn_combine_kernel.
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <stdlib.h>
 
 #include "common.cuh"
@@ -83,6 +84,13 @@ __device__ __forceinline__ int req_rows(const AttnArgs& a, int req) { return a.r
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 v = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ float2 unpack_f16(uint32_t u) {
+  return __half22float2(*reinterpret_cast<__half2*>(&u));
 }
 
 
@@ -427,6 +435,11 @@ __device__ __forceinline__ float ld_dsmem_f1(uint32_t addr) {
   asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint4 ld_dsmem_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ float2 ld_dsmem_f2(uint32_t addr) {
   float2 v;
   asm volatile("ld.shared::cluster.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(addr));
@@ -437,11 +450,13 @@ __device__ __forceinline__ void cluster_sync_all() {
 }
 
 // Cluster split merge (a.merge == 2): the n_splits (<= 16) CTAs of one (head, row block)
-// form a thread-block cluster (rank = split).  Each has staged its unnormalised partial
-// rows (fp32 [128][128], 16-byte chunks swizzled by row % 8) at shared address `stg` and
-// (m, l) per row in ms / ls; after a cluster barrier CTA `split` merges rows
-// [split * per, split * per + per) from every rank over DSMEM in rank order (the same
-// arithmetic and order as split_merge: deterministic) and stores bf16; a second barrier
+// form a thread-block cluster (rank = split).  Each has staged its partial rows
+// normalised by its own row sum l, as fp16 [128][128] (16-byte chunks swizzled by
+// row % 8; half the DSMEM bytes of fp32 partials — the merge is bound by DSMEM
+// bandwidth), at shared address `stg`, and (m, l) per row in `ml`; after a cluster
+// barrier CTA `split` merges rows [split * per, split * per + per) from every rank over
+// DSMEM in rank order, weighting rank q by 2^(m_q - M) l_q (deterministic), and stores
+// bf16; a second barrier
 // keeps the staging alive until every remote read is done.  This replaces the L2 merge's
 // partial stores, arrival atomic, poll and partial loads (three dependent gpu-scope round
 // trips, ~3 us per launch at c = 2K) by two cluster barriers and DSMEM loads.
@@ -450,23 +465,25 @@ template <int NT>
 __device__ void cluster_split_merge(const AttnArgs& a, const float2* ml, uint32_t stg, int head,
                                     int split, int req, int rb, int R) {
   cluster_sync_all();
+  if (threadIdx.x == 64) TRACE(30, 5);
+  if (threadIdx.x == 64) TRACE_MAX(3);
   if (threadIdx.x >= 64 && threadIdx.x < 64 + NT) {
     const int t = threadIdx.x - 64, ns = a.n_splits;
     const int Rb = min(128, R - rb * 128);
     const int per = (Rb + ns - 1) / ns, r0 = split * per, r1 = min(r0 + per, Rb);
     const uint32_t ml_u = sm100::smem_u32(ml);
-    for (int it = t; it < (r1 - r0) * 32; it += NT) {
-      const int r = r0 + (it >> 5), cq = it & 31;
-      const uint32_t off = (uint32_t)(r * A_D + ((cq ^ (r & 7)) << 2)) * 4u;
+    for (int it = t; it < (r1 - r0) * 16; it += NT) {
+      const int r = r0 + (it >> 4), cq = it & 15;  // dims [8 cq, 8 cq + 8) of row r
+      const uint32_t off = (uint32_t)(r * 256 + ((cq ^ (r & 7)) << 4));
       float m[T2_CLUSTER_MAX], l[T2_CLUSTER_MAX];
-      float4 v[T2_CLUSTER_MAX];
+      uint4 v[T2_CLUSTER_MAX];
 #pragma unroll
       for (int q = 0; q < T2_CLUSTER_MAX; ++q) {
         if (q < ns) {
           const float2 v2 = ld_dsmem_f2(mapa_shared(ml_u + r * 8, q));  // (m, l) in one request
           m[q] = v2.x;
           l[q] = v2.y;
-          v[q] = ld_dsmem_f4(mapa_shared(stg + off, q));
+          v[q] = ld_dsmem_u4(mapa_shared(stg + off, q));
         }
       }
       float M = -INFINITY;
@@ -474,21 +491,27 @@ __device__ void cluster_split_merge(const AttnArgs& a, const float2* ml, uint32_
       for (int q = 0; q < T2_CLUSTER_MAX; ++q)
         if (q < ns) M = fmaxf(M, m[q]);
       float Lsum = 0.f;
-      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      float acc[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) acc[e] = 0.f;
 #pragma unroll
       for (int q = 0; q < T2_CLUSTER_MAX; ++q) {
         if (q < ns && m[q] != -INFINITY) {
-          const float w = ex2(m[q] - M);
-          Lsum += w * l[q];
-          acc.x += w * v[q].x; acc.y += w * v[q].y; acc.z += w * v[q].z; acc.w += w * v[q].w;
+          const float w = ex2(m[q] - M) * l[q];  // the rank's softmax mass (its rows were staged normalised)
+          const float2 p0 = unpack_f16(v[q].x), p1 = unpack_f16(v[q].y), p2 = unpack_f16(v[q].z), p3 = unpack_f16(v[q].w);
+          Lsum += w;
+          acc[0] += w * p0.x; acc[1] += w * p0.y; acc[2] += w * p1.x; acc[3] += w * p1.y;
+          acc[4] += w * p2.x; acc[5] += w * p2.y; acc[6] += w * p3.x; acc[7] += w * p3.y;
         }
       }
       const float inv = Lsum > 0.f ? 1.f / Lsum : 0.f;
       const int rg = rb * 128 + r, tok = rg / a.group, qh = head * a.group + rg % a.group;
-      __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 4 * cq;
-      *reinterpret_cast<uint2*>(op) = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+      __nv_bfloat16* op = a.out + (req_row0(a, req) + tok) * a.o_tok_stride + (int64_t)qh * A_D + 8 * cq;
+      *reinterpret_cast<uint4*>(op) = make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                                                 pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
     }
   }
+  if (threadIdx.x == 64) TRACE(30, 6);
   cluster_sync_all();
 }
 
@@ -761,11 +784,14 @@ __global__ void __launch_bounds__(T_THREADS, 1) attn_tc_kernel(const __grid_cons
       for (int e = 0; e < 128; ++e) o[e] = 0.f;
     }
     if (a.n_splits > 1 && a.merge == 2) {
-      float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
+      // normalised rows as fp16 (the merge re-weights them by each rank's mass m, l): half
+      // the DSMEM bytes of fp32 partials; the K/V ring is idle once the last PV is done
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
-      for (int q = 0; q < 32; ++q)
-        *reinterpret_cast<float4*>(stg + row * A_D + ((q ^ (row & 7)) << 2)) =
-            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      for (int q = 0; q < 16; ++q)
+        *reinterpret_cast<uint4*>(gKV + row * 256 + ((q ^ (row & 7)) << 4)) =
+            make_uint4(pack_f16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_f16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                       pack_f16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_f16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
       cml[row] = make_float2(m_run, l_run);
     } else if (a.n_splits > 1 && a.merge) {
       float* stg = reinterpret_cast<float*>(gKV);  // the K/V ring is idle once the last PV is done
@@ -1076,6 +1102,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
     }
     // ---------------- merge the two groups; thread (g, row) writes dims [64 g, 64 g + 64)
     if (u >= 1) sm100::mbar_wait(&o_done[g], (u - 1) & 1);
+    if (threadIdx.x == 64) TRACE(31, 4);
     xm[g][row] = m_run;
     sm100::tc_fence_before();
     named_bar_sync(1, 256);
@@ -1115,12 +1142,13 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
           for (int e = 0; e < 16; ++e) o[16 * cc + e] = (hasA ? o[16 * cc + e] : 0.f) + wB * __uint_as_float(r[cc][e]);
       }
     }
-    if (a.n_splits > 1 && a.merge == 2) {
-      float* stg = reinterpret_cast<float*>(gKV);
+    if (a.n_splits > 1 && a.merge == 2) {  // normalised fp16 rows (see attn_tc_kernel)
+      const float inv = L > 0.f ? 1.f / L : 0.f;
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        *reinterpret_cast<float4*>(stg + row * A_D + (((16 * g + q) ^ (row & 7)) << 2)) =
-            make_float4(o[4 * q], o[4 * q + 1], o[4 * q + 2], o[4 * q + 3]);
+      for (int q = 0; q < 8; ++q)
+        *reinterpret_cast<uint4*>(gKV + row * 256 + (((8 * g + q) ^ (row & 7)) << 4)) =
+            make_uint4(pack_f16(o[8 * q] * inv, o[8 * q + 1] * inv), pack_f16(o[8 * q + 2] * inv, o[8 * q + 3] * inv),
+                       pack_f16(o[8 * q + 4] * inv, o[8 * q + 5] * inv), pack_f16(o[8 * q + 6] * inv, o[8 * q + 7] * inv));
       if (g == 0) cml[row] = make_float2(M, L);
     } else if (a.n_splits > 1 && a.merge) {
       const int Rws = a.group * a.s;  // the workspace keeps the uniform per-request row stride
@@ -1154,6 +1182,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1) attn_tc2_kernel(const __grid_co
       }
     }
   }
+  if (threadIdx.x == 64) TRACE(31, 6);
   if (a.n_splits > 1 && a.merge == 2) cluster_split_merge<256>(a, cml, sm100::smem_u32(gKV), head, split, req, rb, R);
   if (threadIdx.x == 64) TRACE_MAX(2);
   if (threadIdx.x == 0) TRACE(31, 0);

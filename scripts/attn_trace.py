@@ -25,10 +25,14 @@ run()
 torch.cuda.synchronize()
 lib.bst_debug_attn_trace.argtypes = [C.c_void_p]
 lib.bst_debug_attn_trace(tr.data_ptr())
+if len(sys.argv) > 3:
+    lib.bst_debug_attn_trace_cta(int(sys.argv[3]))
 run()
 torch.cuda.synchronize()
 t = tr.view(32, 8).cpu()
 t0 = int(t[31, 1])  # kernel entry of the traced CTA
+rel = lambda i, k: round((int(t[i, k]) - t0) / 1000, 2) if int(t[i, k]) else None
+print("row31:", [rel(31, k) for k in range(8)], "row30:", [rel(30, k) for k in range(8)])
 print("entry->depwait/q_ready/staged/exit:", [round((int(t[31, k]) - t0) / 1000, 2) for k in (2, 3, 5, 0)])
 print("all CTAs max depwait/staged/end/arrive/spin_done:", [round((int(t[29, k]) - t0) / 1000, 2) for k in range(5)])
 names = ["tma_issued", "mma:full", "mma:p_full", "sm:s_full", "sm:sm_done", "sm:o_done", "sm:p_arrive", "sm:max_local"]
