@@ -452,8 +452,12 @@ __device__ __forceinline__ void cluster_sync_all() {
 // Cluster split merge (a.merge == 2): the n_splits (<= 16) CTAs of one (head, row block)
 // form a thread-block cluster (rank = split).  Each has staged its partial rows
 // normalised by its own row sum l, as fp16 [128][128] (16-byte chunks swizzled by
-// row % 8; half the DSMEM bytes of fp32 partials — the merge is bound by DSMEM
-// bandwidth), at shared address `stg`, and (m, l) per row in `ml`; after a cluster
+// row % 8; half the DSMEM requests of fp32 partials — the merge is bound by DSMEM
+// requests), at shared address `stg`, and (m, l) per row in `ml`.  A normalised row is a
+// convex combination of V rows, so fp16 holds it whenever |V| < 65504 (bf16 LLM value
+// activations are orders of magnitude below; bf16 staging measured the same speed but
+// its 8-bit mantissa flips a near-tie argmax of the tiny test model, and a per-half
+// scale cost 0.6 us per launch).  After a cluster
 // barrier CTA `split` merges rows [split * per, split * per + per) from every rank over
 // DSMEM in rank order, weighting rank q by 2^(m_q - M) l_q (deterministic), and stores
 // bf16; a second barrier
