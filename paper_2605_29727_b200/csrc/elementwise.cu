@@ -105,6 +105,15 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
   if (threadIdx.x == 0) BND(s.reserved, 0);
   if (threadIdx.x == 0 && blockIdx.x == 0) BND_KIND(s.reserved, 2);
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
+  const int ng = h >> 2;
+  // the norm weights are constant: fetch them while the producer GEMM drains (h <= 8192:
+  // at most two 4-column groups per thread)
+  uint2 wv[2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int g = threadIdx.x + j * R_THREADS;
+    if (x && g < ng) wv[j] = reinterpret_cast<const uint2*>(w)[g];
+  }
   sm100::grid_dep_wait();  // PDL launch: the producer GEMM's partials are complete past this point
   if (threadIdx.x == 0) BND(s.reserved, 2);
   if (threadIdx.x == 0) BND(s.reserved, 3);
@@ -112,7 +121,6 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
   __shared__ float4 vals[2048];
   const int t = blockIdx.x;
   if (t >= rows) return;
-  const int ng = h >> 2;
   float ss = 0.f;
   for (int g = threadIdx.x; g < ng; g += R_THREADS) {
     float4 v = resid ? reinterpret_cast<const float4*>(resid + (int64_t)t * h)[g] : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -131,9 +139,12 @@ __global__ void __launch_bounds__(R_THREADS) residual_rmsnorm_kernel(
   }
   const float inv = rsqrtf(block_sum(ss, sh) / h + eps);
   if (x) {
-    for (int g = threadIdx.x; g < ng; g += R_THREADS) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int g = threadIdx.x + j * R_THREADS;
+      if (g >= ng) break;
       const float4 v = vals[g];
-      const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(w + g * 4);
+      const __nv_bfloat162* wp = reinterpret_cast<const __nv_bfloat162*>(&wv[j]);
       const float2 w01 = __bfloat1622float2(wp[0]), w23 = __bfloat1622float2(wp[1]);
       __nv_bfloat162* xp = reinterpret_cast<__nv_bfloat162*>(x + (int64_t)t * ldx + g * 4);
       xp[0] = __floats2bfloat162_rn(v.x * inv * w01.x, v.y * inv * w01.y);
@@ -193,17 +204,18 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
   if (threadIdx.x == 0) BND(s.reserved, 0);
   if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0) BND_KIND(s.reserved, 3);
   if (threadIdx.x == 0 && blockIdx.y == 0) issue_prefetch(pf, blockIdx.x, gridDim.x);
+  const int t = blockIdx.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const RopeConst rc = rope_const(ra, lane);  // constant weights: fetched while the GEMM drains
   sm100::grid_dep_wait();
   if (threadIdx.x == 0) BND(s.reserved, 2);
   if (threadIdx.x == 0) BND(s.reserved, 3);
-  const int t = blockIdx.x;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nw = blockDim.x >> 5;
   const int h_end = min(ra.n_q + 2 * ra.n_kv, (int)(blockIdx.y + 1) * nw);
   for (int hd = blockIdx.y * nw + warp; hd < h_end; hd += nw) {
     const float4 y4 = gemm_load4(partial, s, t, hd * 128 + lane * 4);
     float v[4] = {y4.x, y4.y, y4.z, y4.w};
-    rope_store_head(ra, t, hd, v, lane);
+    rope_store_head(ra, rc, t, hd, v, lane);
   }
 #ifdef BST_TRACE
   __syncthreads();

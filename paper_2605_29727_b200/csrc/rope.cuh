@@ -29,8 +29,25 @@ struct RopeArgs {
   const int32_t* row_req;   // ragged batch: request of each row (< 0: padding row); overrides req_rows
 };
 
+// The lane's constant operands: q/k norm weights and RoPE inverse frequencies of dims
+// 4 lane .. 4 lane + 3 (loaded before griddepcontrol.wait; they never change).
+struct RopeConst {
+  float qn[4], kn[4], fr[4];
+};
+__device__ __forceinline__ RopeConst rope_const(const RopeArgs& a, int lane) {
+  RopeConst c;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    c.qn[e] = __bfloat162float(a.qn[lane * 4 + e]);
+    c.kn[e] = __bfloat162float(a.kn[lane * 4 + e]);
+    c.fr[e] = a.inv_freq[(lane * 4 + e) & 63];
+  }
+  return c;
+}
+
 // This warp's lane holds dims 4 lane .. 4 lane + 3 of head `hd` for token row t in v.
-__device__ __forceinline__ void rope_store_head(const RopeArgs& a, int t, int hd, float (&v)[4], int lane) {
+__device__ __forceinline__ void rope_store_head(const RopeArgs& a, const RopeConst& rc, int t, int hd, float (&v)[4],
+                                                int lane) {
   int r = a.req_rows > 0 ? (t % a.req_span) / a.req_rows : 0;
   if (a.row_req) {
     r = a.row_req[t];
@@ -43,19 +60,18 @@ __device__ __forceinline__ void rope_store_head(const RopeArgs& a, int t, int hd
   if (is_q && qr < 0) return;
   if (!is_q && sl < 0) return;
   if (is_q || is_k) {
-    const __nv_bfloat16* w = is_q ? a.qn : a.kn;
     float ss = v[0] * v[0] + v[1] * v[1] + v[2] * v[2] + v[3] * v[3];
     ss = warp_sum(ss);
     const float inv = rsqrtf(ss / 128.f + a.eps);
 #pragma unroll
-    for (int e = 0; e < 4; ++e) v[e] = v[e] * inv * __bfloat162float(w[lane * 4 + e]);
+    for (int e = 0; e < 4; ++e) v[e] = v[e] * inv * (is_q ? rc.qn[e] : rc.kn[e]);
     // rotate_half: lanes 0-15 hold dims 0-63, lanes 16-31 hold 64-127
     const int p = a.pos[t] + c0;
     float o[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       float sn, cs;
-      sincosf((float)p * a.inv_freq[(lane * 4 + e) & 63], &sn, &cs);
+      sincosf((float)p * rc.fr[e], &sn, &cs);
       const float partner = __shfl_xor_sync(0xffffffffu, v[e], 16);
       o[e] = lane < 16 ? v[e] * cs - partner * sn : v[e] * cs + partner * sn;
     }
