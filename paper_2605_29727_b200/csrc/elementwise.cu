@@ -224,6 +224,10 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
 }
 
 // ---------------------------------------------------------------- swiglu
+#ifndef BST_SW_GROUPS  // measurement builds may override (BST_NVCC_EXTRA=-DBST_SW_GROUPS=..)
+#define BST_SW_GROUPS 2
+#endif
+constexpr int SW_GROUPS = BST_SW_GROUPS;
 __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int ffn, __nv_bfloat16* act,
                               int64_t lda, bst_prefetch_t pf) {
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
@@ -234,13 +238,27 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
   sm100::grid_dep_wait();
   if (threadIdx.x == 0) BND(s.reserved, 2);
   if (threadIdx.x == 0) BND(s.reserved, 3);
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < (ffn >> 2); g += gridDim.x * blockDim.x) {
-    const float4 gt = gemm_load4(partial, s, t, g * 4);
-    const float4 up = gemm_load4(partial, s, t, ffn + g * 4);
-    auto si = [](float z) { return z / (1.f + __expf(-z)); };
-    __nv_bfloat162* ap = reinterpret_cast<__nv_bfloat162*>(act + (int64_t)t * lda + g * 4);
-    ap[0] = __floats2bfloat162_rn(si(gt.x) * up.x, si(gt.y) * up.y);
-    ap[1] = __floats2bfloat162_rn(si(gt.z) * up.z, si(gt.w) * up.w);
+  // SW_GROUPS 4-column groups per thread (grid sized by the host): the row's CTAs fit in
+  // one wave next to the down GEMM's early-launched CTAs
+  const int g0 = blockIdx.x * blockDim.x * SW_GROUPS + threadIdx.x;
+  float4 gt[SW_GROUPS], up[SW_GROUPS];
+#pragma unroll
+  for (int j = 0; j < SW_GROUPS; ++j) {
+    const int g = g0 + j * blockDim.x;
+    if (g < (ffn >> 2)) {
+      gt[j] = gemm_load4(partial, s, t, g * 4);
+      up[j] = gemm_load4(partial, s, t, ffn + g * 4);
+    }
+  }
+  auto si = [](float z) { return z / (1.f + __expf(-z)); };
+#pragma unroll
+  for (int j = 0; j < SW_GROUPS; ++j) {
+    const int g = g0 + j * blockDim.x;
+    if (g < (ffn >> 2)) {
+      __nv_bfloat162* ap = reinterpret_cast<__nv_bfloat162*>(act + (int64_t)t * lda + g * 4);
+      ap[0] = __floats2bfloat162_rn(si(gt[j].x) * up[j].x, si(gt[j].y) * up[j].y);
+      ap[1] = __floats2bfloat162_rn(si(gt[j].z) * up[j].z, si(gt[j].w) * up[j].w);
+    }
   }
 #ifdef BST_TRACE
   __syncthreads();
@@ -377,7 +395,7 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
                           int64_t lda, bst_stream_t stream) {
   BST_REQUIRE(partial && sched && act, "null pointer argument");
   BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
-  dim3 grid((ffn / 4 + 255) / 256, rows);
+  dim3 grid((ffn / 4 + 256 * SW_GROUPS - 1) / (256 * SW_GROUPS), rows);
   bst_gemm_sched_t s = *sched;
   s.reserved = bnd_next_seq();
   BST_CUDA(launch_pdl(swiglu_kernel, grid, dim3(256), 0, as_stream(stream), partial, s, ffn,
