@@ -35,7 +35,15 @@ constexpr int G_BM = 128;
 constexpr int G_BK = 64;
 constexpr int G_TILE_W = G_BM * G_BK * 2;  // 16 KiB
 constexpr int G_MAX_STAGES = 12;
-constexpr int G_SMEM_BUDGET = 160 * 1024;  // leaves room for a co-resident epilogue CTA (PDL overlap)
+// one-CTA ring budget by token columns (leaves room for a co-resident epilogue CTA under PDL
+// overlap): 160 KiB, except 176 KiB for 49..112 columns and 200 KiB at 128 — measured in the
+// verify graph at 32 / 48 / 96 / 128 / 256 rows (BST_GEMM_SMEM_KB sweeps 128..200): 96 rows
+// 4.01-4.04 -> 3.96-3.98 ms, 128 rows 4.38-4.42 -> 4.25 ms; 32 / 48 rows and the drafter's
+// 17 / 34 rows equal or best at 160, the one-CTA launches at 256 rows slower above 160
+constexpr int G_SMEM_BUDGET = 160 * 1024;
+__host__ __forceinline__ int gemm_smem_budget(int bn) {
+  return bn <= 48 || bn > 128 ? G_SMEM_BUDGET : (bn < 128 ? 176 * 1024 : 200 * 1024);
+}
 constexpr int G_SMEM_BUDGET_PAIR = 200 * 1024;  // pair mode: 3 stages of 2 weight tiles + a 256-row X block
 
 // ------------------------------------------------------------ tensor maps
@@ -677,13 +685,14 @@ extern "C" int bst_gemm_schedule(int n_out, int k, int m, int grid, bst_gemm_sch
   if (tc < s.bn) tc = 512;
   s.tmem_cols = tc;
   const int stage_bytes = s.cta2 ? G_TILE_W + (s.bn / 2) * G_BK * 2 : s.pair * G_TILE_W + s.bn * G_BK * 2;
-  static int budget = 0, budget_pair = 0;
-  if (!budget) {
+  static int budget_env = -1, budget_pair = 0;
+  if (budget_env < 0) {
     const char* e = getenv("BST_GEMM_SMEM_KB");  // measurement knobs
-    budget = e ? atoi(e) * 1024 : G_SMEM_BUDGET;
+    budget_env = e ? atoi(e) * 1024 : 0;
     e = getenv("BST_GEMM_PAIR_SMEM_KB");
     budget_pair = e ? atoi(e) * 1024 : G_SMEM_BUDGET_PAIR;
   }
+  const int budget = budget_env > 0 ? budget_env : gemm_smem_budget(s.bn);
   // pair and CTA-pair modes (m > 128): deeper weight prefetch, no co-resident epilogue needed
   int stages = ((s.pair == 2 ? budget_pair : budget) - 1024) / stage_bytes;
   BST_REQUIRE(stages >= 2, "GEMM smem budget too small for two stages");
