@@ -2128,6 +2128,9 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
   // (the largest cluster <= the one-wave split count that fits); taken when it lengthens
   // each CTA's page run by at most 4 pages (~0.65 us each) against the ~3 us it saves.
   // BST_ATTN_CLUSTER=0 disables it (measurement).
+#ifndef BST_CLUSTER_SLACK  // measurement builds may override: extra pages per CTA a cluster may cost
+#define BST_CLUSTER_SLACK 4
+#endif
   static int cl_on = -1;
   if (cl_on < 0) cl_on = getenv("BST_ATTN_CLUSTER") ? atoi(getenv("BST_ATTN_CLUSTER")) : 1;
   if (cl_on && a.merge && n_splits_arg <= 0) {
@@ -2138,7 +2141,7 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
       const int nsc = (pages + pk - 1) / pk;
       const bool tg = pk >= T2_MIN_PAGES;
       if (nsc < 2 || rm_cluster_fits(tg, nsc, tg ? smem_tc2 : smem_tc) < groups_total) continue;
-      if (pk - pps <= 4) {
+      if (pk - pps <= BST_CLUSTER_SLACK) {
         n_splits = nsc;
         pps = pk;
         two_groups = tg;
