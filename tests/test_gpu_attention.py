@@ -145,3 +145,34 @@ def test_back_to_back_launches_in_a_graph(c, variant):
         st.synchronize()
         for o, w in zip(outs, want):
             assert torch.equal(o, w)
+
+
+@pytest.mark.parametrize("c,s", [(2048, 96), (2048, 17)])
+def test_cluster_merge_large_values(c, s):
+    """The cluster split merge stages each split's normalised rows as fp16 (a convex
+    combination of V rows): V rows ~1e3 (far above LLM value activations, below fp16's
+    65504) still match the dense fp32 reference to bf16 precision."""
+    from oracle import specplan_port as O
+    from paper_2605_29727_b200 import ops
+    import numpy as np
+    n_q, n_kv = 32, 8
+    kv, q = _setup(n_q, n_kv, c, s, seed=c + 3 * s)
+    L = kv.buf.view(kv.n_layers, kv.n_pages, 2, n_kv, 64, 128)
+    L[:, :, 1].mul_(1000.0)  # V pages only
+    gen = torch.Generator().manual_seed(s)
+    parent = [-1] + [int(torch.randint(0, i, (1,), generator=gen)) for i in range(1, s)]
+    anc = torch.from_numpy(O.ancestor_bits(np.array(parent))).cuda()
+    words = (s + 31) // 32
+    packed = torch.from_numpy(pack_mask(anc.cpu().numpy(), words)).cuda()
+    out = torch.empty(s, n_q * 128, device="cuda", dtype=torch.bfloat16)
+    ws = torch.zeros(8 << 20, device="cuda", dtype=torch.float32)
+    ops.attention(q, out, kv.buf, 2, kv.n_pages, 1, kv.page_table, n_q, n_kv, s, c, s, c + s, None, 0, packed.view(-1),
+                  words, ws)
+    vis = torch.zeros(s, c + s, dtype=torch.bool, device="cuda")
+    vis[:, :c] = True
+    vis[:, c:] = anc
+    ref = _ref(q, kv, 1, n_q, n_kv, c, s, vis)
+    torch.cuda.synchronize()
+    assert torch.isfinite(out.float()).all()
+    err = (out.float() - ref).abs().max().item()
+    assert err < 2e-2 * 1000.0, err
