@@ -170,11 +170,14 @@ __device__ double estimate_tau(const double* prob, int gamma, int k, int n_max, 
   __shared__ int s_bstar;
   int* cost = reinterpret_cast<int*>(sm.lo);  // [gamma*k] quantized -log2(p), lo is free here
   __shared__ int s_range, s_cross;
-  for (int pass = 0; pass < 3; ++pass) {
-    // pass 0: 1/16-bit bins up to 2^-64 (typical drafter rows); pass 1: up to 2^-256;
-    // pass 2: 1/2-bit bins covering the whole fp64 range
-    const double S = pass < 2 ? 16.0 : 2.0;
-    const int max_range = pass == 0 ? 1024 : EX_BINS;
+  for (int pass = 0; pass < 4; ++pass) {
+    // pass 0: 1/16-bit bins up to 2^-16 (the usual crossing: a quarter of the bins, a quarter
+    // of the instructions per level); pass 1: up to 2^-64 (typical drafter rows); pass 2: up
+    // to 2^-256; pass 3: 1/2-bit bins covering the whole fp64 range.  Bins below a pass's
+    // range get the same counts in every pass (the convolution only reads lower bins), so
+    // the first crossing — and tau — do not depend on the pass that finds it.
+    const double S = pass < 3 ? 16.0 : 2.0;
+    const int max_range = pass == 0 ? 256 : (pass == 1 ? 1024 : EX_BINS);
     // est cost = floor(-log2(p) * S) + 1 >= the true scaled cost, so a path's
     // summed est cost never undercounts: est <= B  =>  rho > 2^(-(B+1)/S).
     for (int e = threadIdx.x; e < gamma * k; e += EX_THREADS) {
