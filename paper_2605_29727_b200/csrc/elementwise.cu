@@ -224,10 +224,11 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
 }
 
 // ---------------------------------------------------------------- swiglu
-#ifndef BST_SW_GROUPS  // measurement builds may override (BST_NVCC_EXTRA=-DBST_SW_GROUPS=..)
-#define BST_SW_GROUPS 2
-#endif
-constexpr int SW_GROUPS = BST_SW_GROUPS;
+// G 4-column groups per thread, G = 1 or 2 chosen by the host (bst_swiglu): 256-thread CTAs,
+// at most 7 of them per SM beside the down GEMM's early-launched CTA; G = 2 once one group
+// per thread would need a second wave (96 rows: 4.06-4.08 -> 4.02-4.03 ms in the verify
+// graph; at 32 rows G = 1 is 45 us faster; four groups slower everywhere)
+template <int SW_GROUPS>
 __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, int ffn, __nv_bfloat16* act,
                               int64_t lda, bst_prefetch_t pf) {
   if (threadIdx.x == 0) issue_prefetch(pf, blockIdx.y * gridDim.x + blockIdx.x, gridDim.x * gridDim.y);
@@ -238,8 +239,6 @@ __global__ void swiglu_kernel(const float* __restrict__ partial, bst_gemm_sched_
   sm100::grid_dep_wait();
   if (threadIdx.x == 0) BND(s.reserved, 2);
   if (threadIdx.x == 0) BND(s.reserved, 3);
-  // SW_GROUPS 4-column groups per thread (grid sized by the host): the row's CTAs fit in
-  // one wave next to the down GEMM's early-launched CTAs
   const int g0 = blockIdx.x * blockDim.x * SW_GROUPS + threadIdx.x;
   float4 gt[SW_GROUPS], up[SW_GROUPS];
 #pragma unroll
@@ -395,10 +394,18 @@ extern "C" int bst_swiglu(const float* partial, const bst_gemm_sched_t* sched, i
                           int64_t lda, bst_stream_t stream) {
   BST_REQUIRE(partial && sched && act, "null pointer argument");
   BST_REQUIRE(sched->n_out == 2 * ffn && ffn % 4 == 0, "gate/up width mismatch");
-  dim3 grid((ffn / 4 + 256 * SW_GROUPS - 1) / (256 * SW_GROUPS), rows);
+  static int n_sm = 0;
+  if (!n_sm) {
+    int dev = 0;
+    BST_CUDA(cudaGetDevice(&dev));
+    BST_CUDA(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int ctas1 = (ffn / 4 + 255) / 256;
+  const int groups = (int64_t)ctas1 * rows <= 7ll * n_sm ? 1 : 2;
+  dim3 grid((ffn / 4 + 256 * groups - 1) / (256 * groups), rows);
   bst_gemm_sched_t s = *sched;
   s.reserved = bnd_next_seq();
-  BST_CUDA(launch_pdl(swiglu_kernel, grid, dim3(256), 0, as_stream(stream), partial, s, ffn,
+  BST_CUDA(launch_pdl(groups == 1 ? swiglu_kernel<1> : swiglu_kernel<2>, grid, dim3(256), 0, as_stream(stream), partial, s, ffn,
                       static_cast<__nv_bfloat16*>(act), lda, take_prefetch()));
   BST_LAUNCH_CHECK();
   return BST_OK;
