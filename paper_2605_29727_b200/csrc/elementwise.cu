@@ -198,6 +198,10 @@ __global__ void __launch_bounds__(R_THREADS) residual_dense_kernel(
 }
 
 // ------------------------------------------------------------- q/k/v + rope
+#ifndef BST_QR_LOAD_BATCH  // measurement builds may override
+#define BST_QR_LOAD_BATCH 4
+#endif
+constexpr int QR_LOAD_BATCH = BST_QR_LOAD_BATCH;
 // One CTA per (token row, group of 16 heads); one warp per head (d = 128, 4 values per lane).
 __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sched_t s, RopeArgs ra, bst_prefetch_t pf) {
   sm100::grid_dep_launch();
@@ -213,7 +217,9 @@ __global__ void qkv_rope_kernel(const float* __restrict__ partial, bst_gemm_sche
   const int nw = blockDim.x >> 5;
   const int h_end = min(ra.n_q + 2 * ra.n_kv, (int)(blockIdx.y + 1) * nw);
   for (int hd = blockIdx.y * nw + warp; hd < h_end; hd += nw) {
-    const float4 y4 = gemm_load4(partial, s, t, hd * 128 + lane * 4);
+    // the qkv tiles span ~4 stream-K slots: their loads in flight together (the next kernel,
+    // K3, takes a whole SM, so the extra registers cost no co-residency)
+    const float4 y4 = gemm_load4<QR_LOAD_BATCH>(partial, s, t, hd * 128 + lane * 4);
     float v[4] = {y4.x, y4.y, y4.z, y4.w};
     rope_store_head(ra, rc, t, hd, v, lane);
   }

@@ -39,11 +39,13 @@ __device__ __forceinline__ int tile_nslot(const bst_gemm_sched_t& s, int tile) {
 }
 
 // Four consecutive outputs Y[t, n0..n0+3] (n0 % 4 == 0, same 128-wide tile): one
-// slot lookup, float4 loads, slots summed lowest k range first.  GEMM_LOAD_BATCH > 1
-// issues that many slot loads before their adds (measurement builds; same sums).
+// slot lookup, float4 loads, slots summed lowest k range first.  B > 1 issues that many
+// slot loads before their adds (same sums); the default GEMM_LOAD_BATCH keeps the register
+// count of the epilogues that share SMs with the next GEMM's early CTAs.
 #ifndef GEMM_LOAD_BATCH
 #define GEMM_LOAD_BATCH 1
 #endif
+template <int B = GEMM_LOAD_BATCH>
 __device__ __forceinline__ float4 gemm_load4(const float* __restrict__ partial, const bst_gemm_sched_t& s, int t,
                                              int n0) {
   const int tile = n0 >> 7;
@@ -51,13 +53,13 @@ __device__ __forceinline__ float4 gemm_load4(const float* __restrict__ partial, 
   const float4* p = reinterpret_cast<const float4*>(partial + ((int64_t)tile * s.s_max * s.bn + t) * 128 + (n0 & 127));
   const int64_t stride = (int64_t)s.bn * 32;  // in float4
   float4 acc = __ldg(p);
-  for (int k0 = 1; k0 < nslot; k0 += GEMM_LOAD_BATCH) {
-    float4 v[GEMM_LOAD_BATCH];
+  for (int k0 = 1; k0 < nslot; k0 += B) {
+    float4 v[B];
 #pragma unroll
-    for (int u = 0; u < GEMM_LOAD_BATCH; ++u)
+    for (int u = 0; u < B; ++u)
       if (k0 + u < nslot) v[u] = __ldg(p + (k0 + u) * stride);
 #pragma unroll
-    for (int u = 0; u < GEMM_LOAD_BATCH; ++u) {
+    for (int u = 0; u < B; ++u) {
       if (k0 + u < nslot) {
         acc.x += v[u].x;
         acc.y += v[u].y;
