@@ -58,20 +58,29 @@ class ClockSampler:
         self.index, self.proc = index, None
 
     def __enter__(self):
+        # 50 ms sampling, and the timed region starts only once nvidia-smi has printed its
+        # first sample: a short region (40 cycles ~ 0.2 s) still gets several samples
+        self.first = ""
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
+        if self.proc:
+            import select
+            ready, _, _ = select.select([self.proc.stdout], [], [], 10.0)
+            if ready:
+                self.first = self.proc.stdout.readline()
         return self
 
     def __exit__(self, *a):
-        self.out = ""
+        self.out = self.first
         if self.proc:
             self.proc.terminate()
             try:
-                self.out, _ = self.proc.communicate(timeout=5)
+                rest, _ = self.proc.communicate(timeout=5)
+                self.out += rest or ""
             except subprocess.TimeoutExpired:
                 self.proc.kill()
 
