@@ -1946,6 +1946,9 @@ static int attention_impl(const void* q, int64_t q_tok_stride, void* out, int64_
     // one wave of CTAs: per-tile work (GQA group x tokens rows against 64 keys)
     // dominates a CTA's fixed cost, so spread the pages over every SM
     int want = n_sm / (n_kv * row_blocks * n_req);
+    static int split_cap = -1;  // measurement knob: leave SMs free for the next GEMM's early CTAs
+    if (split_cap < 0) split_cap = getenv("BST_ATTN_SPLIT_CAP") ? atoi(getenv("BST_ATTN_SPLIT_CAP")) : 0;
+    if (split_cap > 0 && want > split_cap) want = split_cap;
     n_splits = want < 1 ? 1 : want;
   }
   if (n_splits > pages) n_splits = pages;
