@@ -1,0 +1,86 @@
+"""The SPEC.md known-answer tests driven through the device path:
+K1 (`top_k_truncate` on a hand-built MarginalBlock) -> K2 (`best_first_expand`,
+`beam_expand`, `run_cycle`) through the reference-named façade, with the SPEC's
+2 x 2 lattice relabelled to tokens a=5, b=9, c=7, d=3 (SURVEY §4.2 last row:
+the GPU-lattice parity seam).  Expected values are the SPEC's, cross-checked
+against the CPU oracle on the same lattice."""
+
+import numpy as np
+import pytest
+
+from oracle import specplan_port as O
+
+pytestmark = pytest.mark.gpu
+
+V = 10
+A, B, C, D = 5, 9, 7, 3
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2605_29727_b200 as P
+    return P
+
+
+def _block(P):
+    # q1 = {a: .6, b: .3}, q2 = {c: .7, d: .2}; the remaining .1 spread evenly
+    probs = np.full((2, V), 0.1 / (V - 2))
+    probs[0, A], probs[0, B] = 0.6, 0.3
+    probs[1, C], probs[1, D] = 0.7, 0.2
+    return P.MarginalBlock(gamma=2, vocab_size=V, probs=probs)
+
+
+def _nodes(tree):
+    parent = [-1 if n.parent is None else n.parent for n in tree.nodes]
+    token = [-1 if n.token is None else n.token for n in tree.nodes]
+    return parent, token, np.array([n.path_score for n in tree.nodes[1:]])
+
+
+def test_k1_spec_lattice_entries(P):
+    lat = P.top_k_truncate(_block(P), 2)
+    assert [[t for t, _ in row] for row in lat.entries] == [[A, B], [C, D]]
+    assert [[p for _, p in row] for row in lat.entries] == [[0.6, 0.3], [0.7, 0.2]]
+
+
+def test_k2_spec_best_first_order(P):
+    # SPEC.md:133 / :160: a(.60), ac(.42), b(.30), bc(.21), ad(.12), bd(.06); gains non-increasing
+    tree = P.best_first_expand(P.top_k_truncate(_block(P), 2), 10)
+    parent, token, rho = _nodes(tree)
+    assert parent == [-1, 0, 1, 0, 3, 1, 3]
+    assert token == [-1, A, C, B, C, D, D]
+    np.testing.assert_allclose(rho, [0.6, 0.42, 0.3, 0.21, 0.12, 0.06], rtol=0, atol=1e-15)
+    assert np.all(np.diff(rho) <= 0)
+    assert abs(tree.surrogate - 2.71) < 1e-12
+    want = O.best_first(np.array([[A, B], [C, D]], dtype=np.int32), np.array([[0.6, 0.3], [0.7, 0.2]]), 10)
+    assert parent == want.parent.tolist() and token == want.token.tolist()
+    assert rho.tobytes() == want.rho[1:].tobytes() and tree.surrogate == want.surrogate
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 4, 5, 6])
+def test_k2_spec_nested_prefixes(P, n):
+    # best-first trees are nested: the n-node tree is the first n pops
+    lat = P.top_k_truncate(_block(P), 2)
+    full = _nodes(P.best_first_expand(lat, 10))
+    part = _nodes(P.best_first_expand(lat, n))
+    assert part[0] == full[0][: n + 1] and part[1] == full[1][: n + 1]
+
+
+def test_k2_spec_beam(P):
+    # beam w=2, d=2 -> {a, b, ac, bc}, A_hat = 2.53 (level order)
+    tree = P.beam_expand(P.top_k_truncate(_block(P), 2), 2, 2)
+    parent, token, _ = _nodes(tree)
+    assert token == [-1, A, B, C, C] and parent == [-1, 0, 0, 1, 2]
+    assert abs(tree.surrogate - 2.53) < 1e-12
+
+
+def test_k2_spec_run_cycle_budget_cap(P):
+    # run_cycle with n_max = 1 -> budget 1, stop "budget-cap", the node a
+    params = P.CostModelParams(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=151936, bp=2,
+                               peak_flops=1.6e15, bandwidth=6.5e12)
+    est = P.VerifyLatencyEstimator(params, variant="static")
+    cfg = P.ControllerConfig(n_max=1, latencies=P.CycleLatencies(5e-4, 0.0, 3e-3), variant="static",
+                             context_len=2048)
+    d = P.run_cycle(P.top_k_truncate(_block(P), 2), cfg, est)
+    assert d.budget == 1 and d.stop_reason == "budget-cap"
+    parent, token, rho = _nodes(d.tree)
+    assert parent == [-1, 0] and token == [-1, A] and rho.tolist() == [0.6]
