@@ -84,3 +84,26 @@ def test_k2_spec_run_cycle_budget_cap(P):
     assert d.budget == 1 and d.stop_reason == "budget-cap"
     parent, token, rho = _nodes(d.tree)
     assert parent == [-1, 0] and token == [-1, A] and rho.tolist() == [0.6]
+
+
+def test_k2_spec_controller_trace(P):
+    # gains .6, .42, .3, .21, ... with C(N) = 1 + 0.15 N and L_AR = 1 stop at N = 3,
+    # S_hat trace (1.3913, 1.5538, 1.6, 1.58125).  Device plan: fixed 0.85 + curve(N + 1) with
+    # memory = 15 * s * 0.01 (integer bytes, reciprocal bandwidth as in sp/cost_model.py:305-309).
+    from paper_2605_29727_b200 import _lib
+    from paper_2605_29727_b200.draft_tree import expand_device
+
+    lat = P.top_k_truncate(_block(P), 2)
+    tok, prob = lat.device_arrays()
+    plan = _lib.Plan(policy=_lib.POLICY_ADAPTIVE, n_max=16,
+                     curve=_lib.Curve(0, 0, 0, 15, 0, 0.0, 0.01, 1.0, 0.0, 1.0), fixed_cost=0.85, l_ar=1.0)
+    dt = expand_device(tok, prob, plan, 16)
+    n, n_exp, stop = (int(x) for x in dt.meta[:3].cpu().tolist())
+    assert n == 3 and _lib.STOP_NAMES[stop] == "first-decrease"
+    trace = dt.trace[:n_exp].cpu().numpy()
+    np.testing.assert_allclose(trace, [1.6 / 1.15, 2.02 / 1.3, 2.32 / 1.45, 2.53 / 1.6], rtol=1e-12)
+    cv = O.Curve(0, 0, 0, 15, 0, 0.0, 0.01, 1.0, 0.0, 1.0)
+    want = O.controller(lat.device_arrays()[0].cpu().numpy(), lat.device_arrays()[1].cpu().numpy(), 16, cv,
+                        0.85, 0.0, 1.0)
+    assert want.budget == 3 and trace.tobytes() == np.asarray(want.trace).tobytes()
+    assert dt.parent[:4].cpu().tolist() == [-1, 0, 1, 0] and dt.token[:4].cpu().tolist() == [-1, A, C, B]
