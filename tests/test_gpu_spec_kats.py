@@ -107,3 +107,74 @@ def test_k2_spec_controller_trace(P):
                         0.85, 0.0, 1.0)
     assert want.budget == 3 and trace.tobytes() == np.asarray(want.trace).tobytes()
     assert dt.parent[:4].cpu().tolist() == [-1, 0, 1, 0] and dt.token[:4].cpu().tolist() == [-1, A, C, B]
+
+
+class _TableTarget:
+    """Greedy target given as a per-node table: the token it predicts after each node."""
+
+    def __init__(self, table):
+        self.table = table
+
+    def tree_argmax(self, tree, prefix):
+        import torch
+        return torch.tensor(self.table, dtype=torch.int32, device="cuda")
+
+
+def _parent_walk_mask(parents, prefix_len):
+    # independent restatement of the ancestor rule (SPEC.md:469-471): row i sees the prefix,
+    # then itself and its ancestors by walking parent pointers
+    t = len(parents)
+    m = np.zeros((prefix_len + t, prefix_len + t), dtype=bool)
+    m[:prefix_len, :prefix_len] = True  # the prefix block is all-True (sp/verify_sim.py:346-352)
+    for i in range(t):
+        m[prefix_len + i, :prefix_len] = True
+        j = i
+        while j >= 0:
+            m[prefix_len + i, prefix_len + j] = True
+            j = parents[j]
+    return m
+
+
+@pytest.mark.parametrize("prefix_len", [0, 3])
+def test_linearize_spec_six_node_mask(P, prefix_len):
+    # SPEC.md:471: the gamma = 2 / K = 2 six-node tree, mask cell by cell against a parent walk
+    tree = P.best_first_expand(P.top_k_truncate(_block(P), 2), 6)
+    lin = P.linearize(tree, prefix_len)
+    assert lin.parents == (-1, 0, 1, 0, 3, 1, 3) and lin.position_ids == (0, 1, 2, 1, 2, 2, 2)
+    want = _parent_walk_mask(list(lin.parents), prefix_len)
+    blk = slice(prefix_len, None)
+    assert np.array_equal(lin.mask[blk, blk], want[blk, blk])
+    assert lin.mask[blk, :prefix_len].all()
+    assert np.array_equal(lin.mask, want)
+
+
+def test_linearize_spec_chain_and_siblings(P):
+    # SPEC.md:469-470: a depth-2 chain is causal over the tree block; depth-1 siblings see root + self
+    lat = P.top_k_truncate(_block(P), 2)
+    chain = P.beam_expand(lat, 1, 2)
+    m = P.linearize(chain, 0).mask
+    assert np.array_equal(m, np.tril(np.ones((3, 3), dtype=bool)))
+    sib = P.beam_expand(lat, 2, 1)
+    m = P.linearize(sib, 0).mask
+    assert np.array_equal(m, np.array([[1, 0, 0], [1, 1, 0], [1, 0, 1]], dtype=bool))
+
+
+def test_k6_spec_verify_and_commit(P):
+    # SPEC.md:480: a target preferring b then c on the six-node tree -> root -> b -> bc, accepted_len 3;
+    # SPEC.md:478: a first choice that is not a child of the root -> accepted_len 1 (bonus only)
+    tree = P.best_first_expand(P.top_k_truncate(_block(P), 2), 6)
+    lin = P.linearize(tree, 0)
+    table = [0] * 7
+    table[0], table[3], table[4] = B, C, 1
+    rec = P.verify_tree(lin, tree, _TableTarget(table), 0.0)
+    assert rec.accepted_path == (0, 3, 4) and rec.accepted_len == 3 and rec.bonus_token == 1
+    parent = np.array(lin.parents)
+    token = np.array(lin.tokens)
+    wpath, wbonus = O.accept_from_argmax(parent, token, np.array(table))
+    assert list(rec.accepted_path) == wpath and rec.bonus_token == wbonus
+    cache = P.commit(P.SimCache(tokens=(42,)), rec, tree)
+    assert tuple(cache.tokens) == (42, B, C, 1)
+    miss = [8] + [0] * 6
+    rec = P.verify_tree(lin, tree, _TableTarget(miss), 0.0)
+    assert rec.accepted_path == (0,) and rec.accepted_len == 1 and rec.bonus_token == 8
+    assert tuple(P.commit(P.SimCache(tokens=(42,)), rec, tree).tokens) == (42, 8)
