@@ -178,3 +178,50 @@ def test_k6_spec_verify_and_commit(P):
     rec = P.verify_tree(lin, tree, _TableTarget(miss), 0.0)
     assert rec.accepted_path == (0,) and rec.accepted_len == 1 and rec.bonus_token == 8
     assert tuple(P.commit(P.SimCache(tokens=(42,)), rec, tree).tokens) == (42, 8)
+
+
+class _AlignedPair:
+    """alignment 1.0 with a one-hot drafter.  The greedy target emits
+    f(position); the drafter's row j puts all mass on the target's token at j."""
+
+    gamma, vocab = 6, 32
+
+    def __init__(self, P):
+        self.P = P
+
+    @staticmethod
+    def f(pos):
+        return (pos * 7 + 3) % 31
+
+    def drafter_marginals(self, prefix):
+        p = np.zeros((self.gamma, self.vocab))
+        for j in range(self.gamma):
+            p[j, self.f(len(prefix) + j)] = 1.0
+        return self.P.MarginalBlock(gamma=self.gamma, vocab_size=self.vocab, probs=p)
+
+    def next_token(self, prefix, temperature):
+        return self.f(len(prefix))
+
+
+class _AlignedTreePair(_AlignedPair):
+    def tree_argmax(self, tree, prefix):
+        import torch
+        am = [self.f(len(prefix) + len(tree.node_path(n.id))) for n in tree.nodes]
+        return torch.tensor(am, dtype=torch.int32, device="cuda")
+
+
+@pytest.mark.parametrize("cls", [_AlignedPair, _AlignedTreePair])
+@pytest.mark.parametrize("policy", ["adaptive", "fixed-16", "greedy-chain", "beam-2x6"])
+def test_decode_spec_full_acceptance(P, cls, policy):
+    # every cycle commits gamma + 1 tokens and the stream equals AR decoding (SPEC.md:496, :510)
+    pair = cls(P)
+    params = P.CostModelParams(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=151936, bp=2,
+                               peak_flops=1.6e15, bandwidth=6.5e12)
+    est = P.VerifyLatencyEstimator(params, variant="static")
+    lat = P.CycleLatencies(5e-4, 1e-4, 3e-3)
+    cfg = P.SimConfig(controller=P.ControllerConfig(n_max=64, latencies=lat, variant="static", context_len=2048),
+                      run_length=70, top_k=4)
+    records, tokens = P.decode_full(pair, cfg, P.Policy.parse(policy), est)
+    assert all(r.accepted_len == pair.gamma + 1 for r in records)
+    assert list(tokens) == [pair.f(i) for i in range(len(tokens))] and len(tokens) >= 70
+    assert len(records) == -(-70 // (pair.gamma + 1))

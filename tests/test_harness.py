@@ -63,3 +63,19 @@ def test_committed_b200_profile_and_calibration():
     report = root / "r2_qwen3_8b_b200_calibration.txt"
     if trace.exists() and report.exists():
         assert H.calibrate(root / "qwen3_8b_b200.txt", trace).render() == report.read_text()
+
+
+def test_realized_speedup_spec_kats():
+    # 1 token per cycle at cycle time l_ar -> 1.0; 5 tokens at 2 l_ar -> 2.5; empty -> error
+    import pytest
+
+    import paper_2605_29727_b200 as P
+
+    def rec(acc, t):
+        return P.CycleRecord(tree_size=1, accepted_len=acc, surrogate=1.0, t_draft=t / 2, t_verify=t / 2, t_aux=0.0,
+                             l_ar=0.01, cycle_speedup=acc * 0.01 / t)
+
+    assert P.realized_speedup([rec(1, 0.01)] * 4) == pytest.approx(1.0, rel=1e-15)
+    assert P.realized_speedup([rec(5, 0.02)] * 3) == pytest.approx(2.5, rel=1e-15)
+    with pytest.raises(ValueError):
+        P.realized_speedup([])
