@@ -225,3 +225,49 @@ def test_decode_spec_full_acceptance(P, cls, policy):
     assert all(r.accepted_len == pair.gamma + 1 for r in records)
     assert list(tokens) == [pair.f(i) for i in range(len(tokens))] and len(tokens) >= 70
     assert len(records) == -(-70 // (pair.gamma + 1))
+
+
+def _edge_blocks():
+    rng = np.random.default_rng(7)
+    out = []
+    out.append(("v2_g1", np.array([[0.5, 0.5]])))                         # smallest shape, an exact tie
+    out.append(("uniform", np.full((3, 16), 1 / 16)))                    # all ties: token-ascending
+    z = np.zeros((4, 12))
+    z[:, :3] = [0.5, 0.3, 0.2]                                            # zero-probability tail
+    out.append(("zeros", z))
+    oh = np.zeros((5, 8))
+    oh[np.arange(5), rng.integers(0, 8, 5)] = 1.0                        # one-hot rows: a chain only
+    out.append(("onehot", oh))
+    q = np.round(rng.dirichlet(np.full(24, 0.3), size=6) * 64) + 1        # quantised: many rho ties
+    out.append(("quantised", q / q.sum(1, keepdims=True)))
+    return out
+
+
+@pytest.mark.parametrize("name,probs", _edge_blocks(), ids=[n for n, _ in _edge_blocks()])
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_edge_lattices_match_oracle(P, name, probs, k):
+    k = min(k, probs.shape[1])
+    block = P.MarginalBlock(gamma=probs.shape[0], vocab_size=probs.shape[1], probs=probs)
+    lat = P.top_k_truncate(block, k)
+    otok, oprob = O.topk_rows(probs, k)
+    assert [[t for t, _ in r] for r in lat.entries] == otok.tolist()
+    assert np.array([[p for _, p in r] for r in lat.entries]).tobytes() == oprob.tobytes()
+    for n in (1, 3, 50):
+        parent, token, rho = _nodes(P.best_first_expand(lat, n))
+        want = O.best_first(otok, oprob, n)
+        assert parent == want.parent.tolist() and token == want.token.tolist()
+        assert rho.tobytes() == want.rho[1:].tobytes()
+    params = P.CostModelParams(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288, V=151936, bp=2,
+                               peak_flops=1.6e15, bandwidth=6.5e12)
+    est = P.VerifyLatencyEstimator(params, variant="static")
+    for n_max, fixed in ((64, 1e-4), (64, 1e-1)):   # cheap and expensive fixed cost: short / long trees
+        cfg = P.ControllerConfig(n_max=n_max, latencies=P.CycleLatencies(fixed, 0.0, 3e-3), variant="static",
+                                 context_len=2048)
+        d = P.run_cycle(lat, cfg, est)
+        want = O.controller(otok, oprob, n_max, O.curve_for(O.Dims(L=36, h=4096, n_q=32, n_kv=8, d=128, h_ffn=12288,
+                                                                   V=151936, bp=2, peak_flops=1.6e15,
+                                                                   bandwidth=6.5e12), 2048), fixed, 0.0, 3e-3)
+        assert d.budget == want.budget and np.array(d.s_hat_trace).tobytes() == np.asarray(want.trace).tobytes()
+        assert d.stop_reason == O.STOP_NAMES[want.stop]
+        parent, token, _ = _nodes(d.tree)
+        assert parent == want.tree.parent.tolist() and token == want.tree.token.tolist()
